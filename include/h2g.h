@@ -1,0 +1,111 @@
+/* h2g — C-ABI of the B200-native dependency-free H2-ULV hot path.
+ *
+ * Plain pointers and sizes only; an opaque handle owns all device memory.
+ * Each entry point replaces one piece of the reference's C++ API
+ * (/root/reference/proj/include/h2ulv), cited per function. Every function
+ * returns 0 on success or nonzero with h2g_last_error() set to the
+ * reference's error message (e.g. "singular block in LU of S^RR at step 3",
+ * "basis does not absorb fill-in at level 5 block (2,7)").
+ * Host/device: pointers are host memory unless the *_dev variant is used.
+ * There is no CPU fallback: every call runs sm_100a kernels and fails when no
+ * CUDA device is present.
+ */
+#ifndef H2G_H
+#define H2G_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct h2g_problem h2g_problem;
+
+/* KernelSpec (kernels.hpp:15-23): kind 0 = Laplace, 1 = Yukawa. */
+typedef struct {
+  int32_t kind;
+  double alpha_m;
+  double permittivity_scale;
+  double eta_reg;
+} h2g_kernel;
+
+/* FactorOptions (ulv.hpp:29-45) + AdmissibilityRule (geometry.hpp:60-67). */
+typedef struct {
+  double tol;                   /* RankDecision tol (default 1e-8) */
+  int64_t cap;                  /* <= 0: no cap */
+  double rr_pivot_tol;          /* 1e-13 */
+  int32_t absorb_coupling;      /* 1 */
+  double abort_residual_factor; /* 100 */
+  int32_t structure;            /* 0 = h2 (strong, nodep), 1 = hss (weak) */
+  double eta;                   /* strong admissibility eta (1.0) */
+  int64_t qr_mem_budget;        /* bytes of QR working memory per chunk, <= 0: default */
+} h2g_options;
+
+const char* h2g_last_error(void);
+int h2g_version(void);
+
+/* Handle lifetime: replaces constructing Pipeline (report.hpp:73-99). */
+int h2g_create(h2g_problem** out);
+void h2g_destroy(h2g_problem* p);
+int h2g_set_kernel(h2g_problem* p, const h2g_kernel* k);
+int h2g_set_options(h2g_problem* p, const h2g_options* o);
+
+/* build_cluster_tree (geometry.hpp:58) + classify_blocks (hstructure.hpp:55)
+ * + materialize_dense (hstructure.hpp:101-103) = Pipeline::build
+ * (report.cpp:79-91). xyz is AoS n x 3, q has n charges. */
+int h2g_build(h2g_problem* p, int64_t n, const double* xyz, const double* q, int64_t leaf);
+int h2g_build_dev(h2g_problem* p, int64_t n, const double* d_xyz, const double* d_q, int64_t leaf);
+
+/* prepare_factor_inputs + factorize = build_and_factorize (ulv.hpp:121-123),
+ * Pipeline::factor (report.cpp:93-106). */
+int h2g_factor(h2g_problem* p);
+
+/* solve (solve.hpp:10): b, x are n x nrhs column-major in the ORIGINAL order. */
+int h2g_solve(h2g_problem* p, int64_t nrhs, const double* b, double* x);
+int h2g_solve_dev(h2g_problem* p, int64_t nrhs, const double* d_b, double* d_x);
+
+/* ---- inspection (ClusterTree / BlockStructure / HMatrix / ULVFactors) ---- */
+int h2g_levels(h2g_problem* p);
+int h2g_tree_perm(h2g_problem* p, int64_t* original_index);          /* geometry.hpp:40 */
+int h2g_nodes(h2g_problem* p, int64_t* begin_end, double* center_radius); /* heap order */
+int h2g_reordered_points(h2g_problem* p, double* xyz, double* q);
+int64_t h2g_list_count(h2g_problem* p, int level, int far);
+int h2g_list(h2g_problem* p, int level, int far, int64_t* ptr, int64_t* idx); /* hstructure.hpp:41-42 */
+int64_t h2g_near_entries(h2g_problem* p);
+int h2g_near_dense(h2g_problem* p, double* out); /* HMatrix::leaf_dense, row-major over blocks */
+int h2g_num_factor_levels(h2g_problem* p);
+int h2g_factor_level(h2g_problem* p, int li, int64_t* ranks); /* returns tree level */
+int64_t h2g_cutoff(h2g_problem* p, int64_t* dims);           /* count | level << 32 */
+int64_t h2g_top_n(h2g_problem* p);
+int h2g_top(h2g_problem* p, double* lu, int64_t* perm);      /* ULVFactors::top */
+int64_t h2g_basis(h2g_problem* p, int level, int64_t k, int side, double* sq); /* dim | rank<<32 */
+double h2g_max_fill_residual(h2g_problem* p);
+
+/* Timings [tree, classify, near, factor, solve] (s); counted flops
+ * [fill_precompute, basis, skeleton, factorize, assemble, solve] following the
+ * reference ledger rules (flops.hpp); launches = kernels launched so far. */
+int h2g_stats(h2g_problem* p, double* t5, double* f6, int64_t* launches);
+
+/* Matrix-free direct-summation product y = A x on the ORIGINAL ordering
+ * (replaces matvec_dense_oracle, solve.cpp:234-239, without its N guard). */
+int h2g_matvec(h2g_problem* p, int64_t nrhs, const double* x, double* y);
+
+/* ---- single-primitive entry points (kernel parity tests) ---- */
+/* lu_factor (linalg.cpp:352-388) on one n x n column-major block. */
+int h2g_lu_factor(int64_t n, const double* a, double tol, double* lu, int64_t* perm);
+/* basis_from_members (compression.cpp:111-146): concat dim x width column-major,
+ * nmem members with offsets; writes square [Qr | Qs] (dim x dim) and rank. */
+int h2g_basis_from_members(int64_t dim, int64_t width, const double* concat, int64_t nmem,
+                           const int64_t* offsets, double tol, int64_t cap, int64_t min_rank,
+                           double* sq, int64_t* rank);
+/* LuFactors solve family (linalg.cpp:404-559) with the given packed factors:
+ * kind 0 solve, 1 lower, 2 upper, 3 transpose, 4 right, 5 upper_right. */
+int h2g_lu_solve(int64_t n, const double* lu, const int64_t* perm, int kind, int64_t rows,
+                 int64_t cols, double* x);
+/* gemm (linalg.cpp:86-116): C = alpha op(A) op(B) (+ C when acc). */
+int h2g_gemm(int64_t m, int64_t n, int64_t k, double alpha, const double* a, int transa,
+             const double* b, int transb, int acc, double* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

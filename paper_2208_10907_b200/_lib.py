@@ -1,0 +1,274 @@
+"""ctypes binding of include/h2g.h (libh2g.so, built in-tree by `make`)."""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libh2g.so")
+_lib = None
+
+i64 = ctypes.c_int64
+f64 = ctypes.c_double
+P = ctypes.c_void_p
+
+
+class H2GError(RuntimeError):
+    """Raised with the reference's error message (h2g_last_error)."""
+
+
+class Kernel(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("alpha_m", f64), ("permittivity_scale", f64),
+                ("eta_reg", f64)]
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("tol", f64), ("cap", i64), ("rr_pivot_tol", f64), ("absorb_coupling", ctypes.c_int32),
+                ("abort_residual_factor", f64), ("structure", ctypes.c_int32), ("eta", f64),
+                ("qr_mem_budget", i64)]
+
+
+EXPORTS = [
+    "h2g_last_error", "h2g_version", "h2g_create", "h2g_destroy", "h2g_set_kernel",
+    "h2g_set_options", "h2g_build", "h2g_build_dev", "h2g_factor", "h2g_solve", "h2g_solve_dev",
+    "h2g_levels", "h2g_tree_perm", "h2g_nodes", "h2g_reordered_points", "h2g_list_count",
+    "h2g_list", "h2g_near_entries", "h2g_near_dense", "h2g_num_factor_levels",
+    "h2g_factor_level", "h2g_cutoff", "h2g_top_n", "h2g_top", "h2g_basis",
+    "h2g_max_fill_residual", "h2g_stats", "h2g_matvec", "h2g_lu_factor",
+    "h2g_basis_from_members", "h2g_lu_solve", "h2g_gemm",
+]
+
+
+def lib():
+    """Load libh2g.so; raise loudly if it was not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(lib_path):
+            raise H2GError(f"libh2g.so not built at {lib_path}; run `make -C paper_2208_10907_b200`")
+        L = ctypes.CDLL(lib_path)
+        L.h2g_last_error.restype = ctypes.c_char_p
+        L.h2g_create.argtypes = [ctypes.POINTER(P)]
+        L.h2g_destroy.argtypes = [P]
+        L.h2g_set_kernel.argtypes = [P, ctypes.POINTER(Kernel)]
+        L.h2g_set_options.argtypes = [P, ctypes.POINTER(Options)]
+        L.h2g_build.argtypes = [P, i64, P, P, i64]
+        L.h2g_build_dev.argtypes = [P, i64, P, P, i64]
+        L.h2g_factor.argtypes = [P]
+        L.h2g_solve.argtypes = [P, i64, P, P]
+        L.h2g_solve_dev.argtypes = [P, i64, P, P]
+        L.h2g_levels.argtypes = [P]
+        L.h2g_tree_perm.argtypes = [P, P]
+        L.h2g_nodes.argtypes = [P, P, P]
+        L.h2g_reordered_points.argtypes = [P, P, P]
+        L.h2g_list_count.argtypes = [P, ctypes.c_int, ctypes.c_int]
+        L.h2g_list_count.restype = i64
+        L.h2g_list.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P]
+        L.h2g_near_entries.argtypes = [P]
+        L.h2g_near_entries.restype = i64
+        L.h2g_near_dense.argtypes = [P, P]
+        L.h2g_num_factor_levels.argtypes = [P]
+        L.h2g_factor_level.argtypes = [P, ctypes.c_int, P]
+        L.h2g_cutoff.argtypes = [P, P]
+        L.h2g_cutoff.restype = i64
+        L.h2g_top_n.argtypes = [P]
+        L.h2g_top_n.restype = i64
+        L.h2g_top.argtypes = [P, P, P]
+        L.h2g_basis.argtypes = [P, ctypes.c_int, i64, ctypes.c_int, P]
+        L.h2g_basis.restype = i64
+        L.h2g_max_fill_residual.argtypes = [P]
+        L.h2g_max_fill_residual.restype = f64
+        L.h2g_stats.argtypes = [P, P, P, P]
+        L.h2g_matvec.argtypes = [P, i64, P, P]
+        L.h2g_lu_factor.argtypes = [i64, P, f64, P, P]
+        L.h2g_basis_from_members.argtypes = [i64, i64, P, i64, P, f64, i64, i64, P, P]
+        L.h2g_lu_solve.argtypes = [i64, P, P, ctypes.c_int, i64, i64, P]
+        L.h2g_gemm.argtypes = [i64, i64, i64, f64, P, ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P]
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _check(rc):
+    if rc != 0:
+        raise H2GError(lib().h2g_last_error().decode())
+
+
+class Problem:
+    """One device-resident H2 problem: tree, structure, near field, factors."""
+
+    def __init__(self):
+        L = lib()
+        h = P()
+        _check(L.h2g_create(ctypes.byref(h)))
+        self.L = L
+        self.h = h
+        self.n = 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.h2g_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def set_kernel(self, kind="laplace", alpha_m=0.0, scale=4 * np.pi, reg=0.0):
+        k = Kernel(0 if kind == "laplace" else 1, alpha_m, scale, reg)
+        _check(self.L.h2g_set_kernel(self.h, ctypes.byref(k)))
+
+    def set_options(self, tol=1e-8, cap=None, rr_pivot_tol=1e-13, absorb_coupling=True,
+                    abort_residual_factor=100.0, structure="h2", eta=1.0, qr_mem_budget=0):
+        o = Options(tol, cap or 0, rr_pivot_tol, 1 if absorb_coupling else 0, abort_residual_factor,
+                    {"h2": 0, "hss": 1}[structure], eta, qr_mem_budget)
+        _check(self.L.h2g_set_options(self.h, ctypes.byref(o)))
+
+    def build(self, xyz, q, leaf):
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+        q = np.ascontiguousarray(q, dtype=np.float64)
+        self.n = len(q)
+        _check(self.L.h2g_build(self.h, self.n, _p(xyz), _p(q), leaf))
+
+    def build_dev(self, xyz_ptr, q_ptr, n, leaf):
+        self.n = n
+        _check(self.L.h2g_build_dev(self.h, n, xyz_ptr, q_ptr, leaf))
+
+    def factor(self):
+        _check(self.L.h2g_factor(self.h))
+
+    def solve(self, b):
+        b = np.asfortranarray(b, dtype=np.float64)
+        nrhs = 1 if b.ndim == 1 else b.shape[1]
+        x = np.zeros_like(b)
+        _check(self.L.h2g_solve(self.h, nrhs, _p(b), _p(x)))
+        return x
+
+    def solve_dev(self, b_ptr, x_ptr, nrhs=1):
+        _check(self.L.h2g_solve_dev(self.h, nrhs, b_ptr, x_ptr))
+
+    def matvec(self, x):
+        x = np.asfortranarray(x, dtype=np.float64)
+        nrhs = 1 if x.ndim == 1 else x.shape[1]
+        y = np.zeros_like(x)
+        _check(self.L.h2g_matvec(self.h, nrhs, _p(x), _p(y)))
+        return y
+
+    # ---- inspection ----
+    @property
+    def levels(self):
+        return self.L.h2g_levels(self.h)
+
+    def perm(self):
+        out = np.zeros(self.n, dtype=np.int64)
+        _check(self.L.h2g_tree_perm(self.h, _p(out)))
+        return out
+
+    def nodes(self):
+        nn = (1 << (self.levels + 1)) - 1
+        be = np.zeros((nn, 2), dtype=np.int64)
+        geo = np.zeros((nn, 4))
+        _check(self.L.h2g_nodes(self.h, _p(be), _p(geo)))
+        return be, geo
+
+    def reordered(self):
+        xyz = np.zeros((self.n, 3))
+        q = np.zeros(self.n)
+        _check(self.L.h2g_reordered_points(self.h, _p(xyz), _p(q)))
+        return xyz, q
+
+    def lists(self, lvl, far):
+        cnt = self.L.h2g_list_count(self.h, lvl, 1 if far else 0)
+        ptr = np.zeros((1 << lvl) + 1, dtype=np.int64)
+        idx = np.zeros(max(cnt, 1), dtype=np.int64)
+        _check(self.L.h2g_list(self.h, lvl, 1 if far else 0, _p(ptr), _p(idx)))
+        return ptr, idx[:cnt]
+
+    def leaf_dense(self):
+        out = np.zeros(self.L.h2g_near_entries(self.h))
+        _check(self.L.h2g_near_dense(self.h, _p(out)))
+        return out
+
+    def factor_levels(self):
+        out = []
+        for li in range(self.L.h2g_num_factor_levels(self.h)):
+            ranks = np.zeros(1 << self.levels, dtype=np.int64)
+            lvl = self.L.h2g_factor_level(self.h, li, _p(ranks))
+            out.append((lvl, ranks[: 1 << lvl].copy()))
+        return out
+
+    def cutoff(self):
+        dims = np.zeros(1 << self.levels, dtype=np.int64)
+        v = self.L.h2g_cutoff(self.h, _p(dims))
+        return v >> 32, dims[: v & 0xFFFFFFFF].copy()
+
+    def top(self):
+        n = self.L.h2g_top_n(self.h)
+        lu = np.zeros((n, n), order="F")
+        perm = np.zeros(n, dtype=np.int64)
+        _check(self.L.h2g_top(self.h, _p(lu), _p(perm)))
+        return lu, perm
+
+    def basis(self, lvl, k, side):
+        v = self.L.h2g_basis(self.h, lvl, k, side, None)
+        dim, rank = v & 0xFFFFFFFF, v >> 32
+        out = np.zeros((dim, dim), order="F")
+        if dim:
+            self.L.h2g_basis(self.h, lvl, k, side, _p(out))
+        return out, rank
+
+    def max_fill_residual(self):
+        return self.L.h2g_max_fill_residual(self.h)
+
+    def stats(self):
+        t = np.zeros(5)
+        f = np.zeros(6)
+        n = ctypes.c_int64(0)
+        self.L.h2g_stats(self.h, _p(t), _p(f), ctypes.byref(n))
+        return dict(t_tree=t[0], t_classify=t[1], t_near=t[2], t_factor=t[3], t_solve=t[4],
+                    flops_fills=f[0], flops_basis=f[1], flops_skeleton=f[2], flops_factorize=f[3],
+                    flops_assemble=f[4], flops_solve=f[5], launches=n.value)
+
+
+# ---- single primitives ---------------------------------------------------
+def lu_factor(a, tol=1e-14):
+    a = np.asfortranarray(a, dtype=np.float64)
+    n = a.shape[0]
+    lu = np.zeros((n, n), order="F")
+    perm = np.zeros(n, dtype=np.int64)
+    _check(lib().h2g_lu_factor(n, _p(a), tol, _p(lu), _p(perm)))
+    return lu, perm
+
+
+def lu_solve(lu, perm, x, kind):
+    lu = np.asfortranarray(lu, dtype=np.float64)
+    perm = np.ascontiguousarray(perm, dtype=np.int64)
+    x = np.array(x, dtype=np.float64, order="F")
+    kinds = {"solve": 0, "lower": 1, "upper": 2, "transpose": 3, "right": 4, "upper_right": 5}
+    _check(lib().h2g_lu_solve(lu.shape[0], _p(lu), _p(perm), kinds[kind], x.shape[0], x.shape[1],
+                              _p(x)))
+    return x
+
+
+def gemm(a, b, alpha=1.0, transa=False, transb=False, c=None):
+    a = np.asfortranarray(a, dtype=np.float64)
+    b = np.asfortranarray(b, dtype=np.float64)
+    m = a.shape[1] if transa else a.shape[0]
+    k = a.shape[0] if transa else a.shape[1]
+    n = b.shape[0] if transb else b.shape[1]
+    acc = c is not None
+    out = np.array(c, dtype=np.float64, order="F") if acc else np.zeros((m, n), order="F")
+    _check(lib().h2g_gemm(m, n, k, alpha, _p(a), int(transa), _p(b), int(transb), int(acc), _p(out)))
+    return out
+
+
+def basis_from_members(concat, offsets, tol, cap=None, min_rank=0):
+    concat = np.asfortranarray(concat, dtype=np.float64)
+    dim = concat.shape[0]
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    sq = np.zeros((dim, dim), order="F")
+    rank = np.zeros(1, dtype=np.int64)
+    _check(lib().h2g_basis_from_members(dim, concat.shape[1], _p(concat), len(offsets) - 1,
+                                        _p(offsets), tol, cap or 0, min_rank, _p(sq), _p(rank)))
+    return sq, int(rank[0])

@@ -1,0 +1,328 @@
+// extern "C" boundary (include/h2g.h). Converts C++ exceptions into status
+// codes + h2g_last_error(), copies host buffers in/out, and exposes the
+// factor objects for inspection and parity tests.
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/h2g.h"
+#include "h2.hpp"
+
+struct h2g_problem {
+  h2g::Problem P;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  } catch (...) {
+    g_err = "unknown error";
+    return 1;
+  }
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  explicit DevBuf(size_t bytes) { h2g::cuda_check(cudaMalloc(&p, bytes ? bytes : 8), "cudaMalloc"); }
+  ~DevBuf() { cudaFree(p); }
+  double* d() { return static_cast<double*>(p); }
+};
+
+void require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw std::runtime_error("h2g: no CUDA device (the B200 path has no CPU fallback)");
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* h2g_last_error(void) { return g_err.c_str(); }
+int h2g_version(void) { return 1; }
+
+int h2g_create(h2g_problem** out) {
+  return guarded([&] {
+    require_device();
+    *out = new h2g_problem();
+  });
+}
+
+void h2g_destroy(h2g_problem* p) { delete p; }
+
+int h2g_set_kernel(h2g_problem* p, const h2g_kernel* k) {
+  return guarded([&] {
+    h2g::KernelParams kp;
+    kp.kind = k->kind;
+    kp.alpha_m = k->alpha_m;
+    kp.scale = k->permittivity_scale;
+    kp.reg = k->eta_reg;
+    p->P.set_kernel(kp);
+  });
+}
+
+int h2g_set_options(h2g_problem* p, const h2g_options* o) {
+  return guarded([&] {
+    if (o->tol <= 0) throw std::invalid_argument("config: tol must be positive");
+    if (o->eta <= 0) throw std::invalid_argument("config: eta must be positive");
+    auto& op = p->P.opt;
+    op.tol = o->tol;
+    op.cap = o->cap > 0 ? int(o->cap) : 0;
+    op.rr_pivot_tol = o->rr_pivot_tol;
+    op.absorb_coupling = o->absorb_coupling != 0;
+    op.abort_residual_factor = o->abort_residual_factor;
+    op.structure = o->structure;
+    op.eta = o->eta;
+    if (o->qr_mem_budget > 0) op.qr_mem_budget = size_t(o->qr_mem_budget);
+  });
+}
+
+int h2g_build_dev(h2g_problem* p, int64_t n, const double* d_xyz, const double* d_q, int64_t leaf) {
+  return guarded([&] { p->P.build(d_xyz, d_q, n, leaf); });
+}
+
+int h2g_build(h2g_problem* p, int64_t n, const double* xyz, const double* q, int64_t leaf) {
+  return guarded([&] {
+    DevBuf a(sizeof(double) * 3 * n), b(sizeof(double) * n);
+    h2g::cuda_check(cudaMemcpy(a.p, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice), "h2d");
+    h2g::cuda_check(cudaMemcpy(b.p, q, sizeof(double) * n, cudaMemcpyHostToDevice), "h2d");
+    p->P.build(a.d(), b.d(), n, leaf);
+  });
+}
+
+int h2g_factor(h2g_problem* p) {
+  return guarded([&] { p->P.factor(); });
+}
+
+int h2g_solve_dev(h2g_problem* p, int64_t nrhs, const double* d_b, double* d_x) {
+  return guarded([&] { p->P.solve(d_b, d_x, int(nrhs)); });
+}
+
+int h2g_solve(h2g_problem* p, int64_t nrhs, const double* b, double* x) {
+  return guarded([&] {
+    const size_t bytes = sizeof(double) * size_t(p->P.T.n) * nrhs;
+    DevBuf db(bytes), dx(bytes);
+    h2g::cuda_check(cudaMemcpy(db.p, b, bytes, cudaMemcpyHostToDevice), "h2d");
+    p->P.solve(db.d(), dx.d(), int(nrhs));
+    h2g::cuda_check(cudaMemcpy(x, dx.p, bytes, cudaMemcpyDeviceToHost), "d2h");
+  });
+}
+
+int h2g_matvec(h2g_problem* p, int64_t nrhs, const double* x, double* y) {
+  return guarded([&] {
+    const size_t bytes = sizeof(double) * size_t(p->P.T.n) * nrhs;
+    DevBuf dx(bytes), dy(bytes);
+    h2g::cuda_check(cudaMemcpy(dx.p, x, bytes, cudaMemcpyHostToDevice), "h2d");
+    p->P.matvec(dx.d(), dy.d(), int(nrhs));
+    h2g::cuda_check(cudaMemcpy(y, dy.p, bytes, cudaMemcpyDeviceToHost), "d2h");
+  });
+}
+
+int h2g_levels(h2g_problem* p) { return p->P.T.levels; }
+
+int h2g_tree_perm(h2g_problem* p, int64_t* out) {
+  return guarded([&] {
+    h2g::cuda_check(cudaMemcpy(out, p->P.T.order, sizeof(int64_t) * p->P.T.n, cudaMemcpyDeviceToHost), "d2h");
+  });
+}
+
+int h2g_nodes(h2g_problem* p, int64_t* be, double* geo) {
+  return guarded([&] {
+    const int64_t nn = (int64_t(1) << (p->P.T.levels + 1)) - 1;
+    std::memcpy(be, p->P.be.data(), sizeof(int64_t) * 2 * nn);
+    h2g::cuda_check(cudaMemcpy(geo, p->P.T.geo, sizeof(double) * 4 * nn, cudaMemcpyDeviceToHost), "d2h");
+  });
+}
+
+int h2g_reordered_points(h2g_problem* p, double* xyz, double* q) {
+  return guarded([&] {
+    const int64_t n = p->P.T.n;
+    std::vector<double> x(n), y(n), z(n);
+    h2g::cuda_check(cudaMemcpy(x.data(), p->P.T.x, 8 * n, cudaMemcpyDeviceToHost), "d2h");
+    h2g::cuda_check(cudaMemcpy(y.data(), p->P.T.y, 8 * n, cudaMemcpyDeviceToHost), "d2h");
+    h2g::cuda_check(cudaMemcpy(z.data(), p->P.T.z, 8 * n, cudaMemcpyDeviceToHost), "d2h");
+    h2g::cuda_check(cudaMemcpy(q, p->P.T.q, 8 * n, cudaMemcpyDeviceToHost), "d2h");
+    for (int64_t i = 0; i < n; ++i) {
+      xyz[3 * i] = x[i];
+      xyz[3 * i + 1] = y[i];
+      xyz[3 * i + 2] = z[i];
+    }
+  });
+}
+
+int64_t h2g_list_count(h2g_problem* p, int level, int far) {
+  const auto& L = p->P.S.level[level];
+  return int64_t(far ? L.far_idx.size() : L.near_idx.size());
+}
+
+int h2g_list(h2g_problem* p, int level, int far, int64_t* ptr, int64_t* idx) {
+  return guarded([&] {
+    const auto& L = p->P.S.level[level];
+    const auto& pv = far ? L.far_ptr : L.near_ptr;
+    const auto& iv = far ? L.far_idx : L.near_idx;
+    std::memcpy(ptr, pv.data(), sizeof(int64_t) * pv.size());
+    if (!iv.empty()) std::memcpy(idx, iv.data(), sizeof(int64_t) * iv.size());
+  });
+}
+
+int64_t h2g_near_entries(h2g_problem* p) {
+  int64_t s = 0;
+  for (auto& b : p->P.near) s += b.m.size();
+  return s;
+}
+
+int h2g_near_dense(h2g_problem* p, double* out) {
+  return guarded([&] {
+    int64_t at = 0;
+    for (auto& b : p->P.near) {
+      h2g::cuda_check(cudaMemcpy(out + at, b.m.p, sizeof(double) * b.m.size(), cudaMemcpyDeviceToHost), "d2h");
+      at += b.m.size();
+    }
+  });
+}
+
+int h2g_num_factor_levels(h2g_problem* p) { return int(p->P.levels.size()); }
+
+int h2g_factor_level(h2g_problem* p, int li, int64_t* ranks) {
+  const auto& lf = p->P.levels.at(li);
+  for (size_t k = 0; k < lf.ranks.size(); ++k) ranks[k] = lf.ranks[k];
+  return lf.level;
+}
+
+int64_t h2g_cutoff(h2g_problem* p, int64_t* dims) {
+  for (size_t k = 0; k < p->P.cutoff_dims.size(); ++k) dims[k] = p->P.cutoff_dims[k];
+  return int64_t(p->P.cutoff_dims.size()) | (int64_t(p->P.cutoff_level) << 32);
+}
+
+int64_t h2g_top_n(h2g_problem* p) { return p->P.top.n(); }
+
+int h2g_top(h2g_problem* p, double* lu, int64_t* perm) {
+  return guarded([&] {
+    const int64_t n = p->P.top.n();
+    h2g::cuda_check(cudaMemcpy(lu, p->P.top.lu.m.p, sizeof(double) * n * n, cudaMemcpyDeviceToHost), "d2h");
+    h2g::cuda_check(cudaMemcpy(perm, p->P.top.perm, sizeof(int64_t) * n, cudaMemcpyDeviceToHost), "d2h");
+  });
+}
+
+int64_t h2g_basis(h2g_problem* p, int level, int64_t k, int side, double* sq) {
+  const auto& B = side == 0 ? p->P.U.at(level).at(k) : p->P.V.at(level).at(k);
+  if (sq && B.dim > 0)
+    cudaMemcpy(sq, B.SQ.m.p, sizeof(double) * B.dim * B.dim, cudaMemcpyDeviceToHost);
+  return int64_t(B.dim) | (int64_t(B.rank) << 32);
+}
+
+double h2g_max_fill_residual(h2g_problem* p) { return p->P.stats.max_fill_residual; }
+
+int h2g_stats(h2g_problem* p, double* t5, double* f6, int64_t* launches) {
+  const auto& s = p->P.stats;
+  t5[0] = s.t_tree;
+  t5[1] = s.t_classify;
+  t5[2] = s.t_near;
+  t5[3] = s.t_factor;
+  t5[4] = s.t_solve;
+  auto get = [&](const char* k) {
+    auto it = p->P.c.phase_flops.find(k);
+    return it == p->P.c.phase_flops.end() ? 0.0 : it->second;
+  };
+  f6[0] = get("fill_precompute");
+  f6[1] = get("basis");
+  f6[2] = get("skeleton");
+  f6[3] = get("factorize");
+  f6[4] = get("assemble");
+  f6[5] = get("solve");
+  *launches = p->P.c.launches;
+  return 0;
+}
+
+// ---- single primitives ---------------------------------------------------
+int h2g_lu_factor(int64_t n, const double* a, double tol, double* lu, int64_t* perm) {
+  return guarded([&] {
+    require_device();
+    h2g::Problem P;
+    auto f = h2g::alloc_lu(P.c, int(n));
+    h2g::cuda_check(cudaMemcpy(f.lu.m.p, a, sizeof(double) * n * n, cudaMemcpyHostToDevice), "h2d");
+    h2g::LuBatch lb;
+    lb.add(f, tol, "block");
+    lb.run(P.c);
+    h2g::cuda_check(cudaMemcpy(lu, f.lu.m.p, sizeof(double) * n * n, cudaMemcpyDeviceToHost), "d2h");
+    h2g::cuda_check(cudaMemcpy(perm, f.perm, sizeof(int64_t) * n, cudaMemcpyDeviceToHost), "d2h");
+  });
+}
+
+int h2g_lu_solve(int64_t n, const double* lu, const int64_t* perm, int kind, int64_t rows,
+                 int64_t cols, double* x) {
+  return guarded([&] {
+    require_device();
+    h2g::Problem P;
+    auto f = h2g::alloc_lu(P.c, int(n));
+    auto X = h2g::alloc_mat(P.c, int(rows), int(cols));
+    h2g::cuda_check(cudaMemcpy(f.lu.m.p, lu, sizeof(double) * n * n, cudaMemcpyHostToDevice), "h2d");
+    h2g::cuda_check(cudaMemcpy(f.perm, perm, sizeof(int64_t) * n, cudaMemcpyHostToDevice), "h2d");
+    h2g::cuda_check(cudaMemcpy(X.m.p, x, sizeof(double) * rows * cols, cudaMemcpyHostToDevice), "h2d");
+    h2g::SolveBatch sb;
+    sb.add(f, X.m, kind);
+    sb.run(P.c);
+    P.c.sync();
+    h2g::cuda_check(cudaMemcpy(x, X.m.p, sizeof(double) * rows * cols, cudaMemcpyDeviceToHost), "d2h");
+  });
+}
+
+int h2g_gemm(int64_t m, int64_t n, int64_t k, double alpha, const double* a, int transa,
+             const double* b, int transb, int acc, double* c) {
+  return guarded([&] {
+    require_device();
+    h2g::Problem P;
+    const int ar = transa ? int(k) : int(m), ac = transa ? int(m) : int(k);
+    const int br = transb ? int(n) : int(k), bc = transb ? int(k) : int(n);
+    auto A = h2g::alloc_mat(P.c, ar, ac), B = h2g::alloc_mat(P.c, br, bc), C = h2g::alloc_mat(P.c, int(m), int(n));
+    h2g::cuda_check(cudaMemcpy(A.m.p, a, sizeof(double) * ar * ac, cudaMemcpyHostToDevice), "h2d");
+    h2g::cuda_check(cudaMemcpy(B.m.p, b, sizeof(double) * br * bc, cudaMemcpyHostToDevice), "h2d");
+    h2g::cuda_check(cudaMemcpy(C.m.p, c, sizeof(double) * m * n, cudaMemcpyHostToDevice), "h2d");
+    h2g::GemmBatch gb;
+    gb.job(C.m, acc != 0);
+    gb.seg(transa ? A.m.t() : A.m, transb ? B.m.t() : B.m, alpha);
+    gb.run(P.c);
+    P.c.sync();
+    h2g::cuda_check(cudaMemcpy(c, C.m.p, sizeof(double) * m * n, cudaMemcpyDeviceToHost), "d2h");
+  });
+}
+
+int h2g_basis_from_members(int64_t dim, int64_t width, const double* concat, int64_t nmem,
+                           const int64_t* offsets, double tol, int64_t cap, int64_t min_rank,
+                           double* sq, int64_t* rank) {
+  return guarded([&] {
+    require_device();
+    h2g::Problem P;
+    auto Cm = h2g::alloc_mat(P.c, int(dim), int(width > 0 ? width : 1));
+    if (width > 0)
+      h2g::cuda_check(cudaMemcpy(Cm.m.p, concat, sizeof(double) * dim * width, cudaMemcpyHostToDevice), "h2d");
+    Cm.m.cols = int(width);
+    h2g::QrBatch qb;
+    qb.add(Cm, int(dim), int(width), std::vector<int64_t>(offsets, offsets + nmem + 1), tol, int(cap));
+    std::vector<h2g::DMat> Q;
+    std::vector<int> rk;
+    qb.run(P.c, Q, rk, size_t(1) << 30);
+    const int r = int(std::min<int64_t>(dim, std::max<int64_t>(rk[0], min_rank)));
+    std::vector<double> q(size_t(dim) * dim);
+    h2g::cuda_check(cudaMemcpy(q.data(), Q[0].m.p, sizeof(double) * dim * dim, cudaMemcpyDeviceToHost), "d2h");
+    // row-major Q -> square [Qr | Qs] column-major.
+    for (int64_t j = 0; j < dim; ++j) {
+      const int64_t src = j < dim - r ? r + j : j - (dim - r);
+      for (int64_t i = 0; i < dim; ++i) sq[j * dim + i] = q[i * dim + src];
+    }
+    *rank = r;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,333 @@
+// Host-side batch launchers (see batch.hpp).
+#include <algorithm>
+#include <cmath>
+
+#include "batch.hpp"
+
+namespace h2g {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+Slab Ctx::alloc(size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 8;
+  bytes = (bytes + 255) & ~size_t(255);
+  cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw std::runtime_error("device memory exhausted allocating " + std::to_string(bytes) +
+                             " bytes: " + cudaGetErrorString(e));
+  }
+  cudaStream_t s = stream;
+  return Slab(p, [s](void* q) { cudaFreeAsync(q, s); });
+}
+
+void Ctx::check_err() {
+  ErrWord h{};
+  cuda_check(cudaMemcpy(&h, err, sizeof(h), cudaMemcpyDeviceToHost), "error word");
+  if (h.code == 0) return;
+  cuda_check(cudaMemset(err, 0, sizeof(ErrWord)), "error reset");
+  if (h.code == 1)
+    throw std::runtime_error("assemble_block: singular evaluation (r + eta_reg == 0)");
+  if (h.code == 2) {
+    std::string what = (h.job >= 0 && h.job < int(lu_names.size())) ? lu_names[h.job] : "block";
+    throw std::runtime_error("singular block in LU of " + what + " at step " +
+                             std::to_string(h.step));
+  }
+  throw std::runtime_error("device error code " + std::to_string(h.code));
+}
+
+void Ctx::sync() {
+  cuda_check(cudaStreamSynchronize(stream), "stream sync");
+  check_err();
+}
+
+std::vector<DMat> alloc_mats(Ctx& c, const std::vector<std::pair<int, int>>& shapes) {
+  size_t total = 0;
+  std::vector<size_t> off(shapes.size());
+  for (size_t t = 0; t < shapes.size(); ++t) {
+    off[t] = total;
+    total += (size_t(shapes[t].first) * shapes[t].second + 3) & ~size_t(3);  // 32 B aligned
+  }
+  Slab s = c.alloc(total * sizeof(double));
+  std::vector<DMat> out(shapes.size());
+  for (size_t t = 0; t < shapes.size(); ++t) {
+    double* p = static_cast<double*>(s.get()) + off[t];
+    out[t].m = Mat{p, shapes[t].first, shapes[t].second, 1, shapes[t].first > 0 ? shapes[t].first : 1};
+    out[t].owner = s;
+  }
+  return out;
+}
+
+DMat alloc_mat(Ctx& c, int rows, int cols) { return alloc_mats(c, {{rows, cols}})[0]; }
+
+LuF alloc_lu(Ctx& c, int n) { return alloc_lus(c, {n})[0]; }
+
+std::vector<LuF> alloc_lus(Ctx& c, const std::vector<int>& ns) {
+  std::vector<std::pair<int, int>> shapes;
+  size_t np = 0;
+  for (int n : ns) {
+    shapes.push_back({n, n});
+    np += n;
+  }
+  auto mats = alloc_mats(c, shapes);
+  Slab ps = c.alloc(sizeof(int64_t) * (np ? np : 1));
+  std::vector<LuF> out(ns.size());
+  size_t at = 0;
+  for (size_t t = 0; t < ns.size(); ++t) {
+    out[t].lu = mats[t];
+    out[t].pslab = ps;
+    out[t].perm = static_cast<int64_t*>(ps.get()) + at;
+    at += ns[t];
+  }
+  return out;
+}
+
+namespace {
+
+template <class J>
+void tiles_of(const std::vector<J>& jobs, std::vector<int>& tj, std::vector<int>& ti,
+              Mat J::*field) {
+  for (size_t j = 0; j < jobs.size(); ++j) {
+    const Mat& m = jobs[j].*field;
+    if (m.rows <= 0 || m.cols <= 0) continue;
+    const int t = ((m.rows + 63) / 64) * ((m.cols + 63) / 64);
+    for (int k = 0; k < t; ++k) {
+      tj.push_back(int(j));
+      ti.push_back(k);
+    }
+  }
+}
+
+}  // namespace
+
+void GemmBatch::run(Ctx& c, int tag) {
+  if (jobs.empty()) return;
+  std::vector<GemmTile> tiles;
+  double fl = 0;
+  for (size_t j = 0; j < jobs.size(); ++j) {
+    const Mat& C = jobs[j].C;
+    if (C.rows <= 0 || C.cols <= 0) continue;
+    for (int s = 0; s < jobs[j].nseg; ++s) {
+      const GemmSeg& sg = segs[jobs[j].seg0 + s];
+      fl += 2.0 * C.rows * double(sg.A.cols) * C.cols;
+      if (sg.gen) fl += double(sg.A.cols) * C.cols * (c.kp.kind == 0 ? 9 : 11);
+    }
+    const int tm = (C.rows + 63) / 64, tn = (C.cols + 63) / 64;
+    for (int a = 0; a < tm; ++a)
+      for (int b = 0; b < tn; ++b) tiles.push_back({int(j), a, b});
+  }
+  c.add_flops(fl);
+  if (tiles.empty()) return;
+  Slab k1, k2, k3, k4;
+  const int2* dmask = upload(c, masks, k4);
+  for (size_t s = 0; s < segs.size(); ++s)
+    if (segs[s].gen && seg_mask_off[s] >= 0) segs[s].g.mask = dmask + seg_mask_off[s];
+  const GemmJob* dj = upload(c, jobs, k1);
+  const GemmSeg* ds = upload(c, segs, k2);
+  const GemmTile* dt = upload(c, tiles, k3);
+  launch_gemm(dj, ds, dt, int(tiles.size()), c.kp, c.cloud, c.err, tag, c.stream);
+  c.launches++;
+  cuda_check(cudaGetLastError(), "gemm launch");
+}
+
+void EvalBatch::run(Ctx& c, int tag) {
+  if (jobs.empty()) return;
+  std::vector<int> tj, ti;
+  tiles_of(jobs, tj, ti, &EvalJob::out);
+  double ev = 0;
+  for (auto& j : jobs) ev += double(j.out.rows) * j.out.cols;
+  c.add_flops(ev * (c.kp.kind == 0 ? 9 : 11));
+  if (tj.empty()) return;
+  Slab k1, k2, k3;
+  auto* dj = upload(c, jobs, k1);
+  auto* dtj = upload(c, tj, k2);
+  auto* dti = upload(c, ti, k3);
+  launch_eval(dj, dtj, dti, int(tj.size()), c.kp, c.cloud, c.err, tag, c.stream);
+  c.launches++;
+  cuda_check(cudaGetLastError(), "eval launch");
+}
+
+void CopyBatch::run(Ctx& c) {
+  if (jobs.empty()) return;
+  std::vector<int> tj, ti;
+  tiles_of(jobs, tj, ti, &CopyJob::dst);
+  if (tj.empty()) return;
+  Slab k1, k2, k3;
+  auto* dj = upload(c, jobs, k1);
+  auto* dtj = upload(c, tj, k2);
+  auto* dti = upload(c, ti, k3);
+  launch_copy(dj, dtj, dti, int(tj.size()), c.stream);
+  c.launches++;
+  cuda_check(cudaGetLastError(), "copy launch");
+}
+
+void AccBatch::run(Ctx& c) {
+  if (jobs.empty()) return;
+  std::vector<int> tj, ti;
+  tiles_of(jobs, tj, ti, &AccJob::dst);
+  if (tj.empty()) return;
+  Slab k1, k2, k3, k4;
+  auto* dj = upload(c, jobs, k1);
+  auto* ds = upload(c, srcs, k4);
+  auto* dtj = upload(c, tj, k2);
+  auto* dti = upload(c, ti, k3);
+  launch_accum(dj, ds, dtj, dti, int(tj.size()), c.stream);
+  c.launches++;
+  cuda_check(cudaGetLastError(), "accum launch");
+}
+
+std::vector<double> NormBatch::run(Ctx& c) {
+  std::vector<double> out(mats.size(), 0.0);
+  if (mats.empty()) return out;
+  Slab res = c.alloc(sizeof(double) * mats.size());
+  std::vector<NormJob> jobs(mats.size());
+  for (size_t t = 0; t < mats.size(); ++t) jobs[t] = {mats[t], static_cast<double*>(res.get()) + t};
+  Slab k1;
+  auto* dj = upload(c, jobs, k1);
+  launch_norms(dj, int(jobs.size()), c.stream);
+  c.launches++;
+  cuda_check(cudaMemcpyAsync(out.data(), res.get(), sizeof(double) * mats.size(),
+                             cudaMemcpyDeviceToHost, c.stream),
+             "norms d2h");
+  c.sync();
+  return out;
+}
+
+void LuBatch::run(Ctx& c) {
+  if (jobs.empty()) return;
+  double fl = 0;
+  for (auto& j : jobs) {
+    const double n = j.A.rows;
+    for (double k = 0; k < n; ++k) fl += (n - k - 1) + 2.0 * (n - k - 1) * (n - k - 1);
+  }
+  c.add_flops(fl);
+  Slab k1;
+  auto* dj = upload(c, jobs, k1);
+  c.lu_names = names;
+  launch_lu(dj, int(jobs.size()), c.err, ++c.lu_tag, c.stream);
+  c.launches++;
+  cuda_check(cudaGetLastError(), "lu launch");
+  // LU errors must be attributed to this batch's names: check now.
+  c.sync();
+}
+
+void SolveBatch::run(Ctx& c) {
+  if (jobs.empty()) return;
+  std::vector<SolveChunk> chunks;
+  size_t smem = 1;
+  double fl = 0;
+  for (size_t j = 0; j < jobs.size(); ++j) {
+    const SolveJob& s = jobs[j];
+    const int m = s.lu.rows;
+    const bool right = s.kind >= SOLVE_RIGHT;
+    const int total = right ? s.X.rows : s.X.cols;
+    const int w = solve_chunk_width(m);
+    for (int c0 = 0; c0 < total; c0 += w) chunks.push_back({int(j), c0, std::min(w, total - c0)});
+    smem = std::max(smem, size_t(m) * size_t(std::min(w, total)));
+    const double full = (s.kind == SOLVE_FULL || s.kind == SOLVE_TRANSPOSE || s.kind == SOLVE_RIGHT) ? 2.0 : 1.0;
+    fl += full * double(m) * m * total;
+  }
+  c.add_flops(fl);
+  Slab k1, k2;
+  auto* dj = upload(c, jobs, k1);
+  auto* dc = upload(c, chunks, k2);
+  launch_solve(dj, dc, int(chunks.size()), smem, c.stream);
+  c.launches++;
+  cuda_check(cudaGetLastError(), "solve launch");
+}
+
+void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t mem_budget) {
+  const size_t n_items = items.size();
+  Q.assign(n_items, DMat{});
+  rank.assign(n_items, 0);
+  if (n_items == 0) return;
+  std::vector<std::pair<int, int>> qs;
+  for (auto& it : items) qs.push_back({it.m, it.m});
+  std::vector<DMat> qm = alloc_mats(c, qs);
+  for (size_t t = 0; t < n_items; ++t) {
+    // Q is produced row-major: view element (i, j) at p[i*m + j].
+    Q[t] = qm[t];
+    Q[t].m = Mat{qm[t].m.p, items[t].m, items[t].m, items[t].m > 0 ? items[t].m : 1, 1};
+  }
+  Slab rk = c.alloc(sizeof(int) * n_items);
+  cuda_check(cudaMemsetAsync(rk.get(), 0, sizeof(int) * n_items, c.stream), "rank memset");
+  CopyBatch idents;
+  size_t t0 = 0;
+  while (t0 < n_items) {
+    // Chunk so the working copies + scratch stay under the budget.
+    size_t bytes = 0, t1 = t0;
+    while (t1 < n_items) {
+      const auto& it = items[t1];
+      const size_t need = sizeof(double) * (size_t(it.m) * it.n +
+                                            qr_scratch_doubles(it.m, it.n, int(it.offs.size()) - 1)) +
+                          sizeof(int64_t) * it.offs.size() + 1024;
+      if (t1 > t0 && bytes + need > mem_budget) break;
+      bytes += need;
+      ++t1;
+    }
+    Slab work = c.alloc(bytes);
+    std::vector<QrJob> jobs;
+    std::vector<int64_t> offs_all;
+    std::vector<size_t> offs_at;
+    for (size_t t = t0; t < t1; ++t) {
+      offs_at.push_back(offs_all.size());
+      offs_all.insert(offs_all.end(), items[t].offs.begin(), items[t].offs.end());
+    }
+    Slab ko;
+    int64_t* doffs = upload(c, offs_all, ko);
+    char* at = static_cast<char*>(work.get());
+    int max_m = 1;
+    double fl = 0;
+    for (size_t t = t0; t < t1; ++t) {
+      const auto& it = items[t];
+      if (it.n == 0 || it.m == 0) {
+        if (it.m > 0) idents.ident(Q[t].m);
+        continue;
+      }
+      QrJob j;
+      j.A = it.concat.m;
+      j.m = it.m;
+      j.n = it.n;
+      j.member_off = doffs + offs_at[t - t0];
+      j.nmem = int(it.offs.size()) - 1;
+      j.tol = it.tol;
+      j.member_tol = it.tol * 0.5;  // BasisBuildOptions::member_tol_factor (compression.hpp:67)
+      j.cap = it.cap;
+      j.work = reinterpret_cast<double*>(at);
+      j.ldw = it.n;
+      at += sizeof(double) * size_t(it.m) * it.n;
+      j.scratch = reinterpret_cast<double*>(at);
+      at += sizeof(double) * qr_scratch_doubles(it.m, it.n, j.nmem);
+      j.Q = Q[t].m.p;
+      j.rank_out = static_cast<int*>(rk.get()) + t;
+      jobs.push_back(j);
+      max_m = std::max(max_m, it.m);
+      fl += 2.0 * it.m * double(it.n);  // column norms
+    }
+    c.add_flops(fl);
+    Slab kj;
+    auto* dj = upload(c, jobs, kj);
+    launch_qr(dj, int(jobs.size()), max_m, c.stream);
+    c.launches++;
+    cuda_check(cudaGetLastError(), "qr launch");
+    t0 = t1;
+  }
+  idents.run(c);
+  cuda_check(cudaMemcpyAsync(rank.data(), rk.get(), sizeof(int) * n_items, cudaMemcpyDeviceToHost,
+                             c.stream),
+             "rank d2h");
+  c.sync();
+  // Reference flop rules for the executed steps (linalg.cpp:148, :176).
+  double fl = 0;
+  for (size_t t = 0; t < n_items; ++t) {
+    const double m = items[t].m, n = items[t].n;
+    for (int k = 0; k < rank[t]; ++k) fl += 4.0 * (m - k) + 4.0 * (m - k) * (n - k - 1) + 4.0 * (m - k) * m;
+  }
+  c.add_flops(fl);
+}
+
+}  // namespace h2g

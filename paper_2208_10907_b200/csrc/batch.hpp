@@ -1,0 +1,205 @@
+// Host-side batching layer: stream-ordered device slabs, matrix handles and
+// job builders. A factorization stage (one parallel_for of the reference)
+// becomes a handful of batched launches: the host collects every task's
+// jobs, uploads the descriptors once and launches one kernel per job type.
+#pragma once
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "kernels.hpp"
+
+namespace h2g {
+
+void cuda_check(cudaError_t e, const char* what);
+
+using Slab = std::shared_ptr<void>;
+
+struct Ctx {
+  cudaStream_t stream = nullptr;
+  ErrWord* err = nullptr;  // device
+  KernelParams kp;
+  Cloud cloud;
+  // statistics
+  int64_t launches = 0;
+  double flops = 0;  // algorithmic (reference counting rules)
+  std::map<std::string, double> phase_flops;
+  std::string phase = "other";
+  void add_flops(double f) {
+    flops += f;
+    phase_flops[phase] += f;
+  }
+  Slab alloc(size_t bytes);
+  void sync();            // stream sync + error word check
+  void check_err();       // throws the reference's message for device errors
+  std::vector<std::string> lu_names;  // current LU batch names (for errors)
+  int lu_tag = 0;
+};
+
+struct DMat {
+  Mat m;
+  Slab owner;
+  int rows() const { return m.rows; }
+  int cols() const { return m.cols; }
+};
+
+// Allocate several compact column-major matrices in one slab.
+std::vector<DMat> alloc_mats(Ctx& c, const std::vector<std::pair<int, int>>& shapes);
+DMat alloc_mat(Ctx& c, int rows, int cols);
+
+struct LuF {
+  DMat lu;
+  Slab pslab;
+  int64_t* perm = nullptr;
+  int n() const { return lu.rows(); }
+};
+
+template <class T>
+T* upload(Ctx& c, const std::vector<T>& v, Slab& keep) {
+  if (v.empty()) return nullptr;
+  keep = c.alloc(sizeof(T) * v.size());
+  cuda_check(cudaMemcpyAsync(keep.get(), v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice,
+                             c.stream),
+             "upload");
+  return static_cast<T*>(keep.get());
+}
+
+// ---- GEMM -----------------------------------------------------------------
+struct GemmBatch {
+  std::vector<GemmJob> jobs;
+  std::vector<GemmSeg> segs;
+  std::vector<int2> masks;
+  std::vector<int> seg_mask_off;  // per seg: offset into masks or -1
+  // Begin a job; add segments with seg()/seg_gen() afterwards.
+  void job(Mat C, bool acc) {
+    GemmJob j;
+    j.C = C;
+    j.seg0 = int(segs.size());
+    j.nseg = 0;
+    j.acc = acc ? 1 : 0;
+    jobs.push_back(j);
+  }
+  void seg(Mat A, Mat B, double alpha = 1.0) {
+    GemmSeg s;
+    s.A = A;
+    s.B = B;
+    s.alpha = alpha;
+    s.gen = 0;
+    segs.push_back(s);
+    seg_mask_off.push_back(-1);
+    jobs.back().nseg++;
+  }
+  // B generated from the kernel function: trans = 0 -> B(l,j) = K(rb+l, cb+j).
+  void seg_gen(Mat A, int64_t rb, int64_t cb, int Bcols, bool trans, double alpha,
+               const std::vector<int2>& mask = {}) {
+    GemmSeg s;
+    s.A = A;
+    s.B = Mat{nullptr, A.cols, Bcols, 0, 0};
+    s.alpha = alpha;
+    s.gen = 1;
+    s.g.rb = rb;
+    s.g.cb = cb;
+    s.g.trans = trans ? 1 : 0;
+    s.g.nmask = int(mask.size());
+    seg_mask_off.push_back(mask.empty() ? -1 : int(masks.size()));
+    masks.insert(masks.end(), mask.begin(), mask.end());
+    segs.push_back(s);
+    jobs.back().nseg++;
+  }
+  void run(Ctx& c, int tag = 0);
+  bool empty() const { return jobs.empty(); }
+};
+
+// C = op products convenience: C = A * B (fresh) as one job.
+inline void gemm1(GemmBatch& b, Mat C, Mat A, Mat B, double alpha = 1.0, bool acc = false) {
+  b.job(C, acc);
+  b.seg(A, B, alpha);
+}
+
+// ---- kernel-block evaluation ------------------------------------------------
+struct EvalBatch {
+  std::vector<EvalJob> jobs;
+  void add(Mat out, int64_t rb, int64_t cb) { jobs.push_back({out, rb, cb}); }
+  void run(Ctx& c, int tag = 0);
+};
+
+// ---- copies / adds ----------------------------------------------------------
+struct CopyBatch {
+  std::vector<CopyJob> jobs;
+  void copy(Mat dst, Mat src) { jobs.push_back({dst, src, 1.0, 0, 0}); }
+  void add(Mat dst, Mat src, double alpha) { jobs.push_back({dst, src, alpha, 1, 0}); }
+  void zero(Mat dst) { jobs.push_back({dst, Mat{}, 1.0, 0, 0}); }
+  void ident(Mat dst) { jobs.push_back({dst, Mat{}, 1.0, 0, 1}); }
+  void run(Ctx& c);
+};
+
+// ---- ordered accumulation ---------------------------------------------------------
+struct AccBatch {
+  std::vector<AccJob> jobs;
+  std::vector<AccSrc> srcs;
+  void job(Mat dst, bool zero_init) { jobs.push_back({dst, int(srcs.size()), 0, zero_init ? 1 : 0}); }
+  void src(Mat s, double alpha) {
+    srcs.push_back({s, alpha});
+    jobs.back().nsrc++;
+  }
+  void run(Ctx& c);
+};
+
+// ---- norms --------------------------------------------------------------------
+struct NormBatch {
+  std::vector<Mat> mats;
+  int add(Mat a) {
+    mats.push_back(a);
+    return int(mats.size()) - 1;
+  }
+  std::vector<double> run(Ctx& c);  // synchronous
+};
+
+// ---- LU -------------------------------------------------------------------------
+struct LuBatch {
+  std::vector<LuJob> jobs;
+  std::vector<std::string> names;
+  void add(const LuF& f, double tol, std::string name) {
+    jobs.push_back({f.lu.m, f.perm, tol});
+    names.push_back(std::move(name));
+  }
+  void run(Ctx& c);
+};
+LuF alloc_lu(Ctx& c, int n);
+std::vector<LuF> alloc_lus(Ctx& c, const std::vector<int>& ns);
+
+// ---- LU solves --------------------------------------------------------------------
+struct SolveBatch {
+  std::vector<SolveJob> jobs;
+  void add(const LuF& f, Mat X, int kind) {
+    if (X.rows == 0 || X.cols == 0 || f.n() == 0) return;
+    jobs.push_back({f.lu.m, f.perm, X, kind});
+  }
+  void run(Ctx& c);
+};
+
+// ---- pivoted QR bases ----------------------------------------------------------------
+// One basis_from_members call: a row-major dim x width concatenation.
+struct QrBatch {
+  struct Item {
+    DMat concat;           // m x n view (row-major)
+    int m, n;
+    std::vector<int64_t> offs;
+    double tol;
+    int cap;
+  };
+  std::vector<Item> items;
+  int add(DMat concat, int m, int n, std::vector<int64_t> offs, double tol, int cap) {
+    items.push_back({std::move(concat), m, n, std::move(offs), tol, cap});
+    return int(items.size()) - 1;
+  }
+  // Runs all QRs (in memory-bounded chunks); returns Q (row-major m x m in a
+  // DMat whose view is Q as an m x m matrix) and ranks.
+  void run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t mem_budget);
+};
+
+}  // namespace h2g

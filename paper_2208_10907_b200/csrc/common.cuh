@@ -1,0 +1,84 @@
+// Shared device-side definitions for the B200 H2-ULV hot path.
+//
+// Every dense object is an FP64 strided view: element (i, j) lives at
+// p[i * rs + j * cs]. Column-major (the reference Matrix layout,
+// proj/include/h2ulv/matrix.hpp:19-20) is rs = 1, cs = ld; a transpose is a
+// stride swap, so op(A) never needs a copy.
+//
+// Floating point: all kernels are compiled with --fmad=false and write every
+// FMA the reference's GCC -O3 -mfma build contracts as an explicit fma(), in
+// the reference's per-element accumulation order. That is what makes the GPU
+// results bitwise equal to the reference for the Laplace kernel.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace h2g {
+
+struct Mat {
+  double* p = nullptr;
+  int rows = 0, cols = 0;
+  int64_t rs = 1, cs = 0;
+  __host__ __device__ double& at(int64_t i, int64_t j) const { return p[i * rs + j * cs]; }
+  __host__ __device__ Mat t() const { return Mat{p, cols, rows, cs, rs}; }
+  __host__ __device__ Mat sub(int r0, int c0, int nr, int nc) const {
+    return Mat{p + r0 * rs + c0 * cs, nr, nc, rs, cs};
+  }
+  __host__ __device__ int64_t size() const { return int64_t(rows) * cols; }
+};
+
+inline Mat colmajor(double* p, int rows, int cols, int64_t ld = -1) {
+  return Mat{p, rows, cols, 1, ld < 0 ? rows : ld};
+}
+
+// Kernel function parameters (kernels.hpp:15-23): 0 = Laplace, 1 = Yukawa.
+struct KernelParams {
+  int kind = 0;
+  double alpha_m = 0.0;
+  double scale = 4.0 * 3.14159265358979323846;
+  double reg = 0.0;
+};
+
+// Reordered cloud in SoA form on the device.
+struct Cloud {
+  const double* x = nullptr;
+  const double* y = nullptr;
+  const double* z = nullptr;
+  const double* q = nullptr;
+  int64_t n = 0;
+};
+
+// kernel_eval / assemble_block entry (kernels.cpp:232-268): bitwise equal to
+// the reference for Laplace (r = sqrt(fma(dz,dz,fma(dx,dx,dy*dy))), IEEE
+// sqrt and division). Yukawa uses CUDA exp (<= 1 ulp from glibc).
+__device__ __forceinline__ double kernel_entry(const KernelParams& kp, const Cloud& c, int64_t i,
+                                               int64_t j, int* singular) {
+  const double dx = c.x[i] - c.x[j], dy = c.y[i] - c.y[j], dz = c.z[i] - c.z[j];
+  const double r = sqrt(fma(dz, dz, fma(dx, dx, dy * dy)));
+  const double denom = kp.scale * (r + kp.reg);
+  if (denom == 0.0) {
+    *singular = 1;
+    return 0.0;
+  }
+  const double qj = c.q[j];
+  if (kp.kind == 0) return qj / denom;
+  return qj * exp(-kp.alpha_m * r) / denom;
+}
+
+// Device-wide error word: first nonzero code wins (host reads after sync).
+struct ErrWord {
+  int code;   // 0 ok, 1 singular kernel evaluation, 2 singular LU pivot
+  int job;    // job index within the failing batch
+  int step;   // LU step
+  int tag;    // caller tag (which batch)
+};
+
+__device__ __forceinline__ void raise_err(ErrWord* e, int code, int job, int step, int tag) {
+  if (atomicCAS(&e->code, 0, code) == 0) {
+    e->job = job;
+    e->step = step;
+    e->tag = tag;
+  }
+}
+
+}  // namespace h2g

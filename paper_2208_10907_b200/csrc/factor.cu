@@ -1,0 +1,1444 @@
+// Level-parallel (dependency-free) H2-ULV factorization and solve on the GPU.
+//
+// Host C++ walks the reference's NodepDriver schedule (ulv.cpp:293-760) and
+// turns every parallel_for stage into batched sm_100a launches (batch.hpp).
+// All numerics run on the device; the host only enumerates jobs from the
+// integer block structure and reads back the discrete ranks once per basis
+// stage. Within a stage every element sees the reference's rounding sequence,
+// so factors and solutions are bitwise equal to the reference (Laplace).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <set>
+#include <stdexcept>
+
+#include "h2.hpp"
+
+namespace h2g {
+
+namespace {
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+struct PhaseTimer {
+  Ctx& c;
+  Stats& st;
+  std::string prev;
+  double t0;
+  PhaseTimer(Ctx& c_, Stats& s, const char* name) : c(c_), st(s), prev(c_.phase), t0(now_s()) {
+    c.phase = name;
+  }
+  ~PhaseTimer() {
+    st.phase_seconds[c.phase] += now_s() - t0;
+    c.phase = prev;
+  }
+};
+
+}  // namespace
+
+bool Structure::is_near(int l, int64_t i, int64_t j) const {
+  const int64_t* b = near(l, i);
+  return std::binary_search(b, b + nnear(l, i), j);
+}
+bool Structure::is_far(int l, int64_t i, int64_t j) const {
+  const int64_t* b = far(l, i);
+  return std::binary_search(b, b + nfar(l, i), j);
+}
+
+Problem::Problem() {
+  cuda_check(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaMalloc(&c.err, sizeof(ErrWord)), "err");
+  cuda_check(cudaMemset(c.err, 0, sizeof(ErrWord)), "err");
+}
+
+Problem::~Problem() {
+  // Release device objects before the stream they free on.
+  U.clear();
+  V.clear();
+  levels.clear();
+  top = LuF{};
+  near.clear();
+  near_slab.reset();
+  orig_slab.reset();
+  if (c.stream) cudaStreamSynchronize(c.stream);
+  cudaFree(c.err);
+  if (c.stream) cudaStreamDestroy(c.stream);
+}
+
+// Pipeline::build (report.cpp:79-91): tree, classification, near field.
+void Problem::build(const double* d_xyz, const double* d_q, int64_t n, int64_t leaf) {
+  double t0 = now_s();
+  build_tree_device(T, d_xyz, d_q, n, leaf, c.stream);
+  const int L = T.levels;
+  const int64_t nn = (int64_t(1) << (L + 1)) - 1;
+  be.resize(2 * nn);
+  cuda_check(cudaMemcpyAsync(be.data(), T.be, sizeof(int64_t) * 2 * nn, cudaMemcpyDeviceToHost,
+                             c.stream),
+             "be d2h");
+  c.sync();
+  double t1 = now_s();
+  classify_device(T, opt.eta, opt.structure == 1 ? 1 : 0, S, c.stream);
+  double t2 = now_s();
+  c.cloud = Cloud{T.x, T.y, T.z, T.q, n};
+  {
+    orig_slab = c.alloc(sizeof(double) * 4 * n);
+    double* o = static_cast<double*>(orig_slab.get());
+    DMat src{Mat{const_cast<double*>(d_xyz), int(n), 3, 3, 1}, Slab()};
+    CopyBatch cb;
+    cb.copy(Mat{o, int(n), 3, 1, n}, src.m);
+    cb.run(c);
+    cuda_check(cudaMemcpyAsync(o + 3 * n, d_q, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream), "q");
+    orig = Cloud{o, o + n, o + 2 * n, o + 3 * n, n};
+  }
+  // materialize_dense (hstructure.cpp:142-164): one arena, blocks aligned with near CSR.
+  const auto& LP = S.level[L];
+  std::vector<std::pair<int, int>> shapes;
+  for (int64_t i = 0; i < (int64_t(1) << L); ++i)
+    for (int64_t t = LP.near_ptr[i]; t < LP.near_ptr[i + 1]; ++t)
+      shapes.push_back({int(range_size(L, i)), int(range_size(L, LP.near_idx[t]))});
+  near = alloc_mats(c, shapes);
+  near_slab = near.empty() ? Slab() : near[0].owner;
+  EvalBatch eb;
+  size_t at = 0;
+  for (int64_t i = 0; i < (int64_t(1) << L); ++i)
+    for (int64_t t = LP.near_ptr[i]; t < LP.near_ptr[i + 1]; ++t, ++at)
+      eb.add(near[at].m, range_begin(L, i), range_begin(L, LP.near_idx[t]));
+  {
+    PhaseTimer pt(c, stats, "assemble");
+    eb.run(c);
+    c.sync();
+  }
+  stats.t_tree = t1 - t0;
+  stats.t_classify = t2 - t1;
+  stats.t_near = now_s() - t2;
+  built = true;
+}
+
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Driver {
+  Problem& P;
+  Ctx& c;
+  const Structure& S;
+  const Options& opt;
+  int L;
+  // child big layer (points x rank), per cluster of the previously processed level
+  std::vector<Mat> Ubig, Vbig;
+  std::vector<DMat> big_owner;
+  std::vector<PieceMap> carried;
+
+  Driver(Problem& p) : P(p), c(p.c), S(p.S), opt(p.opt), L(p.T.levels) {}
+
+  int64_t rb(int l, int64_t i) const { return P.range_begin(l, i); }
+  int64_t rs(int l, int64_t i) const { return P.range_size(l, i); }
+
+  static int find_near(const Structure& S, int l, int64_t i, int64_t j) {
+    const int64_t* b = S.near(l, i);
+    const int64_t n = S.nnear(l, i);
+    const int64_t* it = std::lower_bound(b, b + n, j);
+    if (it == b + n || *it != j) return -1;
+    return int(S.level[l].near_ptr[i] + (it - b));
+  }
+  Mat block(const SysL& sys, int64_t i, int64_t j) const {
+    const int t = find_near(S, sys.lvl, i, j);
+    if (t < 0) throw std::out_of_range("DenseSystem::block: no dense block");
+    return sys.blocks[t].m;
+  }
+
+  std::vector<TargetKey> ancestor_far_partners(int lvl, int64_t K) const {
+    std::vector<TargetKey> out;
+    int64_t a = K;
+    for (int l2 = lvl - 1; l2 >= 1; --l2) {
+      a >>= 1;
+      for (int64_t t = 0; t < S.nfar(l2, a); ++t) out.push_back({l2, S.far(l2, a)[t]});
+    }
+    return out;
+  }
+  std::vector<TargetKey> targets_of(int lvl, int64_t k) const {
+    std::vector<TargetKey> t;
+    for (int64_t x = 0; x < S.nfar(lvl, k); ++x) t.push_back({lvl, S.far(lvl, k)[x]});
+    for (auto& p : ancestor_far_partners(lvl, k)) t.push_back(p);
+    return t;
+  }
+  TargetKey covering_target(int lvl, int64_t i, int64_t j) const {
+    int64_t a = i, b = j;
+    int tl = lvl;
+    while (tl > 1) {
+      a >>= 1;
+      b >>= 1;
+      --tl;
+      if (S.is_far(tl, a, b)) return {tl, b};
+      if (S.is_near(tl, a, b)) throw std::logic_error("covering_target: covering pair is dense");
+    }
+    throw std::logic_error("covering_target: no covering far block");
+  }
+  // Columns of target range jr covered by level-lvl near partners of p
+  // (ulv.cpp:365-371 / :433-440); all_zero when one equals jr.
+  std::vector<int2> mask_for(int lvl, int64_t p, int64_t jb, int64_t je, bool& all_zero) const {
+    std::vector<int2> m;
+    all_zero = false;
+    for (int64_t t = 0; t < S.nnear(lvl, p); ++t) {
+      const int64_t jn = S.near(lvl, p)[t];
+      const int64_t a = rb(lvl, jn), b = a + rs(lvl, jn);
+      if (a >= jb && b <= je) {
+        m.push_back(make_int2(int(a - jb), int(b - jb)));
+        if (a == jb && b == je) all_zero = true;
+      }
+    }
+    return m;
+  }
+
+  // ---- precompute_fillins (compression.cpp:55-109) -------------------------
+  FillSet precompute_fillins(SysL& sys) {
+    PhaseTimer pt(c, P.stats, "fill_precompute");
+    FillSet out;
+    const int l = sys.lvl;
+    const int64_t m = sys.m;
+    if (!sys.offdiag) return out;
+    sys.diag_lu = alloc_lus(c, sys.dims);
+    {
+      CopyBatch cb;
+      LuBatch lb;
+      for (int64_t p = 0; p < m; ++p) {
+        cb.copy(sys.diag_lu[p].lu.m, block(sys, p, p));
+        lb.add(sys.diag_lu[p], opt.rr_pivot_tol, "diagonal block " + std::to_string(p));
+      }
+      cb.run(c);
+      lb.run(c);
+    }
+    // W_pj = A_pp^-1 A_pj for every off-diagonal near block.
+    std::map<std::pair<int64_t, int64_t>, DMat> W;
+    {
+      std::vector<std::pair<int64_t, int64_t>> keys;
+      std::vector<std::pair<int, int>> shapes;
+      for (int64_t p = 0; p < m; ++p)
+        for (int64_t t = 0; t < S.nnear(l, p); ++t) {
+          const int64_t j = S.near(l, p)[t];
+          if (j == p) continue;
+          keys.push_back({p, j});
+          shapes.push_back({sys.dims[p], sys.dims[j]});
+        }
+      auto mats = alloc_mats(c, shapes);
+      CopyBatch cb;
+      SolveBatch sb;
+      for (size_t t = 0; t < keys.size(); ++t) {
+        cb.copy(mats[t].m, block(sys, keys[t].first, keys[t].second));
+        sb.add(sys.diag_lu[keys[t].first], mats[t].m, SOLVE_FULL);
+        W[keys[t]] = mats[t];
+      }
+      cb.run(c);
+      sb.run(c);
+    }
+    // Targets: (c, j) sharing a common near p (both != p).
+    std::set<std::pair<int64_t, int64_t>> targets;
+    for (int64_t p = 0; p < m; ++p)
+      for (int64_t a = 0; a < S.nnear(l, p); ++a) {
+        const int64_t cc = S.near(l, p)[a];
+        if (cc == p) continue;
+        for (int64_t b = 0; b < S.nnear(l, p); ++b) {
+          const int64_t j = S.near(l, p)[b];
+          if (j == p) continue;
+          targets.insert({cc, j});
+        }
+      }
+    std::vector<std::pair<int, int>> shapes;
+    for (auto& t : targets) shapes.push_back({sys.dims[t.first], sys.dims[t.second]});
+    auto mats = alloc_mats(c, shapes);
+    GemmBatch gb;
+    size_t at = 0;
+    for (auto& t : targets) {
+      const auto [cc, j] = t;
+      gb.job(mats[at].m, false);
+      for (int64_t a = 0; a < S.nnear(l, cc); ++a) {
+        const int64_t p = S.near(l, cc)[a];
+        if (p == cc || p == j) continue;
+        auto it = W.find({p, j});
+        if (it == W.end()) continue;
+        gb.seg(block(sys, cc, p), it->second.m, -1.0);
+      }
+      out[t] = mats[at++];
+    }
+    gb.run(c);
+    return out;
+  }
+
+  // ---- basis_from_members (compression.cpp:111-146) batched -----------------
+  // A member list is realised straight into a row-major dim x width concat.
+  struct Members {
+    int dim = 0;
+    int width = 0;
+    std::vector<int64_t> offs{0};
+    DMat concat;
+    Mat slice(int off, int w) const {
+      return Mat{concat.m.p + off, dim, w, width > 0 ? width : 1, 1};
+    }
+    int add(int w) {
+      const int off = width;
+      width += w;
+      offs.push_back(width);
+      return off;
+    }
+  };
+  void alloc_concat(Members& M) {
+    M.concat = alloc_mat(c, M.dim, std::max(M.width, 1));
+    M.concat.m = Mat{M.concat.m.p, M.dim, M.width, std::max(M.width, 1), 1};
+  }
+
+  // Run QRs and produce bases with ranks equalised per cluster
+  // (compression.cpp:224-229 / ulv.cpp:507-511).
+  void bases_from_concats(std::vector<Members>& rows, std::vector<Members>& cols,
+                          std::vector<Basis>& Ub, std::vector<Basis>& Vb) {
+    const size_t m = rows.size();
+    QrBatch qb;
+    for (size_t k = 0; k < m; ++k)
+      qb.add(rows[k].concat, rows[k].dim, rows[k].width, rows[k].offs, opt.tol, opt.cap);
+    for (size_t k = 0; k < m; ++k)
+      qb.add(cols[k].concat, cols[k].dim, cols[k].width, cols[k].offs, opt.tol, opt.cap);
+    std::vector<DMat> Q;
+    std::vector<int> rank;
+    qb.run(c, Q, rank, opt.qr_mem_budget);
+    Ub.assign(m, {});
+    Vb.assign(m, {});
+    std::vector<std::pair<int, int>> shapes;
+    for (size_t k = 0; k < m; ++k) {
+      shapes.push_back({rows[k].dim, rows[k].dim});
+      shapes.push_back({rows[k].dim, rows[k].dim});
+    }
+    auto sq = alloc_mats(c, shapes);
+    CopyBatch cb;
+    for (size_t k = 0; k < m; ++k) {
+      const int dim = rows[k].dim;
+      // min_rank extension == re-splitting the same Q (basis_from_members
+      // is deterministic; compression.cpp:138-144).
+      const int r = std::min(dim, std::max(rank[k], rank[m + k]));
+      for (int side = 0; side < 2; ++side) {
+        Basis& B = side == 0 ? Ub[k] : Vb[k];
+        B.SQ = sq[2 * k + side];
+        B.dim = dim;
+        B.rank = r;
+        const Mat q = Q[side * m + k].m;
+        if (dim == 0) continue;
+        if (dim - r > 0) cb.copy(B.SQ.m.sub(0, 0, dim, dim - r), q.sub(0, r, dim, dim - r));
+        if (r > 0) cb.copy(B.SQ.m.sub(0, dim - r, dim, r), q.sub(0, 0, dim, r));
+      }
+    }
+    cb.run(c);
+  }
+
+  // ---- build_leaf_bases (compression.cpp:193-234) ---------------------------
+  void build_leaf_bases(SysL& sys, const FillSet& fills) {
+    PhaseTimer pt(c, P.stats, "basis");
+    const int64_t m = sys.m;
+    const bool coupling = opt.absorb_coupling && opt.structure == 0 && sys.offdiag;
+    // Row members: fills (i, j != i) | A(i, far j) | A(i, ancestor far J) [+ coupling].
+    std::vector<Members> rows(m), cols(m);
+    std::vector<std::vector<std::pair<int64_t, int>>> couple_at(m);
+    for (int64_t i = 0; i < m; ++i) {
+      Members& R = rows[i];
+      R.dim = sys.dims[i];
+      for (auto& [key, F] : fills)
+        if (key.first == i && key.second != i) R.add(F.cols());
+      for (int64_t t = 0; t < S.nfar(L, i); ++t) R.add(int(rs(L, S.far(L, i)[t])));
+      for (auto [l2, J] : ancestor_far_partners(L, i)) R.add(int(rs(l2, J)));
+      Members& C = cols[i];
+      C.dim = sys.dims[i];
+      for (auto& [key, F] : fills)
+        if (key.second == i && key.first != i) C.add(F.rows());
+      for (int64_t t = 0; t < S.nfar(L, i); ++t) C.add(int(rs(L, S.far(L, i)[t])));
+      for (auto [l2, I] : ancestor_far_partners(L, i)) C.add(int(rs(l2, I)));
+    }
+    // Provisional bases need the plain row members first.
+    std::vector<int> base_width(m);
+    for (int64_t i = 0; i < m; ++i) base_width[i] = rows[i].width;
+    std::vector<Basis> prov_rank_only;
+    std::vector<DMat> provQ;
+    std::vector<int> provR;
+    auto fill_row_members = [&](std::vector<Members>& R, bool with_tail) {
+      CopyBatch cb;
+      EvalBatch eb;
+      for (int64_t i = 0; i < m; ++i) {
+        alloc_concat(R[i]);
+        int off = 0;
+        for (auto& [key, F] : fills)
+          if (key.first == i && key.second != i) {
+            cb.copy(R[i].slice(off, F.cols()), F.m);
+            off += F.cols();
+          }
+        for (int64_t t = 0; t < S.nfar(L, i); ++t) {
+          const int64_t j = S.far(L, i)[t];
+          eb.add(R[i].slice(off, int(rs(L, j))), rb(L, i), rb(L, j));
+          off += int(rs(L, j));
+        }
+        for (auto [l2, J] : ancestor_far_partners(L, i)) {
+          eb.add(R[i].slice(off, int(rs(l2, J))), rb(L, i), rb(l2, J));
+          off += int(rs(l2, J));
+        }
+        (void)with_tail;
+      }
+      cb.run(c);
+      eb.run(c);
+    };
+    if (coupling) {
+      std::vector<Members> prow = rows;
+      fill_row_members(prow, false);
+      QrBatch qb;
+      for (int64_t p = 0; p < m; ++p) qb.add(prow[p].concat, prow[p].dim, prow[p].width, prow[p].offs, opt.tol, opt.cap);
+      qb.run(c, provQ, provR, opt.qr_mem_budget);
+      prow.clear();
+      // X_p = A_pp^-1 Qs_p, coupling member A_ip X_p for p in near(i).
+      std::vector<DMat> X(m);
+      std::vector<std::pair<int, int>> shapes;
+      for (int64_t p = 0; p < m; ++p) shapes.push_back({sys.dims[p], provR[p]});
+      auto xs = alloc_mats(c, shapes);
+      CopyBatch cb;
+      SolveBatch sb;
+      for (int64_t p = 0; p < m; ++p) {
+        X[p] = xs[p];
+        if (provR[p] == 0) continue;
+        cb.copy(X[p].m, provQ[p].m.sub(0, 0, sys.dims[p], provR[p]));
+        sb.add(sys.diag_lu[p], X[p].m, SOLVE_FULL);
+      }
+      cb.run(c);
+      sb.run(c);
+      for (int64_t i = 0; i < m; ++i)
+        for (int64_t t = 0; t < S.nnear(L, i); ++t) {
+          const int64_t p = S.near(L, i)[t];
+          if (p == i || provR[p] == 0) continue;
+          couple_at[i].push_back({p, rows[i].add(provR[p])});
+        }
+      fill_row_members(rows, true);
+      GemmBatch gb;
+      for (int64_t i = 0; i < m; ++i)
+        for (auto [p, off] : couple_at[i]) gemm1(gb, rows[i].slice(off, provR[p]), block(sys, i, p), X[p].m);
+      gb.run(c);
+    } else {
+      fill_row_members(rows, false);
+    }
+    // Column members: F(c, j)^T | A(i, j)^T | A(I, j)^T.
+    {
+      CopyBatch cb;
+      EvalBatch eb;
+      for (int64_t j = 0; j < m; ++j) {
+        Members& C = cols[j];
+        alloc_concat(C);
+        int off = 0;
+        for (auto& [key, F] : fills)
+          if (key.second == j && key.first != j) {
+            cb.copy(C.slice(off, F.rows()).t(), F.m);
+            off += F.rows();
+          }
+        for (int64_t t = 0; t < S.nfar(L, j); ++t) {
+          const int64_t i = S.far(L, j)[t];
+          eb.add(C.slice(off, int(rs(L, i))).t(), rb(L, i), rb(L, j));
+          off += int(rs(L, i));
+        }
+        for (auto [l2, I] : ancestor_far_partners(L, j)) {
+          eb.add(C.slice(off, int(rs(l2, I))).t(), rb(l2, I), rb(L, j));
+          off += int(rs(l2, I));
+        }
+      }
+      cb.run(c);
+      eb.run(c);
+    }
+    bases_from_concats(rows, cols, P.U[L], P.V[L]);
+  }
+
+  // ---- build_leaf_pieces (ulv.cpp:336-401) -----------------------------------
+  void build_leaf_pieces(SysL& sys, const FillSet& fills, std::vector<PieceMap>& pieces,
+                         double* level_max) {
+    PhaseTimer pt(c, P.stats, "skeleton");
+    const int64_t m = sys.m;
+    const auto& Ub = P.U[L];
+    const auto& Vb = P.V[L];
+    pieces.assign(m, {});
+    // q_cp = (A_pp^-T A_cp^T Us_c)^T for near p != c.
+    std::map<std::pair<int64_t, int64_t>, DMat> qT;  // stored as B = dims_p x r_c (q = B^T)
+    if (sys.offdiag) {
+      std::vector<std::pair<int64_t, int64_t>> keys;
+      std::vector<std::pair<int, int>> shapes;
+      for (int64_t cc = 0; cc < m; ++cc) {
+        if (Ub[cc].rank == 0) continue;
+        for (int64_t t = 0; t < S.nnear(L, cc); ++t) {
+          const int64_t p = S.near(L, cc)[t];
+          if (p == cc) continue;
+          keys.push_back({cc, p});
+          shapes.push_back({sys.dims[p], Ub[cc].rank});
+        }
+      }
+      auto mats = alloc_mats(c, shapes);
+      GemmBatch gb;
+      SolveBatch sb;
+      for (size_t t = 0; t < keys.size(); ++t) {
+        const auto [cc, p] = keys[t];
+        gemm1(gb, mats[t].m, block(sys, cc, p).t(), Ub[cc].Qs());
+        sb.add(sys.diag_lu[p], mats[t].m, SOLVE_TRANSPOSE);
+        qT[keys[t]] = mats[t];
+      }
+      gb.run(c);
+      sb.run(c);
+    }
+    // Pieces: Us_c^T A(c, J) - sum_p q_cp A(p, J)[masked], B generated in-kernel.
+    std::vector<std::pair<int64_t, TargetKey>> pkeys;
+    std::vector<std::pair<int, int>> shapes;
+    for (int64_t cc = 0; cc < m; ++cc)
+      for (auto& tk : targets_of(L, cc)) {
+        pkeys.push_back({cc, tk});
+        shapes.push_back({Ub[cc].rank, int(rs(tk.first, tk.second))});
+      }
+    auto mats = alloc_mats(c, shapes);
+    GemmBatch gb;
+    for (size_t t = 0; t < pkeys.size(); ++t) {
+      const auto [cc, tk] = pkeys[t];
+      const int64_t jb = rb(tk.first, tk.second), je = jb + rs(tk.first, tk.second);
+      const int w = int(je - jb);
+      gb.job(mats[t].m, false);
+      gb.seg_gen(Ub[cc].Qs().t(), rb(L, cc), jb, w, false, 1.0);
+      if (Ub[cc].rank > 0 && sys.offdiag)
+        for (int64_t x = 0; x < S.nnear(L, cc); ++x) {
+          const int64_t p = S.near(L, cc)[x];
+          if (p == cc) continue;
+          bool all_zero;
+          auto mask = mask_for(L, p, jb, je, all_zero);
+          if (all_zero) continue;
+          gb.seg_gen(qT[{cc, p}].m.t(), rb(L, p), jb, w, false, -1.0, mask);
+        }
+      pieces[cc][tk] = mats[t];
+    }
+    gb.run(c);
+    // Fill content: project, measure absorption, add into the target piece.
+    observe_and_add_fills(L, fills, pieces, level_max, true);
+  }
+
+  // uf = Us_c^T F, proj = uf Vs_j; observe_fill (ulv.cpp:140-147); for leaf,
+  // add uf into far / covering pieces (ulv.cpp:380-400).
+  void observe_and_add_fills(int lvl, const FillSet& fills, std::vector<PieceMap>& pieces,
+                             double* level_max, bool add_to_pieces) {
+    const auto& Ub = P.U[lvl];
+    const auto& Vb = P.V[lvl];
+    std::vector<std::pair<int64_t, int64_t>> keys;
+    std::vector<std::pair<int, int>> shapes;
+    for (auto& [key, F] : fills) {
+      if (key.first == key.second) continue;
+      keys.push_back(key);
+      shapes.push_back({Ub[key.first].rank, F.cols()});
+      shapes.push_back({Ub[key.first].rank, Vb[key.second].rank});
+    }
+    auto mats = alloc_mats(c, shapes);
+    GemmBatch g1, g2;
+    NormBatch nb;
+    for (size_t t = 0; t < keys.size(); ++t) {
+      const auto [cc, j] = keys[t];
+      const DMat& F = fills.at(keys[t]);
+      gemm1(g1, mats[2 * t].m, Ub[cc].Qs().t(), F.m);
+      gemm1(g2, mats[2 * t + 1].m, mats[2 * t].m, Vb[j].Qs());
+      nb.add(F.m);
+      nb.add(mats[2 * t + 1].m);
+    }
+    g1.run(c);
+    g2.run(c);
+    auto norms = nb.run(c);
+    for (size_t t = 0; t < keys.size(); ++t)
+      observe_fill(lvl, keys[t].first, keys[t].second, norms[2 * t], norms[2 * t + 1], level_max);
+    if (!add_to_pieces) return;
+    CopyBatch cb;
+    for (size_t t = 0; t < keys.size(); ++t) {
+      const auto [cc, j] = keys[t];
+      const Mat uf = mats[2 * t].m;
+      if (S.is_far(lvl, cc, j)) {
+        cb.add(pieces[cc].at({lvl, j}).m, uf, 1.0);
+      } else if (!S.is_near(lvl, cc, j)) {
+        TargetKey tk = covering_target(lvl, cc, j);
+        const int off = int(rb(lvl, j) - rb(tk.first, tk.second));
+        const Mat& pc = pieces[cc].at(tk).m;
+        cb.add(pc.sub(0, off, pc.rows, uf.cols), uf, 1.0);
+      }
+    }
+    cb.run(c);
+  }
+
+  void observe_fill(int lvl, int64_t cc, int64_t j, double nf, double kept, double* level_max) {
+    const double resid = std::sqrt(std::max(0.0, nf * nf - kept * kept));
+    if (nf > 0.0 && level_max) *level_max = std::max(*level_max, resid / nf);
+    if (resid > opt.abort_residual_factor * opt.tol * nf && nf > 1e-300)
+      throw std::runtime_error("basis does not absorb fill-in at level " + std::to_string(lvl) +
+                               " block (" + std::to_string(cc) + "," + std::to_string(j) + ")");
+  }
+
+  // cols_to_merged (ulv.cpp:468-474) of a piece whose rows come in up to two
+  // row blocks (vconcat of carried children), written into out (rows x dims_J).
+  void cols_to_merged(GemmBatch& gb, Mat out, const std::vector<Mat>& row_blocks, int64_t J) {
+    const Mat v0 = Vbig[2 * J], v1 = Vbig[2 * J + 1];
+    int r = 0;
+    for (const Mat& pb : row_blocks) {
+      if (pb.rows > 0) {
+        gemm1(gb, out.sub(r, 0, pb.rows, v0.cols), pb.sub(0, 0, pb.rows, v0.rows), v0);
+        gemm1(gb, out.sub(r, v0.cols, pb.rows, v1.cols), pb.sub(0, v0.rows, pb.rows, v1.rows), v1);
+      }
+      r += pb.rows;
+    }
+  }
+
+  // ---- build_upper_pieces (ulv.cpp:405-464) ----------------------------------
+  void build_upper_pieces(SysL& sys, const FillSet& fills, std::vector<PieceMap>& stack,
+                          std::vector<PieceMap>& merged) {
+    PhaseTimer pt(c, P.stats, "skeleton");
+    const int lvl = sys.lvl;
+    const int64_t m = sys.m;
+    stack.assign(m, {});
+    {
+      std::vector<std::pair<int64_t, TargetKey>> keys;
+      std::vector<std::pair<int, int>> shapes;
+      for (int64_t K = 0; K < m; ++K)
+        for (auto& tk : targets_of(lvl, K)) {
+          if (!carried[2 * K].count(tk) || !carried[2 * K + 1].count(tk))
+            throw std::logic_error("build_upper_pieces: missing child piece");
+          keys.push_back({K, tk});
+          shapes.push_back({sys.dims[K], int(rs(tk.first, tk.second))});
+        }
+      auto mats = alloc_mats(c, shapes);
+      CopyBatch cb;
+      for (size_t t = 0; t < keys.size(); ++t) {
+        const auto [K, tk] = keys[t];
+        const Mat a = carried[2 * K].at(tk).m, b = carried[2 * K + 1].at(tk).m;
+        if (a.rows) cb.copy(mats[t].m.sub(0, 0, a.rows, a.cols), a);
+        if (b.rows) cb.copy(mats[t].m.sub(a.rows, 0, b.rows, b.cols), b);
+        stack[K][tk] = mats[t];
+      }
+      cb.run(c);
+    }
+    merged.assign(m, {});
+    if (sys.offdiag) {
+      // g(P, tk) = A_PP^-1 (stack[P][tk] with P's near columns zeroed), shared across K.
+      std::map<std::pair<int64_t, TargetKey>, DMat> g;
+      std::vector<std::pair<int64_t, TargetKey>> need;
+      for (int64_t K = 0; K < m; ++K)
+        for (int64_t x = 0; x < S.nnear(lvl, K); ++x) {
+          const int64_t Pp = S.near(lvl, K)[x];
+          if (Pp == K) continue;
+          for (auto& [tk, piece] : stack[K]) {
+            if (!stack[Pp].count(tk)) continue;
+            need.push_back({Pp, tk});
+          }
+        }
+      std::sort(need.begin(), need.end());
+      need.erase(std::unique(need.begin(), need.end()), need.end());
+      std::vector<std::pair<int, int>> shapes;
+      std::vector<std::pair<int64_t, TargetKey>> gkeys;
+      std::vector<std::vector<int2>> gmasks;
+      for (auto& [Pp, tk] : need) {
+        const int64_t jb = rb(tk.first, tk.second), je = jb + rs(tk.first, tk.second);
+        bool all_zero;
+        auto mask = mask_for(lvl, Pp, jb, je, all_zero);
+        if (all_zero) continue;
+        gkeys.push_back({Pp, tk});
+        gmasks.push_back(mask);
+        shapes.push_back({sys.dims[Pp], int(je - jb)});
+      }
+      auto mats = alloc_mats(c, shapes);
+      CopyBatch cb, zb;
+      SolveBatch sb;
+      for (size_t t = 0; t < gkeys.size(); ++t) {
+        const auto [Pp, tk] = gkeys[t];
+        cb.copy(mats[t].m, stack[Pp].at(tk).m);
+        for (auto& r : gmasks[t]) zb.zero(mats[t].m.sub(0, r.x, mats[t].rows(), r.y - r.x));
+        sb.add(sys.diag_lu[Pp], mats[t].m, SOLVE_FULL);
+        g[gkeys[t]] = mats[t];
+      }
+      cb.run(c);
+      zb.run(c);
+      sb.run(c);
+      // corrected = stack - sum_P A_KP g(P, tk), accumulated over P in order.
+      std::vector<std::pair<int64_t, TargetKey>> keys;
+      std::vector<std::pair<int, int>> cshapes;
+      for (int64_t K = 0; K < m; ++K)
+        for (auto& [tk, piece] : stack[K]) {
+          keys.push_back({K, tk});
+          cshapes.push_back({piece.rows(), piece.cols()});
+        }
+      auto cm = alloc_mats(c, cshapes);
+      CopyBatch cc;
+      GemmBatch gb;
+      for (size_t t = 0; t < keys.size(); ++t) {
+        const auto [K, tk] = keys[t];
+        cc.copy(cm[t].m, stack[K].at(tk).m);
+        bool any = false;
+        for (int64_t x = 0; x < S.nnear(lvl, K); ++x) {
+          const int64_t Pp = S.near(lvl, K)[x];
+          if (Pp == K) continue;
+          auto it = g.find({Pp, tk});
+          if (it == g.end()) continue;
+          if (!any) gb.job(cm[t].m, true);
+          any = true;
+          gb.seg(block(sys, K, Pp), it->second.m, -1.0);
+        }
+        merged[K][tk] = cm[t];
+      }
+      cc.run(c);
+      gb.run(c);
+    } else {
+      merged = stack;
+    }
+    // Covered fills: expand merged columns to raw columns, add into the covering slice.
+    std::vector<std::pair<int64_t, int64_t>> fk;
+    std::vector<std::pair<int, int>> shapes;
+    for (auto& [key, F] : fills) {
+      const auto [cc, j] = key;
+      if (cc == j || S.is_far(lvl, cc, j) || S.is_near(lvl, cc, j)) continue;
+      fk.push_back(key);
+      shapes.push_back({F.rows(), int(rs(lvl, j))});
+    }
+    if (fk.empty()) return;
+    auto raws = alloc_mats(c, shapes);
+    GemmBatch gb;
+    CopyBatch cb;
+    for (size_t t = 0; t < fk.size(); ++t) {
+      const auto [cc, j] = fk[t];
+      const Mat F = fills.at(fk[t]).m;
+      const Mat v0 = Vbig[2 * j], v1 = Vbig[2 * j + 1];
+      gemm1(gb, raws[t].m.sub(0, 0, F.rows, v0.rows), F.sub(0, 0, F.rows, v0.cols), v0.t());
+      gemm1(gb, raws[t].m.sub(0, v0.rows, F.rows, v1.rows), F.sub(0, v0.cols, F.rows, v1.cols), v1.t());
+      TargetKey tk = covering_target(lvl, cc, j);
+      const int off = int(rb(lvl, j) - rb(tk.first, tk.second));
+      const Mat pc = merged[cc].at(tk).m;
+      cb.add(pc.sub(0, off, pc.rows, raws[t].cols()), raws[t].m, 1.0);
+    }
+    gb.run(c);
+    cb.run(c);
+  }
+
+  // ---- build_transfers_nodep (ulv.cpp:476-521) --------------------------------
+  void build_transfers(SysL& sys, const FillSet& fills, const std::vector<PieceMap>& merged) {
+    PhaseTimer pt(c, P.stats, "basis");
+    const int lvl = sys.lvl;
+    const int64_t m = sys.m;
+    std::vector<Members> rows(m), cols(m);
+    for (int64_t k = 0; k < m; ++k) {
+      rows[k].dim = cols[k].dim = sys.dims[k];
+      for (auto& [key, F] : fills)
+        if (key.first == k && key.second != k) rows[k].add(F.cols());
+      for (auto& [tk, piece] : merged[k]) rows[k].add(piece.cols());
+      for (auto& [key, F] : fills)
+        if (key.second == k && key.first != k) cols[k].add(F.rows());
+      for (int64_t t = 0; t < S.nfar(lvl, k); ++t) cols[k].add(sys.dims[S.far(lvl, k)[t]]);
+      for (auto [l2, I] : ancestor_far_partners(lvl, k)) cols[k].add(int(rs(l2, I)));
+    }
+    CopyBatch cb;
+    GemmBatch gb;
+    for (int64_t k = 0; k < m; ++k) {
+      alloc_concat(rows[k]);
+      alloc_concat(cols[k]);
+      int off = 0;
+      for (auto& [key, F] : fills)
+        if (key.first == k && key.second != k) {
+          cb.copy(rows[k].slice(off, F.cols()), F.m);
+          off += F.cols();
+        }
+      for (auto& [tk, piece] : merged[k]) {
+        cb.copy(rows[k].slice(off, piece.cols()), piece.m);
+        off += piece.cols();
+      }
+      off = 0;
+      for (auto& [key, F] : fills)
+        if (key.second == k && key.first != k) {
+          cb.copy(cols[k].slice(off, F.rows()).t(), F.m);
+          off += F.rows();
+        }
+      for (int64_t t = 0; t < S.nfar(lvl, k); ++t) {
+        const int64_t i = S.far(lvl, k)[t];
+        const Mat piece = merged[i].at({lvl, k}).m;
+        cols_to_merged(gb, cols[k].slice(off, piece.rows).t(), {piece}, k);
+        off += piece.rows;
+      }
+      for (auto [l2, I] : ancestor_far_partners(lvl, k)) {
+        // (A(I, c0) Vbig_c0 | A(I, c1) Vbig_c1)^T = [Vbig_c0^T A(I,c0)^T ; ...]
+        const int w = int(rs(l2, I));
+        const Mat dst = cols[k].slice(off, w);
+        const Mat v0 = Vbig[2 * k], v1 = Vbig[2 * k + 1];
+        gb.job(dst.sub(0, 0, v0.cols, w), false);
+        gb.seg_gen(v0.t(), rb(l2, I), rb(lvl + 1, 2 * k), w, true, 1.0);
+        gb.job(dst.sub(v0.cols, 0, v1.cols, w), false);
+        gb.seg_gen(v1.t(), rb(l2, I), rb(lvl + 1, 2 * k + 1), w, true, 1.0);
+        off += w;
+      }
+    }
+    cb.run(c);
+    gb.run(c);
+    for (int64_t k = 0; k < m; ++k)
+      if (sys.dims[k] == 0 && rows[k].width > 0)
+        throw std::runtime_error("compute_transfer: rank-0 children with nonzero parent blocks");
+    bases_from_concats(rows, cols, P.U[lvl], P.V[lvl]);
+  }
+
+  // ---- assemble_level (ulv.cpp:526-607) ----------------------------------------
+  void assemble_level(SysL& sys, const FillSet& fills, const std::vector<PieceMap>& pieces,
+                      const std::vector<PieceMap>& merged, std::vector<DMat>& diag_S,
+                      std::map<std::pair<int64_t, int64_t>, DMat>& far_ss,
+                      std::map<std::pair<int64_t, int64_t>, DMat>& dense_ss, double* level_max) {
+    PhaseTimer pt(c, P.stats, "factorize");
+    const int lvl = sys.lvl;
+    const bool is_leaf = lvl == L;
+    const int64_t m = sys.m;
+    const auto& Ub = P.U[lvl];
+    const auto& Vb = P.V[lvl];
+    // Diagonal skeletons: [Ur Us]^T (A_kk + F_kk) [Vr Vs].
+    {
+      std::vector<std::pair<int, int>> shapes;
+      for (int64_t k = 0; k < m; ++k) {
+        shapes.push_back({sys.dims[k], sys.dims[k]});
+        shapes.push_back({sys.dims[k], sys.dims[k]});
+        shapes.push_back({sys.dims[k], sys.dims[k]});
+      }
+      auto mats = alloc_mats(c, shapes);
+      CopyBatch cb, ab;
+      GemmBatch g1, g2;
+      diag_S.assign(m, {});
+      for (int64_t k = 0; k < m; ++k) {
+        const Mat D = mats[3 * k].m, T1 = mats[3 * k + 1].m;
+        cb.copy(D, block(sys, k, k));
+        auto it = fills.find({k, k});
+        if (it != fills.end()) ab.add(D, it->second.m, 1.0);
+        gemm1(g1, T1, Ub[k].SQ.m.t(), D);
+        gemm1(g2, mats[3 * k + 2].m, T1, Vb[k].SQ.m);
+        diag_S[k] = mats[3 * k + 2];
+      }
+      cb.run(c);
+      ab.run(c);
+      g1.run(c);
+      g2.run(c);
+    }
+    // Far skeletons from the pieces.
+    {
+      std::vector<std::pair<int64_t, int64_t>> keys;
+      std::vector<std::pair<int, int>> shapes;
+      for (int64_t k = 0; k < m; ++k)
+        for (int64_t t = 0; t < S.nfar(lvl, k); ++t) {
+          const int64_t j = S.far(lvl, k)[t];
+          keys.push_back({k, j});
+          shapes.push_back({Ub[k].rank, Vb[j].rank});
+          if (!is_leaf) {
+            shapes.push_back({sys.dims[k], sys.dims[j]});
+            shapes.push_back({Ub[k].rank, sys.dims[j]});
+          }
+        }
+      auto mats = alloc_mats(c, shapes);
+      GemmBatch g1, g2, g3;
+      const int per = is_leaf ? 1 : 3;
+      for (size_t t = 0; t < keys.size(); ++t) {
+        const auto [k, j] = keys[t];
+        const Mat Sm = mats[per * t].m;
+        if (is_leaf) {
+          gemm1(g1, Sm, pieces[k].at({lvl, j}).m, Vb[j].Qs());
+        } else {
+          const Mat y = mats[per * t + 1].m, ty = mats[per * t + 2].m;
+          cols_to_merged(g1, y, {merged[k].at({lvl, j}).m}, j);
+          gemm1(g2, ty, Ub[k].Qs().t(), y);
+          gemm1(g3, Sm, ty, Vb[j].Qs());
+        }
+        far_ss[keys[t]] = mats[per * t];
+      }
+      g1.run(c);
+      g2.run(c);
+      g3.run(c);
+    }
+    if (!sys.offdiag) return;
+    // Off-diagonal near content: projected fills + T terms over far (p, j).
+    std::vector<std::pair<int64_t, int64_t>> pairs;
+    for (int64_t k = 0; k < m; ++k)
+      for (int64_t t = 0; t < S.nnear(lvl, k); ++t) {
+        const int64_t j = S.near(lvl, k)[t];
+        if (j != k) pairs.push_back({k, j});
+      }
+    // Fill projections (uf, proj) and their observation.
+    std::map<std::pair<int64_t, int64_t>, DMat> proj;
+    {
+      std::vector<std::pair<int64_t, int64_t>> keys;
+      std::vector<std::pair<int, int>> shapes;
+      for (auto& kj : pairs) {
+        auto it = fills.find(kj);
+        if (it == fills.end()) continue;
+        keys.push_back(kj);
+        shapes.push_back({Ub[kj.first].rank, it->second.cols()});
+        shapes.push_back({Ub[kj.first].rank, Vb[kj.second].rank});
+      }
+      auto mats = alloc_mats(c, shapes);
+      GemmBatch g1, g2;
+      NormBatch nb;
+      for (size_t t = 0; t < keys.size(); ++t) {
+        const auto [k, j] = keys[t];
+        const Mat F = fills.at(keys[t]).m;
+        gemm1(g1, mats[2 * t].m, Ub[k].Qs().t(), F);
+        gemm1(g2, mats[2 * t + 1].m, mats[2 * t].m, Vb[j].Qs());
+        nb.add(F);
+        nb.add(mats[2 * t + 1].m);
+        proj[keys[t]] = mats[2 * t + 1];
+      }
+      g1.run(c);
+      g2.run(c);
+      auto norms = nb.run(c);
+      for (size_t t = 0; t < keys.size(); ++t)
+        observe_fill(lvl, keys[t].first, keys[t].second, norms[2 * t], norms[2 * t + 1], level_max);
+    }
+    // g(p, j) = A_pp^-1 content(p, j), shared across k.
+    std::vector<std::tuple<int64_t, int64_t, int64_t>> triples;  // (k, j, p)
+    std::set<std::pair<int64_t, int64_t>> gneed;
+    for (auto [k, j] : pairs)
+      for (int64_t x = 0; x < S.nnear(lvl, k); ++x) {
+        const int64_t p = S.near(lvl, k)[x];
+        if (p == k || p == j || !S.is_far(lvl, p, j)) continue;
+        triples.push_back({k, j, p});
+        gneed.insert({p, j});
+      }
+    std::map<std::pair<int64_t, int64_t>, DMat> g;
+    {
+      std::vector<std::pair<int64_t, int64_t>> keys(gneed.begin(), gneed.end());
+      std::vector<std::pair<int, int>> shapes;
+      for (auto [p, j] : keys) shapes.push_back({sys.dims[p], sys.dims[j]});
+      auto mats = alloc_mats(c, shapes);
+      EvalBatch eb;
+      GemmBatch gb;
+      SolveBatch sb;
+      for (size_t t = 0; t < keys.size(); ++t) {
+        const auto [p, j] = keys[t];
+        if (is_leaf) {
+          eb.add(mats[t].m, rb(lvl, p), rb(lvl, j));
+        } else {
+          cols_to_merged(gb, mats[t].m, {carried[2 * p].at({lvl, j}).m, carried[2 * p + 1].at({lvl, j}).m}, j);
+        }
+        sb.add(sys.diag_lu[p], mats[t].m, SOLVE_FULL);
+        g[keys[t]] = mats[t];
+      }
+      eb.run(c);
+      gb.run(c);
+      sb.run(c);
+    }
+    // T terms: t = Us_k^T (A_kp g), term = t Vs_j, D -= term (in p order).
+    std::vector<std::pair<int, int>> shapes;
+    for (auto [k, j, p] : triples) {
+      shapes.push_back({sys.dims[k], sys.dims[j]});
+      shapes.push_back({Ub[k].rank, sys.dims[j]});
+      shapes.push_back({Ub[k].rank, Vb[j].rank});
+    }
+    auto tm = alloc_mats(c, shapes);
+    GemmBatch g1, g2, g3;
+    for (size_t t = 0; t < triples.size(); ++t) {
+      const auto [k, j, p] = triples[t];
+      gemm1(g1, tm[3 * t].m, block(sys, k, p), g.at({p, j}).m);
+      gemm1(g2, tm[3 * t + 1].m, Ub[k].Qs().t(), tm[3 * t].m);
+      gemm1(g3, tm[3 * t + 2].m, tm[3 * t + 1].m, Vb[j].Qs());
+    }
+    g1.run(c);
+    g2.run(c);
+    g3.run(c);
+    std::vector<std::pair<int, int>> dshapes;
+    std::vector<std::pair<int64_t, int64_t>> dkeys;
+    std::map<std::pair<int64_t, int64_t>, std::vector<size_t>> terms_of;
+    for (size_t t = 0; t < triples.size(); ++t)
+      terms_of[{std::get<0>(triples[t]), std::get<1>(triples[t])}].push_back(t);
+    for (auto kj : pairs) {
+      if (!proj.count(kj) && !terms_of.count(kj)) continue;
+      dkeys.push_back(kj);
+      dshapes.push_back({Ub[kj.first].rank, Vb[kj.second].rank});
+    }
+    auto dm = alloc_mats(c, dshapes);
+    AccBatch acc;
+    for (size_t t = 0; t < dkeys.size(); ++t) {
+      acc.job(dm[t].m, true);
+      auto pi = proj.find(dkeys[t]);
+      if (pi != proj.end()) acc.src(pi->second.m, 1.0);
+      auto ti = terms_of.find(dkeys[t]);
+      if (ti != terms_of.end())
+        for (size_t x : ti->second) acc.src(tm[3 * x + 2].m, -1.0);
+      dense_ss[dkeys[t]] = dm[t];
+    }
+    acc.run(c);
+  }
+
+  // ---- eliminate_level (ulv.cpp:25-48, :609-630) --------------------------------
+  void eliminate_level(SysL& sys, std::vector<DMat>& diag_S, LevelF& lf) {
+    PhaseTimer pt(c, P.stats, "factorize");
+    const int64_t m = sys.m;
+    lf.elim.assign(m, {});
+    std::vector<int> rr;
+    std::vector<std::pair<int, int>> shapes;
+    for (int64_t k = 0; k < m; ++k) {
+      const int rank = P.U[sys.lvl][k].rank;
+      const int rdim = sys.dims[k] - rank, sdim = rank;
+      lf.elim[k].rdim = rdim;
+      lf.elim[k].sdim = sdim;
+      rr.push_back(rdim);
+      shapes.push_back({rdim, sdim});
+      shapes.push_back({sdim, rdim});
+    }
+    auto lus = alloc_lus(c, rr);
+    auto mats = alloc_mats(c, shapes);
+    CopyBatch cb;
+    LuBatch lb;
+    for (int64_t k = 0; k < m; ++k) {
+      ElimF& e = lf.elim[k];
+      e.piv = lus[k];
+      e.urs = mats[2 * k];
+      e.lsr = mats[2 * k + 1];
+      if (e.rdim == 0) continue;
+      const Mat Sk = diag_S[k].m;
+      cb.copy(e.piv.lu.m, Sk.sub(0, 0, e.rdim, e.rdim));
+      if (e.sdim) {
+        cb.copy(e.urs.m, Sk.sub(0, e.rdim, e.rdim, e.sdim));
+        cb.copy(e.lsr.m, Sk.sub(e.rdim, 0, e.sdim, e.rdim));
+      }
+      lb.add(e.piv, opt.rr_pivot_tol, "S^RR");
+    }
+    cb.run(c);
+    lb.run(c);
+    SolveBatch s1;
+    GemmBatch gb;
+    for (int64_t k = 0; k < m; ++k) {
+      ElimF& e = lf.elim[k];
+      if (e.rdim == 0 || e.sdim == 0) continue;
+      s1.add(e.piv, e.urs.m, SOLVE_LOWER);
+      s1.add(e.piv, e.lsr.m, SOLVE_UPPER_RIGHT);
+      gb.job(diag_S[k].m.sub(e.rdim, e.rdim, e.sdim, e.sdim), true);
+      gb.seg(e.lsr.m, e.urs.m, -1.0);
+    }
+    s1.run(c);
+    gb.run(c);
+  }
+
+  // ---- merge (ulv.cpp:632-671) ---------------------------------------------------
+  SysL merge(const SysL& sys, const std::vector<DMat>& diag_S,
+             const std::map<std::pair<int64_t, int64_t>, DMat>& far_ss,
+             const std::map<std::pair<int64_t, int64_t>, DMat>& dense_ss) {
+    PhaseTimer pt(c, P.stats, "factorize");
+    const int lvl = sys.lvl;
+    const int64_t mp = int64_t(1) << (lvl - 1);
+    SysL next;
+    next.lvl = lvl - 1;
+    next.m = int(mp);
+    next.dims.resize(mp);
+    const auto& Ub = P.U[lvl];
+    for (int64_t I = 0; I < mp; ++I) next.dims[I] = Ub[2 * I].rank + Ub[2 * I + 1].rank;
+    std::vector<std::pair<int, int>> shapes;
+    const auto& LP = S.level[lvl - 1];
+    for (int64_t I = 0; I < mp; ++I)
+      for (int64_t t = LP.near_ptr[I]; t < LP.near_ptr[I + 1]; ++t)
+        shapes.push_back({next.dims[I], next.dims[LP.near_idx[t]]});
+    next.blocks = alloc_mats(c, shapes);
+    CopyBatch cb;
+    for (int64_t I = 0; I < mp; ++I)
+      for (int64_t t = LP.near_ptr[I]; t < LP.near_ptr[I + 1]; ++t) {
+        const int64_t J = LP.near_idx[t];
+        const Mat B = next.blocks[t].m;
+        for (int a = 0; a < 2; ++a)
+          for (int b = 0; b < 2; ++b) {
+            const int64_t ci = 2 * I + a, cj = 2 * J + b;
+            const int r0 = a == 0 ? 0 : Ub[2 * I].rank;
+            const int c0 = b == 0 ? 0 : Ub[2 * J].rank;
+            const int nr = Ub[ci].rank, nc = Ub[cj].rank;
+            if (nr == 0 || nc == 0) continue;
+            const Mat dst = B.sub(r0, c0, nr, nc);
+            if (ci == cj) {
+              const int rd = diag_S[ci].rows() - nr;
+              cb.copy(dst, diag_S[ci].m.sub(rd, rd, nr, nr));
+            } else if (far_ss.count({ci, cj})) {
+              cb.copy(dst, far_ss.at({ci, cj}).m);
+            } else if (dense_ss.count({ci, cj})) {
+              cb.copy(dst, dense_ss.at({ci, cj}).m);
+            } else {
+              cb.zero(dst);
+            }
+          }
+      }
+    cb.run(c);
+    next.offdiag = false;
+    for (int64_t I = 0; I < mp && !next.offdiag; ++I)
+      for (int64_t t = LP.near_ptr[I]; t < LP.near_ptr[I + 1]; ++t)
+        if (LP.near_idx[t] != I) next.offdiag = true;
+    return next;
+  }
+
+  // ---- assemble_top_nodep (ulv.cpp:691-708) --------------------------------------
+  void assemble_top(SysL& sys) {
+    PhaseTimer pt(c, P.stats, "factorize");
+    const int lvl = sys.lvl;
+    const int64_t m = sys.m;
+    P.cutoff_level = lvl;
+    P.cutoff_dims = sys.dims;
+    std::vector<int64_t> off(m + 1, 0);
+    for (int64_t k = 0; k < m; ++k) off[k + 1] = off[k] + sys.dims[k];
+    P.top = alloc_lu(c, int(off[m]));
+    const Mat A = P.top.lu.m;
+    CopyBatch zb, cb;
+    GemmBatch gb;
+    zb.zero(A);
+    for (int64_t i = 0; i < m; ++i) {
+      for (int64_t t = 0; t < S.nnear(lvl, i); ++t) {
+        const int64_t j = S.near(lvl, i)[t];
+        if (sys.dims[i] && sys.dims[j])
+          cb.copy(A.sub(int(off[i]), int(off[j]), sys.dims[i], sys.dims[j]), block(sys, i, j));
+      }
+      for (int64_t t = 0; t < S.nfar(lvl, i); ++t) {
+        const int64_t j = S.far(lvl, i)[t];
+        cols_to_merged(gb, A.sub(int(off[i]), int(off[j]), sys.dims[i], sys.dims[j]),
+                       {carried[2 * i].at({lvl, j}).m, carried[2 * i + 1].at({lvl, j}).m}, j);
+      }
+    }
+    zb.run(c);
+    cb.run(c);
+    gb.run(c);
+    LuBatch lb;
+    lb.add(P.top, 1e-15, "top system");
+    lb.run(c);
+  }
+
+  // ---- lift_layer (compression.cpp:302-322) --------------------------------------
+  void make_layer(int lvl) {
+    const int64_t m = int64_t(1) << lvl;
+    std::vector<Mat> nu(m), nv(m);
+    if (lvl == L) {
+      for (int64_t i = 0; i < m; ++i) {
+        nu[i] = P.U[L][i].Qs();
+        nv[i] = P.V[L][i].Qs();
+      }
+      big_owner.clear();
+    } else {
+      std::vector<std::pair<int, int>> shapes;
+      for (int64_t k = 0; k < m; ++k) {
+        shapes.push_back({int(rs(lvl, k)), P.U[lvl][k].rank});
+        shapes.push_back({int(rs(lvl, k)), P.V[lvl][k].rank});
+      }
+      auto mats = alloc_mats(c, shapes);
+      GemmBatch gb;
+      for (int64_t k = 0; k < m; ++k) {
+        for (int side = 0; side < 2; ++side) {
+          const Mat Tq = side == 0 ? P.U[lvl][k].Qs() : P.V[lvl][k].Qs();
+          const auto& child = side == 0 ? Ubig : Vbig;
+          const Mat u0 = child[2 * k], u1 = child[2 * k + 1];
+          const Mat out = mats[2 * k + side].m;
+          if (Tq.cols == 0) continue;
+          gemm1(gb, out.sub(0, 0, u0.rows, Tq.cols), u0, Tq.sub(0, 0, u0.cols, Tq.cols));
+          gemm1(gb, out.sub(u0.rows, 0, u1.rows, Tq.cols), u1, Tq.sub(u0.cols, 0, u1.cols, Tq.cols));
+        }
+        nu[k] = mats[2 * k].m;
+        nv[k] = mats[2 * k + 1].m;
+      }
+      gb.run(c);
+      std::vector<DMat> keep = std::move(mats);
+      big_owner_next_ = std::move(keep);
+    }
+    Ubig = std::move(nu);
+    Vbig = std::move(nv);
+  }
+  std::vector<DMat> big_owner_next_;
+
+  // ---- NodepDriver::run (ulv.cpp:710-760) -----------------------------------------
+  void run() {
+    SysL sys;
+    sys.lvl = L;
+    sys.m = 1 << L;
+    sys.dims.resize(sys.m);
+    for (int64_t i = 0; i < sys.m; ++i) sys.dims[i] = int(rs(L, i));
+    sys.blocks = P.near;
+    sys.offdiag = false;
+    for (int64_t i = 0; i < sys.m && !sys.offdiag; ++i)
+      for (int64_t t = 0; t < S.nnear(L, i); ++t)
+        if (S.near(L, i)[t] != i) sys.offdiag = true;
+    P.U.assign(L + 1, {});
+    P.V.assign(L + 1, {});
+    for (int l = 0; l <= L; ++l) {
+      P.U[l].resize(size_t(1) << l);
+      P.V[l].resize(size_t(1) << l);
+    }
+    // prepare_factor_inputs (ulv.cpp:1108-1126)
+    FillSet fills;
+    if (opt.structure == 0 && sys.offdiag) fills = precompute_fillins(sys);
+    FillSet basis_fills;
+    for (auto& [k, F] : fills)
+      if (k.first != k.second) basis_fills[k] = F;
+    build_leaf_bases(sys, basis_fills);
+
+    while (true) {
+      const bool is_leaf = sys.lvl == L;
+      std::vector<PieceMap> pieces, stack, merged;
+      P.max_fill_resid.push_back(0.0);
+      double* lm = &P.max_fill_resid.back();
+      if (is_leaf) {
+        build_leaf_pieces(sys, fills, pieces, lm);
+      } else {
+        fills = precompute_fillins(sys);
+        build_upper_pieces(sys, fills, stack, merged);
+        build_transfers(sys, fills, merged);
+      }
+      std::vector<DMat> diag_S;
+      std::map<std::pair<int64_t, int64_t>, DMat> far_ss, dense_ss;
+      assemble_level(sys, fills, pieces, merged, diag_S, far_ss, dense_ss, lm);
+      LevelF lf;
+      lf.level = sys.lvl;
+      lf.dims = sys.dims;
+      lf.ranks.resize(sys.m);
+      for (int64_t k = 0; k < sys.m; ++k) lf.ranks[k] = P.U[sys.lvl][k].rank;
+      eliminate_level(sys, diag_S, lf);
+      lf.use_z = sys.offdiag;
+      // project_pieces (ulv.cpp:675-689)
+      {
+        PhaseTimer pt(c, P.stats, "skeleton");
+        std::vector<PieceMap> next(sys.m);
+        GemmBatch gb;
+        std::vector<std::pair<int64_t, TargetKey>> keys;
+        std::vector<std::pair<int, int>> shapes;
+        const auto& src = is_leaf ? pieces : merged;
+        for (int64_t k = 0; k < sys.m; ++k)
+          for (auto& [tk, piece] : src[k]) {
+            if (tk.first == sys.lvl) continue;
+            if (is_leaf) {
+              next[k][tk] = piece;
+            } else {
+              keys.push_back({k, tk});
+              shapes.push_back({P.U[sys.lvl][k].rank, piece.cols()});
+            }
+          }
+        auto mats = alloc_mats(c, shapes);
+        for (size_t t = 0; t < keys.size(); ++t) {
+          const auto [k, tk] = keys[t];
+          gemm1(gb, mats[t].m, P.U[sys.lvl][k].Qs().t(), src[k].at(tk).m);
+          next[k][tk] = mats[t];
+        }
+        gb.run(c);
+        carried = std::move(next);
+      }
+      make_layer(sys.lvl);
+      big_owner = std::move(big_owner_next_);
+      SysL next = merge(sys, diag_S, far_ss, dense_ss);
+      lf.sys = std::move(sys);
+      P.levels.push_back(std::move(lf));
+      const int next_lvl = next.lvl;
+      int64_t total = 0;
+      for (int d : next.dims) total += d;
+      if (next_lvl <= 1 || total <= 4 * P.T.leaf) {
+        assemble_top(next);
+        break;
+      }
+      sys = std::move(next);
+    }
+  }
+};
+
+}  // namespace
+
+void Problem::factor() {
+  if (!built) throw std::logic_error("Pipeline::factor: build() first");
+  if (factored) return;
+  const double t0 = now_s();
+  c.phase_flops.clear();
+  levels.clear();
+  max_fill_resid.clear();
+  Driver d(*this);
+  d.run();
+  c.sync();
+  stats.t_factor = now_s() - t0;
+  for (auto& [k, v] : c.phase_flops) stats.phase_flops[k] += v;
+  stats.launches = c.launches;
+  stats.max_fill_residual = 0;
+  for (double r : max_fill_resid) stats.max_fill_residual = std::max(stats.max_fill_residual, r);
+  factored = true;
+}
+
+void Problem::matvec(const double* d_x, double* d_y, int nrhs) {
+  if (!built) throw std::logic_error("matvec: build() first");
+  Slab flag = c.alloc(sizeof(int));
+  cuda_check(cudaMemsetAsync(flag.get(), 0, sizeof(int), c.stream), "memset");
+  launch_matvec(c.kp, orig, d_x, d_y, nrhs, static_cast<int*>(flag.get()), c.stream);
+  int h = 0;
+  cuda_check(cudaMemcpyAsync(&h, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, c.stream), "flag");
+  c.sync();
+  if (h) throw std::runtime_error("assemble_block: singular evaluation (r + eta_reg == 0)");
+}
+
+// ---- solve (solve.cpp:17-224), all right-hand sides at once -------------------
+void Problem::solve(const double* d_b, double* d_x, int nrhs) {
+  if (!factored) throw std::logic_error("Pipeline::solve_rhs: factor() first");
+  const double t0 = now_s();
+  const int64_t n = T.n;
+  const int L = T.levels;
+  const std::string saved_phase = c.phase;
+  c.phase = "solve";
+  DMat bp = alloc_mat(c, int(n), nrhs);
+  launch_permute_rows(bp.m, Mat{const_cast<double*>(d_b), int(n), nrhs, 1, n}, T.order, 0, c.stream);
+  // r[k]: leaf segments (views).
+  std::vector<Mat> r(size_t(1) << L);
+  for (int64_t k = 0; k < (int64_t(1) << L); ++k)
+    r[k] = bp.m.sub(int(range_begin(L, k)), 0, int(range_size(L, k)), nrhs);
+  std::vector<std::vector<DMat>> z_all(levels.size());
+  std::vector<DMat> keep;
+  for (size_t li = 0; li < levels.size(); ++li) {
+    const LevelF& lf = levels[li];
+    const int lvl = lf.level;
+    const int64_t m = int64_t(lf.dims.size());
+    std::vector<Mat> rt = r;
+    if (lf.use_z) {
+      std::vector<std::pair<int, int>> shapes;
+      for (int64_t p = 0; p < m; ++p) shapes.push_back({lf.dims[p], nrhs});
+      for (int64_t k = 0; k < m; ++k) shapes.push_back({lf.dims[k], nrhs});
+      std::vector<std::pair<int64_t, int64_t>> prods;
+      for (int64_t k = 0; k < m; ++k)
+        for (int64_t t = 0; t < S.nnear(lvl, k); ++t)
+          if (S.near(lvl, k)[t] != k) {
+            prods.push_back({k, S.near(lvl, k)[t]});
+            shapes.push_back({lf.dims[k], nrhs});
+          }
+      auto mats = alloc_mats(c, shapes);
+      CopyBatch cb;
+      SolveBatch sb;
+      for (int64_t p = 0; p < m; ++p) {
+        cb.copy(mats[p].m, r[p]);
+        sb.add(lf.sys.diag_lu[p], mats[p].m, SOLVE_FULL);
+      }
+      cb.run(c);
+      sb.run(c);
+      GemmBatch gb;
+      for (size_t t = 0; t < prods.size(); ++t) {
+        const auto [k, p] = prods[t];
+        const int tt = Driver::find_near(S, lvl, k, p);
+        gemm1(gb, mats[2 * m + t].m, lf.sys.blocks[tt].m, mats[p].m);
+      }
+      gb.run(c);
+      AccBatch acc;
+      size_t t = 0;
+      for (int64_t k = 0; k < m; ++k) {
+        acc.job(mats[m + k].m, true);
+        acc.src(r[k], 1.0);
+        for (; t < prods.size() && prods[t].first == k; ++t) acc.src(mats[2 * m + t].m, -1.0);
+        rt[k] = mats[m + k].m;
+      }
+      acc.run(c);
+      keep.insert(keep.end(), mats.begin(), mats.end());
+    }
+    // c = [Ur Us]^T rt; z = L^-1 P c_R; s = c_S - L^SR z.
+    std::vector<std::pair<int, int>> shapes;
+    for (int64_t k = 0; k < m; ++k) {
+      shapes.push_back({lf.dims[k], nrhs});
+      shapes.push_back({lf.elim[k].sdim, nrhs});
+    }
+    auto mats = alloc_mats(c, shapes);
+    GemmBatch g1, g2;
+    SolveBatch sb;
+    AccBatch acc;
+    z_all[li].resize(m);
+    std::vector<Mat> s(m);
+    for (int64_t k = 0; k < m; ++k) {
+      const ElimF& el = lf.elim[k];
+      const Mat cvec = mats[2 * k].m;
+      gemm1(g1, cvec, U[lvl][k].SQ.m.t(), rt[k]);
+      const Mat z = cvec.sub(0, 0, el.rdim, nrhs);
+      if (el.rdim > 0) sb.add(el.piv, z, SOLVE_LOWER);
+      s[k] = cvec.sub(el.rdim, 0, el.sdim, nrhs);
+      if (el.rdim > 0 && el.sdim > 0) {
+        gemm1(g2, mats[2 * k + 1].m, el.lsr.m, z);
+        acc.job(s[k], false);
+        acc.src(mats[2 * k + 1].m, -1.0);
+      }
+      z_all[li][k] = DMat{z, mats[2 * k].owner};
+    }
+    g1.run(c);
+    sb.run(c);
+    g2.run(c);
+    acc.run(c);
+    keep.insert(keep.end(), mats.begin(), mats.end());
+    // Stack skeleton parts for the next system.
+    const int64_t mp = m / 2;
+    std::vector<std::pair<int, int>> pshapes;
+    for (int64_t I = 0; I < mp; ++I) pshapes.push_back({s[2 * I].rows + s[2 * I + 1].rows, nrhs});
+    auto nr = alloc_mats(c, pshapes);
+    CopyBatch cb;
+    std::vector<Mat> rn(mp);
+    for (int64_t I = 0; I < mp; ++I) {
+      if (s[2 * I].rows) cb.copy(nr[I].m.sub(0, 0, s[2 * I].rows, nrhs), s[2 * I]);
+      if (s[2 * I + 1].rows) cb.copy(nr[I].m.sub(s[2 * I].rows, 0, s[2 * I + 1].rows, nrhs), s[2 * I + 1]);
+      rn[I] = nr[I].m;
+    }
+    cb.run(c);
+    keep.insert(keep.end(), nr.begin(), nr.end());
+    r = std::move(rn);
+  }
+  // Top dense solve.
+  const int tn = top.n();
+  DMat y = alloc_mat(c, tn, nrhs);
+  {
+    CopyBatch cb;
+    int at = 0;
+    for (auto& piece : r) {
+      if (piece.rows) cb.copy(y.m.sub(at, 0, piece.rows, nrhs), piece);
+      at += piece.rows;
+    }
+    cb.run(c);
+    SolveBatch sb;
+    sb.add(top, y.m, SOLVE_FULL);
+    sb.run(c);
+  }
+  std::vector<Mat> ys;
+  {
+    int at = 0;
+    for (int d : cutoff_dims) {
+      ys.push_back(y.m.sub(at, 0, d, nrhs));
+      at += d;
+    }
+  }
+  // Downward pass.
+  for (int64_t li = int64_t(levels.size()) - 1; li >= 0; --li) {
+    const LevelF& lf = levels[li];
+    const int lvl = lf.level;
+    const int64_t m = int64_t(lf.dims.size());
+    std::vector<std::pair<int, int>> shapes;
+    for (int64_t k = 0; k < m; ++k) {
+      shapes.push_back({lf.elim[k].rdim, nrhs});
+      shapes.push_back({lf.dims[k], nrhs});
+    }
+    auto mats = alloc_mats(c, shapes);
+    GemmBatch g1, g2;
+    AccBatch acc;
+    SolveBatch sb;
+    std::vector<Mat> yfull(m);
+    for (int64_t k = 0; k < m; ++k) {
+      const ElimF& el = lf.elim[k];
+      const int64_t parent = k >> 1;
+      const int off = (k & 1) ? lf.ranks[k - 1] : 0;
+      const Mat yskel = ys[parent].sub(off, 0, lf.ranks[k], nrhs);
+      const Mat yr = z_all[li][k].m;
+      if (el.rdim > 0) {
+        if (el.sdim > 0) {
+          gemm1(g1, mats[2 * k].m, el.urs.m, yskel);
+          acc.job(yr, false);
+          acc.src(mats[2 * k].m, -1.0);
+        }
+        sb.add(el.piv, yr, SOLVE_UPPER);
+      }
+      // x_k = [V_r V_s] [y_R; y_S] as one product over the stacked vector.
+      const Basis& Vk = V[lvl][k];
+      g2.job(mats[2 * k + 1].m, false);
+      if (el.rdim > 0) g2.seg(Vk.SQ.m.sub(0, 0, Vk.dim, el.rdim), yr);
+      if (el.sdim > 0) g2.seg(Vk.SQ.m.sub(0, el.rdim, Vk.dim, el.sdim), yskel);
+      yfull[k] = mats[2 * k + 1].m;
+    }
+    g1.run(c);
+    acc.run(c);
+    sb.run(c);
+    g2.run(c);
+    keep.insert(keep.end(), mats.begin(), mats.end());
+    ys = std::move(yfull);
+  }
+  // Leaf segments back to the original ordering.
+  DMat xp = alloc_mat(c, int(n), nrhs);
+  {
+    CopyBatch cb;
+    for (int64_t k = 0; k < (int64_t(1) << L); ++k)
+      if (ys[k].rows) cb.copy(xp.m.sub(int(range_begin(L, k)), 0, ys[k].rows, nrhs), ys[k]);
+    cb.run(c);
+  }
+  launch_permute_rows(Mat{d_x, int(n), nrhs, 1, n}, xp.m, T.order, 1, c.stream);
+  c.sync();
+  c.phase = saved_phase;
+  stats.t_solve = now_s() - t0;
+}
+
+}  // namespace h2g

@@ -1,0 +1,174 @@
+// Batched kernel-block evaluation (near-field arena, solve inputs, basis
+// members), batched strided copies/adds, and sequential Frobenius norms.
+#include "kernels.hpp"
+
+namespace h2g {
+
+namespace {
+
+constexpr int T = 64, NT = 256;
+
+// assemble_block (kernels.cpp:242-268) over 64x64 tiles; rows fastest so a
+// column-major destination is written coalesced. The near-field arena write
+// is the HBM-bound phase (8 B per entry).
+__global__ void __launch_bounds__(NT) eval_kernel(const EvalJob* __restrict__ jobs,
+                                                  const int* __restrict__ tile_job,
+                                                  const int* __restrict__ tile_idx,
+                                                  KernelParams kp, Cloud cloud, ErrWord* err,
+                                                  int tag) {
+  const int jb = tile_job[blockIdx.x];
+  const EvalJob job = jobs[jb];
+  const int tpr = (job.out.rows + T - 1) / T;
+  const int ti = tile_idx[blockIdx.x];
+  const int r0 = (ti % tpr) * T, c0 = (ti / tpr) * T;
+  int singular = 0;
+  for (int e = threadIdx.x; e < T * T; e += NT) {
+    const int i = r0 + (e % T), j = c0 + (e / T);
+    if (i < job.out.rows && j < job.out.cols)
+      job.out.at(i, j) = kernel_entry(kp, cloud, job.rb + i, job.cb + j, &singular);
+  }
+  if (singular) raise_err(err, 1, jb, 0, tag);
+}
+
+// dst = (add ? dst : 0) + alpha * src  — the reference's add_block computes
+// dst[i] += alpha * src[i], contracted to fma(alpha, src, dst).
+__global__ void __launch_bounds__(NT) copy_kernel(const CopyJob* __restrict__ jobs,
+                                                  const int* __restrict__ tile_job,
+                                                  const int* __restrict__ tile_idx) {
+  const CopyJob job = jobs[tile_job[blockIdx.x]];
+  const int tpr = (job.dst.rows + T - 1) / T;
+  const int ti = tile_idx[blockIdx.x];
+  const int r0 = (ti % tpr) * T, c0 = (ti / tpr) * T;
+  for (int e = threadIdx.x; e < T * T; e += NT) {
+    const int i = r0 + (e % T), j = c0 + (e / T);
+    if (i >= job.dst.rows || j >= job.dst.cols) continue;
+    double v;
+    if (job.src.p == nullptr) {
+      v = job.ident ? (i == j ? 1.0 : 0.0) : 0.0;
+      if (job.add) v = job.dst.at(i, j);
+    } else if (job.add) {
+      v = fma(job.alpha, job.src.at(i, j), job.dst.at(i, j));
+    } else {
+      v = job.alpha == 1.0 ? job.src.at(i, j) : job.alpha * job.src.at(i, j);
+    }
+    job.dst.at(i, j) = v;
+  }
+}
+
+__global__ void __launch_bounds__(NT) accum_kernel(const AccJob* __restrict__ jobs,
+                                                   const AccSrc* __restrict__ srcs,
+                                                   const int* __restrict__ tile_job,
+                                                   const int* __restrict__ tile_idx) {
+  const AccJob job = jobs[tile_job[blockIdx.x]];
+  const int tpr = (job.dst.rows + T - 1) / T;
+  const int ti = tile_idx[blockIdx.x];
+  const int r0 = (ti % tpr) * T, c0 = (ti / tpr) * T;
+  for (int e = threadIdx.x; e < T * T; e += NT) {
+    const int i = r0 + (e % T), j = c0 + (e / T);
+    if (i >= job.dst.rows || j >= job.dst.cols) continue;
+    double v = job.zero_init ? 0.0 : job.dst.at(i, j);
+    for (int s = 0; s < job.nsrc; ++s) {
+      const AccSrc sr = srcs[job.src0 + s];
+      v = fma(sr.alpha, sr.src.at(i, j), v);
+    }
+    job.dst.at(i, j) = v;
+  }
+}
+
+__global__ void permute_rows_kernel(Mat dst, Mat src, const int64_t* idx, int scatter) {
+  const int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t rows = scatter ? src.rows : dst.rows;
+  if (e >= rows * dst.cols) return;
+  const int64_t i = e % rows, j = e / rows;
+  if (scatter) dst.at(idx[i], j) = src.at(i, j);
+  else dst.at(i, j) = src.at(idx[i], j);
+}
+
+// norm_frobenius (linalg.cpp:604-609): s += d*d over storage order, one
+// thread per matrix so the rounding sequence is the reference's.
+__global__ void norms_kernel(const NormJob* __restrict__ jobs, int njobs) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= njobs) return;
+  const NormJob job = jobs[t];
+  double s = 0.0;
+  for (int j = 0; j < job.a.cols; ++j)
+    for (int i = 0; i < job.a.rows; ++i) {
+      const double d = job.a.at(i, j);
+      s = fma(d, d, s);
+    }
+  *job.out = sqrt(s);
+}
+
+// y = A x by direct summation in the ORIGINAL point order, each y_i
+// accumulated over j in order like matmul(A, x) (solve.cpp:234-239).
+__global__ void __launch_bounds__(256) matvec_kernel(KernelParams kp, Cloud c, const double* x,
+                                                     double* y, int nrhs, int* singular) {
+  __shared__ double sx[256], sy[256], sz[256], sq[256];
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const bool live = i < c.n;
+  double acc[4] = {0, 0, 0, 0};
+  const double xi = live ? c.x[i] : 0.0, yi = live ? c.y[i] : 0.0, zi = live ? c.z[i] : 0.0;
+  int sing = 0;
+  for (int r0 = 0; r0 < nrhs; r0 += 4) {
+    const int nr = min(4, nrhs - r0);
+    for (int a = 0; a < 4; ++a) acc[a] = 0.0;
+    for (int64_t j0 = 0; j0 < c.n; j0 += 256) {
+      __syncthreads();
+      const int64_t jj = j0 + threadIdx.x;
+      if (jj < c.n) {
+        sx[threadIdx.x] = c.x[jj];
+        sy[threadIdx.x] = c.y[jj];
+        sz[threadIdx.x] = c.z[jj];
+        sq[threadIdx.x] = c.q[jj];
+      }
+      __syncthreads();
+      const int cnt = int(c.n - j0 < 256 ? c.n - j0 : 256);
+      if (!live) continue;
+      for (int t = 0; t < cnt; ++t) {
+        const double dx = xi - sx[t], dy = yi - sy[t], dz = zi - sz[t];
+        const double r = sqrt(fma(dz, dz, fma(dx, dx, dy * dy)));
+        const double denom = kp.scale * (r + kp.reg);
+        if (denom == 0.0) sing = 1;
+        const double a = kp.kind == 0 ? sq[t] / denom : sq[t] * exp(-kp.alpha_m * r) / denom;
+        for (int q = 0; q < nr; ++q) acc[q] = fma(a, x[(r0 + q) * c.n + j0 + t], acc[q]);
+      }
+    }
+    if (live)
+      for (int q = 0; q < nr; ++q) y[(r0 + q) * c.n + i] = acc[q];
+  }
+  if (sing) *singular = 1;
+}
+
+}  // namespace
+
+void launch_matvec(KernelParams kp, Cloud c, const double* x, double* y, int nrhs, int* singular,
+                   cudaStream_t st) {
+  if (c.n > 0) matvec_kernel<<<unsigned((c.n + 255) / 256), 256, 0, st>>>(kp, c, x, y, nrhs, singular);
+}
+
+void launch_eval(const EvalJob* jobs, const int* tile_job, const int* tile_idx, int ntiles,
+                 KernelParams kp, Cloud cloud, ErrWord* err, int tag, cudaStream_t st) {
+  if (ntiles > 0) eval_kernel<<<ntiles, NT, 0, st>>>(jobs, tile_job, tile_idx, kp, cloud, err, tag);
+}
+
+void launch_copy(const CopyJob* jobs, const int* tile_job, const int* tile_idx, int ntiles,
+                 cudaStream_t st) {
+  if (ntiles > 0) copy_kernel<<<ntiles, NT, 0, st>>>(jobs, tile_job, tile_idx);
+}
+
+void launch_accum(const AccJob* jobs, const AccSrc* srcs, const int* tile_job, const int* tile_idx,
+                  int ntiles, cudaStream_t st) {
+  if (ntiles > 0) accum_kernel<<<ntiles, NT, 0, st>>>(jobs, srcs, tile_job, tile_idx);
+}
+
+void launch_permute_rows(Mat dst, Mat src, const int64_t* idx, int scatter, cudaStream_t st) {
+  const int64_t rows = scatter ? src.rows : dst.rows;
+  const int64_t tot = rows * dst.cols;
+  if (tot > 0) permute_rows_kernel<<<unsigned((tot + 255) / 256), 256, 0, st>>>(dst, src, idx, scatter);
+}
+
+void launch_norms(const NormJob* jobs, int njobs, cudaStream_t st) {
+  if (njobs > 0) norms_kernel<<<(njobs + 127) / 128, 128, 0, st>>>(jobs, njobs);
+}
+
+}  // namespace h2g

@@ -1,0 +1,236 @@
+// Batched LU with block-local partial pivoting and the LuFactors solve
+// family. One CTA per matrix (LU) or per RHS chunk (solves). Every element
+// sees the reference's exact rounding sequence (linalg.cpp:352-559), so the
+// packed factors and solutions are bitwise equal to the reference.
+#include "kernels.hpp"
+
+namespace h2g {
+
+namespace {
+
+constexpr int NT = 512;
+
+struct ValIdx {
+  double v;
+  int i;
+};
+
+// Max value; ties to the lowest index — the first strict maximum of the
+// reference's ascending scan (linalg.cpp:362-370).
+__device__ __forceinline__ ValIdx better(ValIdx a, ValIdx b) {
+  if (b.v > a.v || (b.v == a.v && b.i < a.i)) return b;
+  return a;
+}
+
+__device__ ValIdx block_argmax(ValIdx x, ValIdx* red) {
+  for (int o = 16; o > 0; o >>= 1) {
+    ValIdx y{__shfl_down_sync(0xffffffffu, x.v, o), __shfl_down_sync(0xffffffffu, x.i, o)};
+    x = better(x, y);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    x = (l < (int)(blockDim.x >> 5)) ? red[l] : ValIdx{-1.0, 0x7fffffff};
+    for (int o = 16; o > 0; o >>= 1) {
+      ValIdx y{__shfl_down_sync(0xffffffffu, x.v, o), __shfl_down_sync(0xffffffffu, x.i, o)};
+      x = better(x, y);
+    }
+    if (l == 0) red[0] = x;
+  }
+  __syncthreads();
+  ValIdx r = red[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(NT) lu_kernel(const LuJob* __restrict__ jobs, ErrWord* err,
+                                                int tag) {
+  __shared__ ValIdx red[32];
+  const LuJob job = jobs[blockIdx.x];
+  const Mat M = job.A;
+  const int n = M.rows;
+  for (int i = threadIdx.x; i < n; i += NT) job.perm[i] = i;
+  // amax = norm_max_abs(A)
+  ValIdx am{0.0, 0};
+  for (int64_t e = threadIdx.x; e < int64_t(n) * n; e += NT) {
+    const double v = fabs(M.at(e % n, e / n));
+    if (v > am.v) am.v = v;
+  }
+  const double amax = block_argmax(am, red).v;
+  for (int k = 0; k < n; ++k) {
+    ValIdx best{-1.0, 0x7fffffff};
+    for (int i = k + threadIdx.x; i < n; i += NT) best = better(best, ValIdx{fabs(M.at(i, k)), i});
+    best = block_argmax(best, red);
+    if (best.v <= job.tol * amax) {
+      if (threadIdx.x == 0) raise_err(err, 2, blockIdx.x, k, tag);
+      return;
+    }
+    const int p = best.i;
+    if (p != k) {
+      for (int j = threadIdx.x; j < n; j += NT) {
+        const double t = M.at(k, j);
+        M.at(k, j) = M.at(p, j);
+        M.at(p, j) = t;
+      }
+      if (threadIdx.x == 0) {
+        const int64_t t = job.perm[k];
+        job.perm[k] = job.perm[p];
+        job.perm[p] = t;
+      }
+      __syncthreads();
+    }
+    const double inv = 1.0 / M.at(k, k);
+    for (int i = k + 1 + threadIdx.x; i < n; i += NT) M.at(i, k) = M.at(i, k) * inv;
+    __syncthreads();
+    const int t = n - k - 1;
+    for (int64_t e = threadIdx.x; e < int64_t(t) * t; e += NT) {
+      const int i = k + 1 + int(e % t), j = k + 1 + int(e / t);
+      M.at(i, j) = fma(-M.at(i, k), M.at(k, j), M.at(i, j));
+    }
+    __syncthreads();
+  }
+}
+
+// xs is chunk-local column-major: xs[c * m + i] (left) / xs[j * nr + r] (right).
+__global__ void __launch_bounds__(256) solve_kernel(const SolveJob* __restrict__ jobs,
+                                                    const SolveChunk* __restrict__ chunks) {
+  extern __shared__ double xs[];
+  const SolveChunk ch = chunks[blockIdx.x];
+  const SolveJob job = jobs[ch.job];
+  const Mat L = job.lu;
+  const int m = L.rows;
+  const int nc = ch.nc;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const Mat X = job.X;
+  const bool right = job.kind >= SOLVE_RIGHT;
+
+  if (!right) {
+    const bool perm_in = job.kind == SOLVE_FULL || job.kind == SOLVE_LOWER;
+    for (int e = tid; e < m * nc; e += nt) {
+      const int i = e % m, c = e / m;
+      xs[c * m + i] = X.at(perm_in ? job.perm[i] : i, ch.c0 + c);
+    }
+    __syncthreads();
+    if (job.kind == SOLVE_TRANSPOSE) {
+      // A = P^T L U: U^T w = b, L^T v = w, x = P^T v (linalg.cpp:479-503).
+      for (int c = tid; c < nc; c += nt) {
+        double* x = xs + c * m;
+        for (int k = 0; k < m; ++k) {
+          double dot = 0.0;
+          for (int i = 0; i < k; ++i) dot = fma(L.at(i, k), x[i], dot);
+          x[k] = (x[k] - dot) / L.at(k, k);
+        }
+        for (int k = m - 1; k >= 0; --k) {
+          double dot = 0.0;
+          for (int i = k + 1; i < m; ++i) dot = fma(L.at(i, k), x[i], dot);
+          x[k] = x[k] - dot;
+        }
+      }
+      __syncthreads();
+      for (int e = tid; e < m * nc; e += nt) {
+        const int i = e % m, c = e / m;
+        X.at(job.perm[i], ch.c0 + c) = xs[c * m + i];
+      }
+      return;
+    }
+    if (job.kind != SOLVE_UPPER) {
+      // Forward, unit lower: x[i] -= L(i,k) * x[k].
+      for (int k = 0; k < m - 1; ++k) {
+        const int t = m - k - 1;
+        for (int e = tid; e < t * nc; e += nt) {
+          const int i = k + 1 + e % t, c = e / t;
+          xs[c * m + i] = fma(-L.at(i, k), xs[c * m + k], xs[c * m + i]);
+        }
+        __syncthreads();
+      }
+    }
+    if (job.kind != SOLVE_LOWER) {
+      // Backward: x[k] /= U(k,k); x[i] -= U(i,k) * x[k] for i < k.
+      for (int k = m - 1; k >= 0; --k) {
+        const double ukk = L.at(k, k);
+        for (int e = tid; e < (k + 1) * nc; e += nt) {
+          const int i = e % (k + 1), c = e / (k + 1);
+          const double xk = xs[c * m + k] / ukk;
+          if (i < k) xs[c * m + i] = fma(-L.at(i, k), xk, xs[c * m + i]);
+        }
+        __syncthreads();
+        for (int c = tid; c < nc; c += nt) xs[c * m + k] = xs[c * m + k] / ukk;
+        __syncthreads();
+      }
+    }
+    for (int e = tid; e < m * nc; e += nt) {
+      const int i = e % m, c = e / m;
+      X.at(i, ch.c0 + c) = xs[c * m + i];
+    }
+    return;
+  }
+
+  // Right solves over a chunk of X rows [c0, c0 + nc).
+  const int nr = nc;
+  for (int e = tid; e < m * nr; e += nt) {
+    const int r = e % nr, j = e / nr;
+    xs[j * nr + r] = X.at(ch.c0 + r, j);
+  }
+  __syncthreads();
+  // X <- X U^-1 (linalg.cpp:441-451 / :547-557).
+  for (int k = 0; k < m; ++k) {
+    const double inv = 1.0 / L.at(k, k);
+    for (int r = tid; r < nr; r += nt) xs[k * nr + r] = xs[k * nr + r] * inv;
+    __syncthreads();
+    const int t = m - k - 1;
+    for (int e = tid; e < t * nr; e += nt) {
+      const int r = e % nr, j = k + 1 + e / nr;
+      const double ukj = L.at(k, j);
+      if (ukj != 0.0) xs[j * nr + r] = fma(-ukj, xs[k * nr + r], xs[j * nr + r]);
+    }
+    __syncthreads();
+  }
+  if (job.kind == SOLVE_RIGHT) {
+    // X <- X L^-1, then undo the row permutation on the columns.
+    for (int k = m - 1; k >= 1; --k) {
+      for (int e = tid; e < k * nr; e += nt) {
+        const int r = e % nr, j = e / nr;
+        const double lkj = L.at(k, j);
+        if (lkj != 0.0) xs[j * nr + r] = fma(-lkj, xs[k * nr + r], xs[j * nr + r]);
+      }
+      __syncthreads();
+    }
+    for (int e = tid; e < m * nr; e += nt) {
+      const int r = e % nr, k = e / nr;
+      X.at(ch.c0 + r, job.perm[k]) = xs[k * nr + r];
+    }
+    return;
+  }
+  for (int e = tid; e < m * nr; e += nt) {
+    const int r = e % nr, j = e / nr;
+    X.at(ch.c0 + r, j) = xs[j * nr + r];
+  }
+}
+
+}  // namespace
+
+void launch_lu(const LuJob* jobs, int njobs, ErrWord* err, int tag, cudaStream_t st) {
+  if (njobs > 0) lu_kernel<<<njobs, NT, 0, st>>>(jobs, err, tag);
+}
+
+int solve_chunk_width(int m) {
+  int w = 24000 / (m > 0 ? m : 1);
+  if (w > 256) w = 256;
+  return w < 1 ? 1 : w;
+}
+
+void launch_solve(const SolveJob* jobs, const SolveChunk* chunks, int nchunks,
+                  size_t smem_doubles, cudaStream_t st) {
+  if (nchunks <= 0) return;
+  const size_t smem = sizeof(double) * (smem_doubles > 0 ? smem_doubles : 1);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  solve_kernel<<<nchunks, 256, smem, st>>>(jobs, chunks);
+}
+
+}  // namespace h2g

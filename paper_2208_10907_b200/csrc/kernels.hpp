@@ -1,0 +1,145 @@
+// Host-visible descriptors and launchers of the batched sm_100a kernels.
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+
+namespace h2g {
+
+// ---- batched GEMM (k_gemm.cu) ---------------------------------------------
+// C = [acc ? C : 0] + sum_s A_s * (alpha_s * B_s), each C element accumulated
+// with fma over the segments in order and over k in order: the reference's
+// gemm_core / gemm_acc order (linalg.cpp:17-62, :86-126).
+// B may be generated on the fly from the kernel function (fused
+// evaluate-and-project; never materialises far-field blocks):
+//   trans = 0: B(l, j) = K(x[rb + l], x[cb + j]) (q of cb + j)
+//   trans = 1: B(l, j) = K(x[rb + j], x[cb + l]) (q of cb + l)
+// with columns inside mask ranges [a, b) forced to zero (the column zeroing
+// of ulv.cpp:365-371 / :433-440).
+struct GenB {
+  int64_t rb = 0, cb = 0;
+  int trans = 0;
+  int nmask = 0;
+  const int2* mask = nullptr;  // device pointer
+};
+struct GemmSeg {
+  Mat A, B;
+  double alpha = 1.0;
+  int gen = 0;
+  GenB g;
+};
+struct GemmJob {
+  Mat C;
+  int seg0 = 0, nseg = 0;
+  int acc = 0;
+};
+struct GemmTile {
+  int job, tm, tn;
+};
+void launch_gemm(const GemmJob* jobs, const GemmSeg* segs, const GemmTile* tiles, int ntiles,
+                 KernelParams kp, Cloud cloud, ErrWord* err, int tag, cudaStream_t st);
+
+// ---- batched kernel-block evaluation (k_eval.cu) ---------------------------
+// out(i, j) = K(x[rb + i], x[cb + j]) (assemble_block, kernels.cpp:242-268).
+struct EvalJob {
+  Mat out;
+  int64_t rb, cb;
+};
+void launch_eval(const EvalJob* jobs, const int* tile_job, const int* tile_idx, int ntiles,
+                 KernelParams kp, Cloud cloud, ErrWord* err, int tag, cudaStream_t st);
+
+// ---- batched copies / adds / zero-fills (k_eval.cu) -----------------------
+// dst = (add ? dst : 0) + alpha * src (add_block alpha form, matrix.cpp:55-64);
+// src.p == nullptr means zero-fill (or identity when ident = 1).
+struct CopyJob {
+  Mat dst, src;
+  double alpha = 1.0;
+  int add = 0;
+  int ident = 0;
+};
+void launch_copy(const CopyJob* jobs, const int* tile_job, const int* tile_idx, int ntiles,
+                 cudaStream_t st);
+
+// ---- ordered accumulation: dst = (zero ? 0 : dst) then, for s in order,
+// dst = fma(alpha_s, src_s, dst) — a chain of the reference's add_block calls.
+struct AccJob {
+  Mat dst;
+  int src0, nsrc;
+  int zero_init;
+};
+struct AccSrc {
+  Mat src;
+  double alpha;
+};
+void launch_accum(const AccJob* jobs, const AccSrc* srcs, const int* tile_job, const int* tile_idx,
+                  int ntiles, cudaStream_t st);
+
+// Row gather/scatter of a multi-column vector block: dst(i, :) = src(idx[i], :)
+// (scatter = 0) or dst(idx[i], :) = src(i, :) (scatter = 1).
+void launch_permute_rows(Mat dst, Mat src, const int64_t* idx, int scatter, cudaStream_t st);
+
+// Direct-summation y = A x over a cloud (original order), x/y n x nrhs col-major.
+void launch_matvec(KernelParams kp, Cloud c, const double* x, double* y, int nrhs, int* singular,
+                   cudaStream_t st);
+
+// ---- Frobenius norms, sequential order (norm_frobenius, linalg.cpp:604-609)
+struct NormJob {
+  Mat a;
+  double* out;
+};
+void launch_norms(const NormJob* jobs, int njobs, cudaStream_t st);
+
+// ---- batched LU with block-local partial pivoting (k_lu.cu) ----------------
+// lu_factor (linalg.cpp:352-388) in place on A (n x n); perm[i] = forward map.
+struct LuJob {
+  Mat A;
+  int64_t* perm;
+  double tol;
+};
+void launch_lu(const LuJob* jobs, int njobs, ErrWord* err, int tag, cudaStream_t st);
+
+// LuFactors solve family (linalg.cpp:404-559), in place on X.
+enum SolveKind : int {
+  SOLVE_FULL = 0,         // X <- A^-1 X        (solve_in_place)
+  SOLVE_LOWER = 1,        // X <- L^-1 P X      (solve_lower_in_place)
+  SOLVE_UPPER = 2,        // X <- U^-1 X        (solve_upper_in_place)
+  SOLVE_TRANSPOSE = 3,    // X <- A^-T X        (solve_transpose_in_place)
+  SOLVE_RIGHT = 4,        // X <- X A^-1        (solve_right_in_place)
+  SOLVE_UPPER_RIGHT = 5,  // X <- X U^-1        (solve_upper_right_in_place)
+};
+struct SolveJob {
+  Mat lu;
+  const int64_t* perm;
+  Mat X;
+  int kind;
+};
+// Chunks: each CTA handles one (job, chunk) of RHS columns (left solves) or
+// rows (right solves); chunk width chosen on the host.
+struct SolveChunk {
+  int job, c0, nc;
+};
+void launch_solve(const SolveJob* jobs, const SolveChunk* chunks, int nchunks,
+                  size_t smem_doubles, cudaStream_t st);
+int solve_chunk_width(int m);
+
+// ---- batched column-pivoted Householder QR with member stopping (k_qr.cu)
+// run_pivoted_qr + form_q (linalg.cpp:137-185, :216-332) as used by
+// basis_from_members (compression.cpp:111-146).
+struct QrJob {
+  Mat A;               // input members concatenation, m x n (any strides)
+  int m, n;
+  const int64_t* member_off;  // nmem + 1 offsets (device)
+  int nmem;
+  double tol, member_tol;
+  int cap;             // <= 0: none
+  double* work;        // m x n row-major working copy (R)
+  int64_t ldw;
+  double* scratch;     // >= 3 n + nmem*2 doubles + m*kmax reflectors
+  double* Q;           // output m x m row-major (Q[i*m + j])
+  int* rank_out;
+};
+void launch_qr(const QrJob* jobs, int njobs, int max_m, cudaStream_t st);
+size_t qr_scratch_doubles(int m, int n, int nmem);
+
+}  // namespace h2g
