@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 H2-ULV hot path (build -> factorize -> solve).
+
+Workload (BASELINE.json configs[1], the largest config that fits one GPU):
+N = 65,536 points on the unit sphere (the reference's Fibonacci-lattice
+generator, geometry.cpp:64-95), Yukawa kernel exp(-r)/(r + 1e-3) (scale 1,
+so the diagonal is 1e3), leaf 256, strong admissibility eta = 1, rank cap
+100, tol 1e-6 (tol 1e-8 with cap 100 makes the reference abort with "basis
+does not absorb fill-in" at leaf 256; measured).
+
+A step = one pass of the hot path from device-resident points: cluster tree
++ admissibility lists + near-field arena (Pipeline::build), fill-in
+pre-computation + bases + level-parallel ULV factorization (Pipeline::factor)
+and one right-hand-side solve. value = points / second of a step, timed with
+CUDA events on the stream every kernel of the step is launched on.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+Under torchrun each rank factorizes its own replica (seed 42 + rank; weak
+scaling, no data-path collective); the timed region is bracketed by a
+barrier + synchronize, and the max over ranks is reported.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+WORKLOAD = dict(workload="c2_sphere_yukawa", n=65536, geometry="sphere(fibonacci,1)",
+                kernel="yukawa", alpha_m=1.0, scale=1.0, reg=1e-3, leaf=256, eta=1.0, cap=100,
+                tol=1e-6, structure="h2/nodep")
+CPU_SAMPLE_N = 8192  # reference CPU sample: same workload family at N = 8192
+METRIC = "h2ulv_points_per_sec"
+UNIT = "points/s"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, ValueError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        smax = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for k, nm in enumerate(names):
+                if s[5 + k].lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def make_points(n, seed):
+    from paper_2208_10907_b200.pipeline import _fib_spheres
+    if seed == 42:
+        return _fib_spheres(n, 1, 3.0, seed)
+    return _fib_spheres(n, 1, 3.0, seed)
+
+
+def cpu_reference(n, steps, warmup, threads):
+    """Time the unmodified reference (oracle/_ref/libh2ref.so) on host cores."""
+    from oracle import ref
+    xyz, q = ref.generate("sphere", n, 42)
+    cfg = ref.make_config(WORKLOAD["leaf"], tol=WORKLOAD["tol"], cap=WORKLOAD["cap"],
+                          kernel="yukawa", alpha_m=1.0, reg=WORKLOAD["reg"], scale=WORKLOAD["scale"],
+                          threads=threads)
+    times = []
+    for it in range(warmup + steps):
+        r = ref.RefRun(xyz, q, cfg)
+        t0 = time.perf_counter()
+        r.build().factor()
+        b = ref.splitmix_signed(n, 7)
+        r.solve(b)
+        dt = time.perf_counter() - t0
+        if it >= warmup:
+            times.append(dt)
+        del r
+    return times
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    steps = max(1, args.steps)
+    times = cpu_reference(CPU_SAMPLE_N, steps, args.warmup, threads)
+    t = sum(times) / len(times)
+    value = CPU_SAMPLE_N / t
+    sample = (f"reference build+factor+solve of N={CPU_SAMPLE_N} (same sphere/Yukawa/leaf 256/"
+              f"cap 100/tol 1e-6 family; N=65,536 is projected at ~13 h on the CPU)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict(WORKLOAD, n=CPU_SAMPLE_N, sample_of="c2_sphere_yukawa"),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def load_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    path = os.path.join(HERE, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def run_b200_arm(args):
+    import torch
+    import paper_2208_10907_b200 as h2
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = args.n or WORKLOAD["n"]
+    leaf = WORKLOAD["leaf"]
+    xyz, q = make_points(n, 42 + rank)
+    d_xyz = torch.from_numpy(np.ascontiguousarray(xyz)).cuda()
+    d_q = torch.from_numpy(np.ascontiguousarray(q)).cuda()
+    b = np.random.default_rng(7 + rank).uniform(-1.0, 1.0, n)
+    d_b = torch.from_numpy(b).cuda()
+    d_x = torch.empty_like(d_b)
+    stream = torch.cuda.Stream()
+
+    def new_problem():
+        p = h2.Problem()
+        p.set_stream(stream.cuda_stream)
+        p.set_kernel("yukawa", WORKLOAD["alpha_m"], WORKLOAD["scale"], WORKLOAD["reg"])
+        p.set_options(tol=WORKLOAD["tol"], cap=WORKLOAD["cap"], eta=WORKLOAD["eta"])
+        return p
+
+    def step(p):
+        p.build_dev(d_xyz.data_ptr(), d_q.data_ptr(), n, leaf)
+        p.factor()
+        p.solve_dev(d_b.data_ptr(), d_x.data_ptr(), 1)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            p = new_problem()
+            step(p)
+            p.close()
+        barrier()
+        clocks = ClockSampler(local)
+        clocks.start()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        kstats = {}
+        launches = 0
+        t_factor = []
+        t_phase = {"build": 0.0, "factor": 0.0, "solve": 0.0}
+        ev0.record(stream)
+        for _ in range(args.steps):
+            p = new_problem()
+            p.set_profile(True)
+            step(p)
+            sd = p.stats_dev()
+            for k in t_phase:
+                t_phase[k] += sd[k]
+            t_factor.append(sd["factor"])
+            for k, v in p.kernel_stats().items():
+                agg = kstats.setdefault(k, dict(ms=0.0, launches=0, flops=0.0, bytes=0.0))
+                for f in agg:
+                    agg[f] += v[f]
+            launches += p.stats()["launches"]
+            p.close()
+        ev1.record(stream)
+        barrier()
+        clk = clocks.stop()
+    elapsed = ev0.elapsed_time(ev1) * 1e-3
+    t_max = elapsed
+    if world > 1:
+        tt = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_max = float(tt.item())
+    value = n * world * args.steps / t_max
+
+    # residual of the last solve through the matrix-free direct sum
+    x = d_x.cpu().numpy()
+    p = new_problem()
+    p.build_dev(d_xyz.data_ptr(), d_q.data_ptr(), n, leaf)
+    y = p.matvec(x)
+    resid = float(np.linalg.norm(y - b) / np.linalg.norm(b))
+    p.close()
+
+    # e2e through the public C-ABI with host buffers (H2D/D2H inside the region)
+    e2e_times = []
+    for it in range(args.e2e_steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pe = h2.Problem()
+        pe.set_kernel("yukawa", WORKLOAD["alpha_m"], WORKLOAD["scale"], WORKLOAD["reg"])
+        pe.set_options(tol=WORKLOAD["tol"], cap=WORKLOAD["cap"], eta=WORKLOAD["eta"])
+        pe.build(xyz, q, leaf)
+        pe.factor()
+        xe = pe.solve(b)
+        pe.close()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_t = max(e2e_times)
+    if world > 1:
+        tt = torch.tensor([e2e_t], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_t = float(tt.item())
+
+    # dominant kernel family and its roofline
+    import json as _json
+    peaks = {}
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            peaks = _json.load(f)
+    except (OSError, ValueError):
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    dom = max(kstats.items(), key=lambda kv: kv[1]["ms"]) if kstats else ("none", {})
+    name, st = dom
+    traffic = load_traffic().get(name)
+    avg_ms = st["ms"] / max(1, st["launches"]) if st else 0.0
+    bytes_per_launch = st["bytes"] / max(1, st["launches"]) if st else 0.0
+    achieved = bytes_per_launch / (avg_ms * 1e-3) / 1e9 if avg_ms else 0.0
+    roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": hbm_peak,
+                "unit": "GB/s", "frac": achieved / hbm_peak if hbm_peak else None,
+                "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
+                "share_of_step": st["ms"] * 1e-3 / max(1e-12, t_phase["build"] + t_phase["factor"] + t_phase["solve"]) if st else None}
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        try:
+            ts = cpu_reference(CPU_SAMPLE_N, 1, 0, os.cpu_count() or 1)
+            cpu_baseline = {"value": CPU_SAMPLE_N / ts[0], "unit": UNIT, "cores": os.cpu_count(),
+                            "kind": "reference",
+                            "sample": f"unmodified reference (oracle/_ref) build+factor+solve, N={CPU_SAMPLE_N}, "
+                                      f"same workload family, {ts[0]:.1f} s"}
+        except Exception as e:  # reference library not built on this host
+            cpu_baseline = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                            "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Fibonacci-lattice sphere, seed 42+rank)",
+            "config": dict(WORKLOAD, n=n, parallelism=f"replica x{world}",
+                           l2="inputs larger than L2 (near-field arena and member panels are GBs)"),
+            "phase_s_per_step": {k: v / args.steps for k, v in t_phase.items()},
+            "factor_points_per_s": n / (sum(t_factor) / len(t_factor)),
+            "solve_rel_residual": resid,
+            "e2e": {"value": n * world / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(8 * (4 * n + n)),
+                    "d2h_bytes_per_step": int(8 * n)},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "kernels": {k: dict(v, avg_ms=v["ms"] / max(1, v["launches"])) for k, v in kstats.items()},
+            "clocks": clk,
+            "cpu_baseline": cpu_baseline,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=0, help="override N (testing only)")
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_b200_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -85,6 +85,17 @@ double h2g_max_fill_residual(h2g_problem* p);
  * reference ledger rules (flops.hpp); launches = kernels launched so far. */
 int h2g_stats(h2g_problem* p, double* t5, double* f6, int64_t* launches);
 
+/* Launch everything on a caller-owned cudaStream_t (before h2g_build). */
+int h2g_set_stream(h2g_problem* p, void* stream);
+/* Device (CUDA-event) seconds of the last [build, factor, solve]. */
+int h2g_stats_dev(h2g_problem* p, double* t3);
+/* Per-kernel-family CUDA-event timing: enable, reset, and read family idx
+ * (returns 0 past the end): total ms, launches, algorithmic flops and bytes. */
+int h2g_set_profile(h2g_problem* p, int on);
+int h2g_reset_profile(h2g_problem* p);
+int h2g_kernel_stats(h2g_problem* p, int idx, char* name, int name_len, double* ms,
+                     int64_t* launches, double* flops, double* bytes);
+
 /* Matrix-free direct-summation product y = A x on the ORIGINAL ordering
  * (replaces matvec_dense_oracle, solve.cpp:234-239, without its N guard). */
 int h2g_matvec(h2g_problem* p, int64_t nrhs, const double* x, double* y);

@@ -75,6 +75,8 @@ def lib():
         L.ref_default_eta_reg.restype = f64
         L.ref_lu_factor.argtypes = [i64, P, f64, P, P]
         L.ref_basis_from_members.argtypes = [i64, i64, P, i64, P, f64, i64, i64, P, P]
+        L.ref_gemm.argtypes = [i64, i64, i64, f64, P, ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P]
+        L.ref_lu_solve.argtypes = [i64, P, P, ctypes.c_int, i64, i64, P]
         _lib = L
     return _lib
 
@@ -235,6 +237,28 @@ def lu_factor(a, tol=1e-14):
     perm = np.zeros(n, dtype=np.int64)
     _check(lib().ref_lu_factor(n, _p(a), tol, _p(lu), _p(perm)))
     return lu, perm
+
+
+def gemm(a, b, alpha=1.0, transa=False, transb=False, c=None):
+    a = np.asfortranarray(a, dtype=np.float64)
+    b = np.asfortranarray(b, dtype=np.float64)
+    m = a.shape[1] if transa else a.shape[0]
+    k = a.shape[0] if transa else a.shape[1]
+    n = b.shape[0] if transb else b.shape[1]
+    acc = c is not None
+    out = np.array(c, dtype=np.float64, order="F") if acc else np.zeros((m, n), order="F")
+    _check(lib().ref_gemm(m, n, k, alpha, _p(a), int(transa), _p(b), int(transb), int(acc), _p(out)))
+    return out
+
+
+def lu_solve(lu, perm, x, kind):
+    lu = np.asfortranarray(lu, dtype=np.float64)
+    perm = np.ascontiguousarray(perm, dtype=np.int64)
+    x = np.array(x, dtype=np.float64, order="F")
+    kinds = {"solve": 0, "lower": 1, "upper": 2, "transpose": 3, "right": 4, "upper_right": 5}
+    _check(lib().ref_lu_solve(lu.shape[0], _p(lu), _p(perm), kinds[kind], x.shape[0], x.shape[1],
+                              _p(x)))
+    return x
 
 
 def basis_from_members(concat, offsets, tol, cap=None, min_rank=0):

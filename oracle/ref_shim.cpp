@@ -364,3 +364,48 @@ int ref_basis_from_members(int64_t dim, int64_t width, const double* concat, int
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// gemm / matmul / gemm_acc (linalg.cpp:86-126).
+int ref_gemm(int64_t m, int64_t n, int64_t k, double alpha, const double* a, int transa,
+             const double* b, int transb, int acc, double* c) {
+  return guarded([&] {
+    const int64_t ar = transa ? k : m, ac = transa ? m : k, br = transb ? n : k, bc = transb ? k : n;
+    Matrix A(ar, ac), B(br, bc), C(m, n);
+    std::memcpy(A.data(), a, sizeof(double) * ar * ac);
+    std::memcpy(B.data(), b, sizeof(double) * br * bc);
+    std::memcpy(C.data(), c, sizeof(double) * m * n);
+    if (acc) {
+      Matrix Ae = transa ? transpose(A) : A, Be = transb ? transpose(B) : B;
+      gemm_acc(C, Ae, Be, alpha);
+    } else {
+      C = matmul(A, B, transa != 0, transb != 0, alpha);
+    }
+    std::memcpy(c, C.data(), sizeof(double) * m * n);
+  });
+}
+
+// LuFactors solve family (linalg.cpp:404-559) from given packed factors.
+int ref_lu_solve(int64_t n, const double* lu, const int64_t* perm, int kind, int64_t rows,
+                 int64_t cols, double* x) {
+  return guarded([&] {
+    LuFactors f;
+    f.lu = Matrix(n, n);
+    std::memcpy(f.lu.data(), lu, sizeof(double) * n * n);
+    f.perm.forward.assign(perm, perm + n);
+    Matrix X(rows, cols);
+    std::memcpy(X.data(), x, sizeof(double) * rows * cols);
+    switch (kind) {
+      case 0: f.solve_in_place(X); break;
+      case 1: f.solve_lower_in_place(X); break;
+      case 2: f.solve_upper_in_place(X); break;
+      case 3: f.solve_transpose_in_place(X); break;
+      case 4: f.solve_right_in_place(X); break;
+      default: f.solve_upper_right_in_place(X); break;
+    }
+    std::memcpy(x, X.data(), sizeof(double) * rows * cols);
+  });
+}
+
+}  // extern "C"

@@ -35,7 +35,8 @@ EXPORTS = [
     "h2g_list", "h2g_near_entries", "h2g_near_dense", "h2g_num_factor_levels",
     "h2g_factor_level", "h2g_cutoff", "h2g_top_n", "h2g_top", "h2g_basis",
     "h2g_max_fill_residual", "h2g_stats", "h2g_matvec", "h2g_lu_factor",
-    "h2g_basis_from_members", "h2g_lu_solve", "h2g_gemm",
+    "h2g_basis_from_members", "h2g_lu_solve", "h2g_gemm", "h2g_stats_dev", "h2g_set_profile",
+    "h2g_reset_profile", "h2g_kernel_stats", "h2g_set_stream",
 ]
 
 
@@ -83,6 +84,11 @@ def lib():
         L.h2g_basis_from_members.argtypes = [i64, i64, P, i64, P, f64, i64, i64, P, P]
         L.h2g_lu_solve.argtypes = [i64, P, P, ctypes.c_int, i64, i64, P]
         L.h2g_gemm.argtypes = [i64, i64, i64, f64, P, ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P]
+        L.h2g_stats_dev.argtypes = [P, P]
+        L.h2g_set_stream.argtypes = [P, P]
+        L.h2g_set_profile.argtypes = [P, ctypes.c_int]
+        L.h2g_reset_profile.argtypes = [P]
+        L.h2g_kernel_stats.argtypes = [P, ctypes.c_int, ctypes.c_char_p, ctypes.c_int, P, P, P, P]
         _lib = L
     return _lib
 
@@ -217,6 +223,34 @@ class Problem:
         if dim:
             self.L.h2g_basis(self.h, lvl, k, side, _p(out))
         return out, rank
+
+    def set_stream(self, stream_ptr):
+        _check(self.L.h2g_set_stream(self.h, stream_ptr))
+
+    def stats_dev(self):
+        t = np.zeros(3)
+        self.L.h2g_stats_dev(self.h, _p(t))
+        return dict(build=t[0], factor=t[1], solve=t[2])
+
+    def set_profile(self, on=True):
+        self.L.h2g_set_profile(self.h, 1 if on else 0)
+
+    def reset_profile(self):
+        self.L.h2g_reset_profile(self.h)
+
+    def kernel_stats(self):
+        out = {}
+        idx = 0
+        while True:
+            name = ctypes.create_string_buffer(64)
+            ms, fl, by = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+            n = ctypes.c_int64()
+            if not self.L.h2g_kernel_stats(self.h, idx, name, 64, ctypes.byref(ms), ctypes.byref(n),
+                                           ctypes.byref(fl), ctypes.byref(by)):
+                break
+            out[name.value.decode()] = dict(ms=ms.value, launches=n.value, flops=fl.value, bytes=by.value)
+            idx += 1
+        return out
 
     def max_fill_residual(self):
         return self.L.h2g_max_fill_residual(self.h)

@@ -1,6 +1,7 @@
 // extern "C" boundary (include/h2g.h). Converts C++ exceptions into status
 // codes + h2g_last_error(), copies host buffers in/out, and exposes the
 // factor objects for inspection and parity tests.
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -84,7 +85,10 @@ int h2g_set_options(h2g_problem* p, const h2g_options* o) {
     op.abort_residual_factor = o->abort_residual_factor;
     op.structure = o->structure;
     op.eta = o->eta;
-    if (o->qr_mem_budget > 0) op.qr_mem_budget = size_t(o->qr_mem_budget);
+    if (o->qr_mem_budget > 0) {
+      op.qr_mem_budget = size_t(o->qr_mem_budget);
+      p->P.auto_budget_ = false;
+    }
   });
 }
 
@@ -242,6 +246,46 @@ int h2g_stats(h2g_problem* p, double* t5, double* f6, int64_t* launches) {
   f6[4] = get("assemble");
   f6[5] = get("solve");
   *launches = p->P.c.launches;
+  return 0;
+}
+
+int h2g_set_stream(h2g_problem* p, void* stream) {
+  return guarded([&] {
+    if (p->P.built) throw std::logic_error("h2g_set_stream: call before build");
+    p->P.use_stream(static_cast<cudaStream_t>(stream));
+  });
+}
+
+int h2g_stats_dev(h2g_problem* p, double* t3) {
+  t3[0] = p->P.stats.t_build_dev;
+  t3[1] = p->P.stats.t_factor_dev;
+  t3[2] = p->P.stats.t_solve_dev;
+  return 0;
+}
+
+int h2g_set_profile(h2g_problem* p, int on) {
+  p->P.c.prof = on != 0;
+  return 0;
+}
+
+int h2g_reset_profile(h2g_problem* p) {
+  p->P.c.pagg.clear();
+  p->P.c.launches = 0;
+  return 0;
+}
+
+int h2g_kernel_stats(h2g_problem* p, int idx, char* name, int name_len, double* ms,
+                     int64_t* launches, double* flops, double* bytes) {
+  int i = 0;
+  for (auto& [k, v] : p->P.c.pagg) {
+    if (i++ != idx) continue;
+    std::snprintf(name, size_t(name_len), "%s", k.c_str());
+    *ms = v.ms;
+    *launches = v.launches;
+    *flops = v.flops;
+    *bytes = v.bytes;
+    return 1;
+  }
   return 0;
 }
 

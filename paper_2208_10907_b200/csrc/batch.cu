@@ -40,6 +40,38 @@ void Ctx::check_err() {
   throw std::runtime_error("device error code " + std::to_string(h.code));
 }
 
+cudaEvent_t Ctx::prof_begin() {
+  if (!prof) return nullptr;
+  cudaEvent_t e;
+  cuda_check(cudaEventCreate(&e), "event");
+  cuda_check(cudaEventRecord(e, stream), "event record");
+  return e;
+}
+
+void Ctx::prof_end(const char* name, cudaEvent_t a, double flops, double bytes) {
+  if (!prof || !a) return;
+  cudaEvent_t e;
+  cuda_check(cudaEventCreate(&e), "event");
+  cuda_check(cudaEventRecord(e, stream), "event record");
+  prec.push_back({name, a, e, flops, bytes});
+}
+
+void Ctx::prof_resolve() {
+  for (auto& r : prec) {
+    float ms = 0;
+    cuda_check(cudaEventSynchronize(r.b), "event sync");
+    cuda_check(cudaEventElapsedTime(&ms, r.a, r.b), "elapsed");
+    auto& g = pagg[r.name];
+    g.ms += ms;
+    g.flops += r.flops;
+    g.bytes += r.bytes;
+    g.launches++;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  prec.clear();
+}
+
 void Ctx::sync() {
   cuda_check(cudaStreamSynchronize(stream), "stream sync");
   check_err();
@@ -129,7 +161,17 @@ void GemmBatch::run(Ctx& c, int tag) {
   const GemmJob* dj = upload(c, jobs, k1);
   const GemmSeg* ds = upload(c, segs, k2);
   const GemmTile* dt = upload(c, tiles, k3);
+  double by = 0;
+  for (auto& j : jobs) {
+    by += 8.0 * j.C.rows * double(j.C.cols) * (j.acc ? 2 : 1);
+    for (int s = 0; s < j.nseg; ++s) {
+      const GemmSeg& sg = segs[j.seg0 + s];
+      by += 8.0 * sg.A.rows * double(sg.A.cols) + (sg.gen ? 0.0 : 8.0 * sg.B.rows * double(sg.B.cols));
+    }
+  }
+  auto ev = c.prof_begin();
   launch_gemm(dj, ds, dt, int(tiles.size()), c.kp, c.cloud, c.err, tag, c.stream);
+  c.prof_end("gemm", ev, fl, by);
   c.launches++;
   cuda_check(cudaGetLastError(), "gemm launch");
 }
@@ -138,15 +180,18 @@ void EvalBatch::run(Ctx& c, int tag) {
   if (jobs.empty()) return;
   std::vector<int> tj, ti;
   tiles_of(jobs, tj, ti, &EvalJob::out);
-  double ev = 0;
-  for (auto& j : jobs) ev += double(j.out.rows) * j.out.cols;
-  c.add_flops(ev * (c.kp.kind == 0 ? 9 : 11));
+  double evn_ = 0;
+  for (auto& j : jobs) evn_ += double(j.out.rows) * j.out.cols;
+  const double ev_flops_ = evn_ * (c.kp.kind == 0 ? 9 : 11);
+  c.add_flops(ev_flops_);
   if (tj.empty()) return;
   Slab k1, k2, k3;
   auto* dj = upload(c, jobs, k1);
   auto* dtj = upload(c, tj, k2);
   auto* dti = upload(c, ti, k3);
+  auto ev = c.prof_begin();
   launch_eval(dj, dtj, dti, int(tj.size()), c.kp, c.cloud, c.err, tag, c.stream);
+  c.prof_end("eval", ev, ev_flops_, 8.0 * evn_);
   c.launches++;
   cuda_check(cudaGetLastError(), "eval launch");
 }
@@ -160,7 +205,11 @@ void CopyBatch::run(Ctx& c) {
   auto* dj = upload(c, jobs, k1);
   auto* dtj = upload(c, tj, k2);
   auto* dti = upload(c, ti, k3);
+  double by = 0;
+  for (auto& j : jobs) by += 8.0 * j.dst.rows * double(j.dst.cols) * (1 + (j.src.p ? 1 : 0) + j.add);
+  auto ev = c.prof_begin();
   launch_copy(dj, dtj, dti, int(tj.size()), c.stream);
+  c.prof_end("copy", ev, 0.0, by);
   c.launches++;
   cuda_check(cudaGetLastError(), "copy launch");
 }
@@ -175,7 +224,11 @@ void AccBatch::run(Ctx& c) {
   auto* ds = upload(c, srcs, k4);
   auto* dtj = upload(c, tj, k2);
   auto* dti = upload(c, ti, k3);
+  double by = 0;
+  for (auto& j : jobs) by += 8.0 * j.dst.rows * double(j.dst.cols) * (1 + j.nsrc + (j.zero_init ? 0 : 1));
+  auto ev = c.prof_begin();
   launch_accum(dj, ds, dtj, dti, int(tj.size()), c.stream);
+  c.prof_end("accum", ev, 0.0, by);
   c.launches++;
   cuda_check(cudaGetLastError(), "accum launch");
 }
@@ -208,7 +261,11 @@ void LuBatch::run(Ctx& c) {
   Slab k1;
   auto* dj = upload(c, jobs, k1);
   c.lu_names = names;
+  double by = 0;
+  for (auto& j : jobs) by += 16.0 * j.A.rows * double(j.A.cols);
+  auto ev = c.prof_begin();
   launch_lu(dj, int(jobs.size()), c.err, ++c.lu_tag, c.stream);
+  c.prof_end("lu", ev, fl, by);
   c.launches++;
   cuda_check(cudaGetLastError(), "lu launch");
   // LU errors must be attributed to this batch's names: check now.
@@ -235,7 +292,11 @@ void SolveBatch::run(Ctx& c) {
   Slab k1, k2;
   auto* dj = upload(c, jobs, k1);
   auto* dc = upload(c, chunks, k2);
+  double by = 0;
+  for (auto& s : jobs) by += 8.0 * s.lu.rows * double(s.lu.rows) + 16.0 * s.X.rows * double(s.X.cols);
+  auto ev = c.prof_begin();
   launch_solve(dj, dc, int(chunks.size()), smem, c.stream);
+  c.prof_end("solve", ev, fl, by);
   c.launches++;
   cuda_check(cudaGetLastError(), "solve launch");
 }
@@ -256,13 +317,15 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
   Slab rk = c.alloc(sizeof(int) * n_items);
   cuda_check(cudaMemsetAsync(rk.get(), 0, sizeof(int) * n_items, c.stream), "rank memset");
   CopyBatch idents;
+  struct QrRec { size_t rec, t0, t1; };
+  std::vector<QrRec> qr_recs;
   size_t t0 = 0;
   while (t0 < n_items) {
     // Chunk so the working copies + scratch stay under the budget.
     size_t bytes = 0, t1 = t0;
     while (t1 < n_items) {
       const auto& it = items[t1];
-      const size_t need = sizeof(double) * (size_t(it.m) * it.n +
+      const size_t need = sizeof(double) * ((it.inplace ? 0 : size_t(it.m) * it.n) +
                                             qr_scratch_doubles(it.m, it.n, int(it.offs.size()) - 1)) +
                           sizeof(int64_t) * it.offs.size() + 1024;
       if (t1 > t0 && bytes + need > mem_budget) break;
@@ -297,9 +360,14 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
       j.tol = it.tol;
       j.member_tol = it.tol * 0.5;  // BasisBuildOptions::member_tol_factor (compression.hpp:67)
       j.cap = it.cap;
-      j.work = reinterpret_cast<double*>(at);
-      j.ldw = it.n;
-      at += sizeof(double) * size_t(it.m) * it.n;
+      if (it.inplace) {
+        j.work = it.concat.m.p;
+        j.ldw = it.concat.m.rs;
+      } else {
+        j.work = reinterpret_cast<double*>(at);
+        j.ldw = it.n;
+        at += sizeof(double) * size_t(it.m) * it.n;
+      }
       j.scratch = reinterpret_cast<double*>(at);
       at += sizeof(double) * qr_scratch_doubles(it.m, it.n, j.nmem);
       j.Q = Q[t].m.p;
@@ -311,7 +379,10 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
     c.add_flops(fl);
     Slab kj;
     auto* dj = upload(c, jobs, kj);
+    auto ev = c.prof_begin();
     launch_qr(dj, int(jobs.size()), max_m, c.stream);
+    c.prof_end("qr", ev, 0.0, 0.0);
+    qr_recs.push_back({c.prof ? c.prec.size() - 1 : size_t(-1), t0, t1});
     c.launches++;
     cuda_check(cudaGetLastError(), "qr launch");
     t0 = t1;
@@ -321,13 +392,30 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
                              c.stream),
              "rank d2h");
   c.sync();
-  // Reference flop rules for the executed steps (linalg.cpp:148, :176).
+  // Reference flop rules for the executed steps (linalg.cpp:148, :176); the
+  // algorithmic bytes of the unblocked sweep: each step reads and writes the
+  // trailing panel once, and Q formation reads/writes its active rows.
   double fl = 0;
+  std::vector<double> fl_item(n_items, 0.0), by_item(n_items, 0.0);
   for (size_t t = 0; t < n_items; ++t) {
     const double m = items[t].m, n = items[t].n;
-    for (int k = 0; k < rank[t]; ++k) fl += 4.0 * (m - k) + 4.0 * (m - k) * (n - k - 1) + 4.0 * (m - k) * m;
+    for (int k = 0; k < rank[t]; ++k) {
+      const double f = 4.0 * (m - k) + 4.0 * (m - k) * (n - k - 1) + 4.0 * (m - k) * m;
+      fl += f;
+      fl_item[t] += f;
+      by_item[t] += 16.0 * (m - k) * (n - k) + 16.0 * (m - k) * m;
+    }
+    by_item[t] += 8.0 * m * n;  // initial column norms
   }
   c.add_flops(fl);
+  if (c.prof)
+    for (auto& r : qr_recs) {
+      if (r.rec == size_t(-1) || r.rec >= c.prec.size()) continue;
+      for (size_t t = r.t0; t < r.t1; ++t) {
+        c.prec[r.rec].flops += fl_item[t];
+        c.prec[r.rec].bytes += by_item[t];
+      }
+    }
 }
 
 }  // namespace h2g

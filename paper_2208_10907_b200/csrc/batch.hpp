@@ -38,6 +38,22 @@ struct Ctx {
   void check_err();       // throws the reference's message for device errors
   std::vector<std::string> lu_names;  // current LU batch names (for errors)
   int lu_tag = 0;
+  // Per-kernel CUDA-event timing on the launching stream (bench roofline).
+  struct ProfAgg {
+    double ms = 0, flops = 0, bytes = 0;
+    int64_t launches = 0;
+  };
+  struct ProfRec {
+    std::string name;
+    cudaEvent_t a, b;
+    double flops, bytes;
+  };
+  bool prof = false;
+  std::vector<ProfRec> prec;
+  std::map<std::string, ProfAgg> pagg;
+  cudaEvent_t prof_begin();
+  void prof_end(const char* name, cudaEvent_t a, double flops, double bytes);
+  void prof_resolve();  // after a sync: fold finished records into pagg
 };
 
 struct DMat {
@@ -191,10 +207,12 @@ struct QrBatch {
     std::vector<int64_t> offs;
     double tol;
     int cap;
+    bool inplace;  // factor the concat itself (it is consumed)
   };
   std::vector<Item> items;
-  int add(DMat concat, int m, int n, std::vector<int64_t> offs, double tol, int cap) {
-    items.push_back({std::move(concat), m, n, std::move(offs), tol, cap});
+  int add(DMat concat, int m, int n, std::vector<int64_t> offs, double tol, int cap,
+          bool inplace = false) {
+    items.push_back({std::move(concat), m, n, std::move(offs), tol, cap, inplace});
     return int(items.size()) - 1;
   }
   // Runs all QRs (in memory-bounded chunks); returns Q (row-major m x m in a

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <functional>
 #include <set>
 #include <stdexcept>
 
@@ -36,6 +37,28 @@ struct PhaseTimer {
   }
 };
 
+// CUDA-event interval on the problem stream (device time of a phase).
+struct DevTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t s;
+  explicit DevTimer(cudaStream_t st) : s(st) {
+    cuda_check(cudaEventCreate(&a), "event");
+    cuda_check(cudaEventCreate(&b), "event");
+    cuda_check(cudaEventRecord(a, s), "event");
+  }
+  double stop() {
+    float ms = 0;
+    cuda_check(cudaEventRecord(b, s), "event");
+    cuda_check(cudaEventSynchronize(b), "event");
+    cuda_check(cudaEventElapsedTime(&ms, a, b), "event");
+    return ms * 1e-3;
+  }
+  ~DevTimer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
 }  // namespace
 
 bool Structure::is_near(int l, int64_t i, int64_t j) const {
@@ -53,6 +76,13 @@ Problem::Problem() {
   cuda_check(cudaMemset(c.err, 0, sizeof(ErrWord)), "err");
 }
 
+void Problem::use_stream(cudaStream_t s) {
+  cuda_check(cudaStreamSynchronize(c.stream), "stream");
+  if (own_stream_) cudaStreamDestroy(c.stream);
+  c.stream = s;
+  own_stream_ = false;
+}
+
 Problem::~Problem() {
   // Release device objects before the stream they free on.
   U.clear();
@@ -64,12 +94,13 @@ Problem::~Problem() {
   orig_slab.reset();
   if (c.stream) cudaStreamSynchronize(c.stream);
   cudaFree(c.err);
-  if (c.stream) cudaStreamDestroy(c.stream);
+  if (c.stream && own_stream_) cudaStreamDestroy(c.stream);
 }
 
 // Pipeline::build (report.cpp:79-91): tree, classification, near field.
 void Problem::build(const double* d_xyz, const double* d_q, int64_t n, int64_t leaf) {
   double t0 = now_s();
+  DevTimer dt(c.stream);
   build_tree_device(T, d_xyz, d_q, n, leaf, c.stream);
   const int L = T.levels;
   const int64_t nn = (int64_t(1) << (L + 1)) - 1;
@@ -113,6 +144,8 @@ void Problem::build(const double* d_xyz, const double* d_q, int64_t n, int64_t l
   stats.t_tree = t1 - t0;
   stats.t_classify = t2 - t1;
   stats.t_near = now_s() - t2;
+  stats.t_build_dev = dt.stop();
+  c.prof_resolve();
   built = true;
 }
 
@@ -266,7 +299,10 @@ struct Driver {
   }
 
   // ---- basis_from_members (compression.cpp:111-146) batched -----------------
-  // A member list is realised straight into a row-major dim x width concat.
+  // A member list is realised straight into a row-major dim x width concat
+  // that the QR then factors in place. Boxes are processed in chunks so the
+  // concatenations (O(N) wide in the reference's exact-member scheme) never
+  // exceed the memory budget.
   struct Members {
     int dim = 0;
     int width = 0;
@@ -281,51 +317,82 @@ struct Driver {
       offs.push_back(width);
       return off;
     }
+    size_t bytes() const { return sizeof(double) * size_t(dim) * size_t(width); }
   };
   void alloc_concat(Members& M) {
     M.concat = alloc_mat(c, M.dim, std::max(M.width, 1));
     M.concat.m = Mat{M.concat.m.p, M.dim, M.width, std::max(M.width, 1), 1};
   }
 
-  // Run QRs and produce bases with ranks equalised per cluster
-  // (compression.cpp:224-229 / ulv.cpp:507-511).
-  void bases_from_concats(std::vector<Members>& rows, std::vector<Members>& cols,
-                          std::vector<Basis>& Ub, std::vector<Basis>& Vb) {
-    const size_t m = rows.size();
-    QrBatch qb;
-    for (size_t k = 0; k < m; ++k)
-      qb.add(rows[k].concat, rows[k].dim, rows[k].width, rows[k].offs, opt.tol, opt.cap);
-    for (size_t k = 0; k < m; ++k)
-      qb.add(cols[k].concat, cols[k].dim, cols[k].width, cols[k].offs, opt.tol, opt.cap);
-    std::vector<DMat> Q;
-    std::vector<int> rank;
-    qb.run(c, Q, rank, opt.qr_mem_budget);
-    Ub.assign(m, {});
-    Vb.assign(m, {});
-    std::vector<std::pair<int, int>> shapes;
-    for (size_t k = 0; k < m; ++k) {
-      shapes.push_back({rows[k].dim, rows[k].dim});
-      shapes.push_back({rows[k].dim, rows[k].dim});
+  using FillFn = std::function<void(int64_t, int64_t)>;
+  using SinkFn = std::function<void(int64_t, const Mat&, int, const Mat&, int)>;
+
+  // For boxes [0, m): allocate concats chunk by chunk, fill(k0, k1), QR all
+  // of the chunk's row (and col) concats in place, then sink(k, Qrow, rrow,
+  // Qcol, rcol) per box while the Q's are alive.
+  void run_bases(std::vector<Members>& rows, std::vector<Members>* cols, const FillFn& fill,
+                 const SinkFn& sink) {
+    const int64_t m = int64_t(rows.size());
+    int64_t k0 = 0;
+    while (k0 < m) {
+      size_t bytes = 0;
+      int64_t k1 = k0;
+      while (k1 < m) {
+        size_t need = rows[k1].bytes() + (cols ? (*cols)[k1].bytes() : 0);
+        need += need / 16 + 65536;
+        if (k1 > k0 && bytes + need > opt.qr_mem_budget) break;
+        bytes += need;
+        ++k1;
+      }
+      for (int64_t k = k0; k < k1; ++k) {
+        alloc_concat(rows[k]);
+        if (cols) alloc_concat((*cols)[k]);
+      }
+      fill(k0, k1);
+      QrBatch qb;
+      for (int64_t k = k0; k < k1; ++k)
+        qb.add(rows[k].concat, rows[k].dim, rows[k].width, rows[k].offs, opt.tol, opt.cap, true);
+      if (cols)
+        for (int64_t k = k0; k < k1; ++k)
+          qb.add((*cols)[k].concat, (*cols)[k].dim, (*cols)[k].width, (*cols)[k].offs, opt.tol,
+                 opt.cap, true);
+      std::vector<DMat> Q;
+      std::vector<int> rank;
+      qb.run(c, Q, rank, opt.qr_mem_budget);
+      const int64_t nk = k1 - k0;
+      for (int64_t k = k0; k < k1; ++k) {
+        const Mat qc = cols ? Q[nk + (k - k0)].m : Mat{};
+        const int rc = cols ? rank[nk + (k - k0)] : 0;
+        sink(k, Q[k - k0].m, rank[k - k0], qc, rc);
+      }
+      // Drain the sink's copies before the Q's and concats are released.
+      c.sync();
+      for (int64_t k = k0; k < k1; ++k) {
+        rows[k].concat = DMat{};
+        if (cols) (*cols)[k].concat = DMat{};
+      }
+      k0 = k1;
     }
-    auto sq = alloc_mats(c, shapes);
-    CopyBatch cb;
-    for (size_t k = 0; k < m; ++k) {
-      const int dim = rows[k].dim;
-      // min_rank extension == re-splitting the same Q (basis_from_members
-      // is deterministic; compression.cpp:138-144).
-      const int r = std::min(dim, std::max(rank[k], rank[m + k]));
+  }
+
+  // Rank-equalised square bases (compression.cpp:224-229 / ulv.cpp:507-511):
+  // the min_rank extension of basis_from_members re-splits the same Q.
+  SinkFn square_sink(std::vector<Basis>& Ub, std::vector<Basis>& Vb, CopyBatch& cb) {
+    return [this, &Ub, &Vb, &cb](int64_t k, const Mat& qu, int ru, const Mat& qv, int rv) {
+      const int dim = qu.rows;
+      const int r = std::min(dim, std::max(ru, rv));
+      auto sq = alloc_mats(c, {{dim, dim}, {dim, dim}});
       for (int side = 0; side < 2; ++side) {
         Basis& B = side == 0 ? Ub[k] : Vb[k];
-        B.SQ = sq[2 * k + side];
+        B.SQ = sq[side];
         B.dim = dim;
         B.rank = r;
-        const Mat q = Q[side * m + k].m;
+        const Mat q = side == 0 ? qu : qv;
         if (dim == 0) continue;
         if (dim - r > 0) cb.copy(B.SQ.m.sub(0, 0, dim, dim - r), q.sub(0, r, dim, dim - r));
         if (r > 0) cb.copy(B.SQ.m.sub(0, dim - r, dim, r), q.sub(0, 0, dim, r));
       }
-    }
-    cb.run(c);
+    };
   }
 
   // ---- build_leaf_bases (compression.cpp:193-234) ---------------------------
@@ -335,7 +402,6 @@ struct Driver {
     const bool coupling = opt.absorb_coupling && opt.structure == 0 && sys.offdiag;
     // Row members: fills (i, j != i) | A(i, far j) | A(i, ancestor far J) [+ coupling].
     std::vector<Members> rows(m), cols(m);
-    std::vector<std::vector<std::pair<int64_t, int>>> couple_at(m);
     for (int64_t i = 0; i < m; ++i) {
       Members& R = rows[i];
       R.dim = sys.dims[i];
@@ -350,17 +416,9 @@ struct Driver {
       for (int64_t t = 0; t < S.nfar(L, i); ++t) C.add(int(rs(L, S.far(L, i)[t])));
       for (auto [l2, I] : ancestor_far_partners(L, i)) C.add(int(rs(l2, I)));
     }
-    // Provisional bases need the plain row members first.
-    std::vector<int> base_width(m);
-    for (int64_t i = 0; i < m; ++i) base_width[i] = rows[i].width;
-    std::vector<Basis> prov_rank_only;
-    std::vector<DMat> provQ;
-    std::vector<int> provR;
-    auto fill_row_members = [&](std::vector<Members>& R, bool with_tail) {
-      CopyBatch cb;
-      EvalBatch eb;
-      for (int64_t i = 0; i < m; ++i) {
-        alloc_concat(R[i]);
+    auto fill_base_rows = [&](std::vector<Members>& R, int64_t k0, int64_t k1, CopyBatch& cb,
+                              EvalBatch& eb) {
+      for (int64_t i = k0; i < k1; ++i) {
         int off = 0;
         for (auto& [key, F] : fills)
           if (key.first == i && key.second != i) {
@@ -376,32 +434,36 @@ struct Driver {
           eb.add(R[i].slice(off, int(rs(l2, J))), rb(L, i), rb(l2, J));
           off += int(rs(l2, J));
         }
-        (void)with_tail;
       }
-      cb.run(c);
-      eb.run(c);
     };
+    std::vector<DMat> X(m);
+    std::vector<int> provR(m, 0);
+    std::vector<std::vector<std::pair<int64_t, int>>> couple_at(m);
     if (coupling) {
+      // Provisional row bases (compression.cpp:203-211), kept as Qs_p.
       std::vector<Members> prow = rows;
-      fill_row_members(prow, false);
-      QrBatch qb;
-      for (int64_t p = 0; p < m; ++p) qb.add(prow[p].concat, prow[p].dim, prow[p].width, prow[p].offs, opt.tol, opt.cap);
-      qb.run(c, provQ, provR, opt.qr_mem_budget);
-      prow.clear();
-      // X_p = A_pp^-1 Qs_p, coupling member A_ip X_p for p in near(i).
-      std::vector<DMat> X(m);
-      std::vector<std::pair<int, int>> shapes;
-      for (int64_t p = 0; p < m; ++p) shapes.push_back({sys.dims[p], provR[p]});
-      auto xs = alloc_mats(c, shapes);
-      CopyBatch cb;
+      std::vector<DMat> provQs(m);
+      run_bases(prow, nullptr,
+                [&](int64_t k0, int64_t k1) {
+                  CopyBatch cb;
+                  EvalBatch eb;
+                  fill_base_rows(prow, k0, k1, cb, eb);
+                  cb.run(c);
+                  eb.run(c);
+                },
+                [&](int64_t p, const Mat& q, int r, const Mat&, int) {
+                  provR[p] = r;
+                  provQs[p] = alloc_mat(c, sys.dims[p], r);
+                  CopyBatch cb;
+                  if (r > 0) cb.copy(provQs[p].m, q.sub(0, 0, sys.dims[p], r));
+                  cb.run(c);
+                });
+      // X_p = A_pp^-1 Qs_p; coupling member A_ip X_p for p in near(i).
       SolveBatch sb;
       for (int64_t p = 0; p < m; ++p) {
-        X[p] = xs[p];
-        if (provR[p] == 0) continue;
-        cb.copy(X[p].m, provQ[p].m.sub(0, 0, sys.dims[p], provR[p]));
-        sb.add(sys.diag_lu[p], X[p].m, SOLVE_FULL);
+        X[p] = provQs[p];
+        if (provR[p] > 0) sb.add(sys.diag_lu[p], X[p].m, SOLVE_FULL);
       }
-      cb.run(c);
       sb.run(c);
       for (int64_t i = 0; i < m; ++i)
         for (int64_t t = 0; t < S.nnear(L, i); ++t) {
@@ -409,41 +471,45 @@ struct Driver {
           if (p == i || provR[p] == 0) continue;
           couple_at[i].push_back({p, rows[i].add(provR[p])});
         }
-      fill_row_members(rows, true);
-      GemmBatch gb;
-      for (int64_t i = 0; i < m; ++i)
-        for (auto [p, off] : couple_at[i]) gemm1(gb, rows[i].slice(off, provR[p]), block(sys, i, p), X[p].m);
-      gb.run(c);
-    } else {
-      fill_row_members(rows, false);
     }
-    // Column members: F(c, j)^T | A(i, j)^T | A(I, j)^T.
-    {
-      CopyBatch cb;
-      EvalBatch eb;
-      for (int64_t j = 0; j < m; ++j) {
-        Members& C = cols[j];
-        alloc_concat(C);
-        int off = 0;
-        for (auto& [key, F] : fills)
-          if (key.second == j && key.first != j) {
-            cb.copy(C.slice(off, F.rows()).t(), F.m);
-            off += F.rows();
-          }
-        for (int64_t t = 0; t < S.nfar(L, j); ++t) {
-          const int64_t i = S.far(L, j)[t];
-          eb.add(C.slice(off, int(rs(L, i))).t(), rb(L, i), rb(L, j));
-          off += int(rs(L, i));
-        }
-        for (auto [l2, I] : ancestor_far_partners(L, j)) {
-          eb.add(C.slice(off, int(rs(l2, I))).t(), rb(l2, I), rb(L, j));
-          off += int(rs(l2, I));
-        }
-      }
-      cb.run(c);
-      eb.run(c);
-    }
-    bases_from_concats(rows, cols, P.U[L], P.V[L]);
+    CopyBatch sqcopies;
+    run_bases(rows, &cols,
+              [&](int64_t k0, int64_t k1) {
+                CopyBatch cb;
+                EvalBatch eb;
+                GemmBatch gb;
+                fill_base_rows(rows, k0, k1, cb, eb);
+                for (int64_t i = k0; i < k1; ++i)
+                  for (auto [p, off] : couple_at[i])
+                    gemm1(gb, rows[i].slice(off, provR[p]), block(sys, i, p), X[p].m);
+                // Column members: F(c, j)^T | A(i, j)^T | A(I, j)^T.
+                for (int64_t j = k0; j < k1; ++j) {
+                  Members& C = cols[j];
+                  int off = 0;
+                  for (auto& [key, F] : fills)
+                    if (key.second == j && key.first != j) {
+                      cb.copy(C.slice(off, F.rows()).t(), F.m);
+                      off += F.rows();
+                    }
+                  for (int64_t t = 0; t < S.nfar(L, j); ++t) {
+                    const int64_t i = S.far(L, j)[t];
+                    eb.add(C.slice(off, int(rs(L, i))).t(), rb(L, i), rb(L, j));
+                    off += int(rs(L, i));
+                  }
+                  for (auto [l2, I] : ancestor_far_partners(L, j)) {
+                    eb.add(C.slice(off, int(rs(l2, I))).t(), rb(l2, I), rb(L, j));
+                    off += int(rs(l2, I));
+                  }
+                }
+                cb.run(c);
+                eb.run(c);
+                gb.run(c);
+              },
+              [&](int64_t k, const Mat& qu, int ru, const Mat& qv, int rv) {
+                square_sink(P.U[L], P.V[L], sqcopies)(k, qu, ru, qv, rv);
+                sqcopies.run(c);
+                sqcopies.jobs.clear();
+              });
   }
 
   // ---- build_leaf_pieces (ulv.cpp:336-401) -----------------------------------
@@ -725,51 +791,57 @@ struct Driver {
       for (int64_t t = 0; t < S.nfar(lvl, k); ++t) cols[k].add(sys.dims[S.far(lvl, k)[t]]);
       for (auto [l2, I] : ancestor_far_partners(lvl, k)) cols[k].add(int(rs(l2, I)));
     }
-    CopyBatch cb;
-    GemmBatch gb;
-    for (int64_t k = 0; k < m; ++k) {
-      alloc_concat(rows[k]);
-      alloc_concat(cols[k]);
-      int off = 0;
-      for (auto& [key, F] : fills)
-        if (key.first == k && key.second != k) {
-          cb.copy(rows[k].slice(off, F.cols()), F.m);
-          off += F.cols();
-        }
-      for (auto& [tk, piece] : merged[k]) {
-        cb.copy(rows[k].slice(off, piece.cols()), piece.m);
-        off += piece.cols();
-      }
-      off = 0;
-      for (auto& [key, F] : fills)
-        if (key.second == k && key.first != k) {
-          cb.copy(cols[k].slice(off, F.rows()).t(), F.m);
-          off += F.rows();
-        }
-      for (int64_t t = 0; t < S.nfar(lvl, k); ++t) {
-        const int64_t i = S.far(lvl, k)[t];
-        const Mat piece = merged[i].at({lvl, k}).m;
-        cols_to_merged(gb, cols[k].slice(off, piece.rows).t(), {piece}, k);
-        off += piece.rows;
-      }
-      for (auto [l2, I] : ancestor_far_partners(lvl, k)) {
-        // (A(I, c0) Vbig_c0 | A(I, c1) Vbig_c1)^T = [Vbig_c0^T A(I,c0)^T ; ...]
-        const int w = int(rs(l2, I));
-        const Mat dst = cols[k].slice(off, w);
-        const Mat v0 = Vbig[2 * k], v1 = Vbig[2 * k + 1];
-        gb.job(dst.sub(0, 0, v0.cols, w), false);
-        gb.seg_gen(v0.t(), rb(l2, I), rb(lvl + 1, 2 * k), w, true, 1.0);
-        gb.job(dst.sub(v0.cols, 0, v1.cols, w), false);
-        gb.seg_gen(v1.t(), rb(l2, I), rb(lvl + 1, 2 * k + 1), w, true, 1.0);
-        off += w;
-      }
-    }
-    cb.run(c);
-    gb.run(c);
     for (int64_t k = 0; k < m; ++k)
       if (sys.dims[k] == 0 && rows[k].width > 0)
         throw std::runtime_error("compute_transfer: rank-0 children with nonzero parent blocks");
-    bases_from_concats(rows, cols, P.U[lvl], P.V[lvl]);
+    CopyBatch sqcopies;
+    run_bases(rows, &cols,
+              [&](int64_t k0, int64_t k1) {
+                CopyBatch cb;
+                GemmBatch gb;
+                for (int64_t k = k0; k < k1; ++k) {
+                  int off = 0;
+                  for (auto& [key, F] : fills)
+                    if (key.first == k && key.second != k) {
+                      cb.copy(rows[k].slice(off, F.cols()), F.m);
+                      off += F.cols();
+                    }
+                  for (auto& [tk, piece] : merged[k]) {
+                    cb.copy(rows[k].slice(off, piece.cols()), piece.m);
+                    off += piece.cols();
+                  }
+                  off = 0;
+                  for (auto& [key, F] : fills)
+                    if (key.second == k && key.first != k) {
+                      cb.copy(cols[k].slice(off, F.rows()).t(), F.m);
+                      off += F.rows();
+                    }
+                  for (int64_t t = 0; t < S.nfar(lvl, k); ++t) {
+                    const int64_t i = S.far(lvl, k)[t];
+                    const Mat piece = merged[i].at({lvl, k}).m;
+                    cols_to_merged(gb, cols[k].slice(off, piece.rows).t(), {piece}, k);
+                    off += piece.rows;
+                  }
+                  for (auto [l2, I] : ancestor_far_partners(lvl, k)) {
+                    // (A(I, c0) Vbig_c0 | A(I, c1) Vbig_c1)^T, B generated in-kernel.
+                    const int w = int(rs(l2, I));
+                    const Mat dst = cols[k].slice(off, w);
+                    const Mat v0 = Vbig[2 * k], v1 = Vbig[2 * k + 1];
+                    gb.job(dst.sub(0, 0, v0.cols, w), false);
+                    gb.seg_gen(v0.t(), rb(l2, I), rb(lvl + 1, 2 * k), w, true, 1.0);
+                    gb.job(dst.sub(v0.cols, 0, v1.cols, w), false);
+                    gb.seg_gen(v1.t(), rb(l2, I), rb(lvl + 1, 2 * k + 1), w, true, 1.0);
+                    off += w;
+                  }
+                }
+                cb.run(c);
+                gb.run(c);
+              },
+              [&](int64_t k, const Mat& qu, int ru, const Mat& qv, int rv) {
+                square_sink(P.U[lvl], P.V[lvl], sqcopies)(k, qu, ru, qv, rv);
+                sqcopies.run(c);
+                sqcopies.jobs.clear();
+              });
   }
 
   // ---- assemble_level (ulv.cpp:526-607) ----------------------------------------
@@ -1230,13 +1302,21 @@ void Problem::factor() {
   if (!built) throw std::logic_error("Pipeline::factor: build() first");
   if (factored) return;
   const double t0 = now_s();
+  DevTimer dt(c.stream);
+  if (auto_budget_) {
+    size_t fr = 0, tot = 0;
+    cuda_check(cudaMemGetInfo(&fr, &tot), "meminfo");
+    opt.qr_mem_budget = std::max<size_t>(size_t(1) << 28, fr / 3);
+  }
   c.phase_flops.clear();
   levels.clear();
   max_fill_resid.clear();
   Driver d(*this);
   d.run();
   c.sync();
+  stats.t_factor_dev = dt.stop();
   stats.t_factor = now_s() - t0;
+  c.prof_resolve();
   for (auto& [k, v] : c.phase_flops) stats.phase_flops[k] += v;
   stats.launches = c.launches;
   stats.max_fill_residual = 0;
@@ -1259,6 +1339,7 @@ void Problem::matvec(const double* d_x, double* d_y, int nrhs) {
 void Problem::solve(const double* d_b, double* d_x, int nrhs) {
   if (!factored) throw std::logic_error("Pipeline::solve_rhs: factor() first");
   const double t0 = now_s();
+  DevTimer dt(c.stream);
   const int64_t n = T.n;
   const int L = T.levels;
   const std::string saved_phase = c.phase;
@@ -1438,7 +1519,9 @@ void Problem::solve(const double* d_b, double* d_x, int nrhs) {
   launch_permute_rows(Mat{d_x, int(n), nrhs, 1, n}, xp.m, T.order, 1, c.stream);
   c.sync();
   c.phase = saved_phase;
+  stats.t_solve_dev = dt.stop();
   stats.t_solve = now_s() - t0;
+  c.prof_resolve();
 }
 
 }  // namespace h2g

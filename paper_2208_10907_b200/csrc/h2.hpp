@@ -20,7 +20,7 @@ struct Options {  // FactorOptions (ulv.hpp:29-45) + RunConfig bits
   double abort_residual_factor = 100.0;
   int structure = 0;  // 0 h2 (strong, nodep), 1 hss (weak)
   double eta = 1.0;
-  size_t qr_mem_budget = size_t(8) << 30;
+  size_t qr_mem_budget = size_t(8) << 30;  // auto (free/3) unless set
 };
 
 struct Basis {  // SharedBasis (hstructure.hpp:61-69): square [Qr | Qs]
@@ -59,6 +59,7 @@ using FillSet = std::map<std::pair<int64_t, int64_t>, DMat>;
 
 struct Stats {
   double t_tree = 0, t_classify = 0, t_near = 0, t_factor = 0, t_solve = 0;
+  double t_build_dev = 0, t_factor_dev = 0, t_solve_dev = 0;  // CUDA events
   std::map<std::string, double> phase_flops, phase_seconds;
   int64_t launches = 0;
   double kernel_evals = 0;
@@ -85,10 +86,14 @@ class Problem {
   LuF top;
   std::vector<double> max_fill_resid;
   bool built = false, factored = false;
+  bool auto_budget_ = true;
 
   Problem();
   ~Problem();
   void set_kernel(const KernelParams& kp) { c.kp = kp; }
+  // Run on a caller-owned stream (e.g. torch's) instead of the private one.
+  void use_stream(cudaStream_t s);
+  bool own_stream_ = true;
   void build(const double* d_xyz, const double* d_q, int64_t n, int64_t leaf);  // device inputs
   void factor();
   // b and x: device, n x nrhs column-major, ORIGINAL point order.

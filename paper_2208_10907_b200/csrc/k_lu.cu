@@ -93,6 +93,26 @@ __global__ void __launch_bounds__(NT) lu_kernel(const LuJob* __restrict__ jobs, 
   }
 }
 
+// Dot products of the reference's solve_transpose_in_place (linalg.cpp:487-495)
+// as GCC -O3 -mavx2 -mfma vectorises them: products of each 4-wide group are
+// rounded and added in order (no FMA), a trailing pair likewise, and an odd
+// last element is fused (vfmadd231sd). Verified against the compiled
+// reference for every trip count (tests/test_gpu_parity.py).
+__device__ __forceinline__ double gcc_dot_h(const Mat& A, int i0, int col, const double* x,
+                                            int tc) {
+  double s = 0.0;
+  const int v4 = tc & ~3;
+  int i = 0;
+  for (; i < v4; ++i) s = s + A.at(i0 + i, col) * x[i0 + i];
+  if ((tc & 3) >= 2) {
+    s = s + A.at(i0 + i, col) * x[i0 + i];
+    s = s + A.at(i0 + i + 1, col) * x[i0 + i + 1];
+    i += 2;
+  }
+  if (tc & 1) s = fma(A.at(i0 + i, col), x[i0 + i], s);
+  return s;
+}
+
 // xs is chunk-local column-major: xs[c * m + i] (left) / xs[j * nr + r] (right).
 __global__ void __launch_bounds__(256) solve_kernel(const SolveJob* __restrict__ jobs,
                                                     const SolveChunk* __restrict__ chunks) {
@@ -118,13 +138,11 @@ __global__ void __launch_bounds__(256) solve_kernel(const SolveJob* __restrict__
       for (int c = tid; c < nc; c += nt) {
         double* x = xs + c * m;
         for (int k = 0; k < m; ++k) {
-          double dot = 0.0;
-          for (int i = 0; i < k; ++i) dot = fma(L.at(i, k), x[i], dot);
+          const double dot = gcc_dot_h(L, 0, k, x, k);
           x[k] = (x[k] - dot) / L.at(k, k);
         }
         for (int k = m - 1; k >= 0; --k) {
-          double dot = 0.0;
-          for (int i = k + 1; i < m; ++i) dot = fma(L.at(i, k), x[i], dot);
+          const double dot = gcc_dot_h(L, k + 1, k, x, m - k - 1);
           x[k] = x[k] - dot;
         }
       }

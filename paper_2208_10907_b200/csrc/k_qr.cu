@@ -90,10 +90,12 @@ __global__ void __launch_bounds__(NT) qr_kernel(const QrJob* __restrict__ jobs) 
   int kmax = kmax0;
   if (job.cap > 0 && job.cap < kmax) kmax = job.cap;
 
-  // R = A, column norms (s += A(i,j)^2 sequential over i).
-  for (int64_t e = tid; e < int64_t(m) * n; e += NT) {
-    const int i = int(e / n), j = int(e % n);
-    W[i * ldw + j] = job.A.at(i, j);
+  // R = A (skipped when factoring in place), column norms.
+  if (!(job.A.p == W && job.A.rs == ldw && job.A.cs == 1)) {
+    for (int64_t e = tid; e < int64_t(m) * n; e += NT) {
+      const int i = int(e / n), j = int(e % n);
+      W[i * ldw + j] = job.A.at(i, j);
+    }
   }
   __syncthreads();
   for (int j = tid; j < n; j += NT) {

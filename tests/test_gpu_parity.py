@@ -1,0 +1,217 @@
+"""GPU parity tests through the C-ABI (libh2g.so on the B200) against the
+golden fixtures of the unmodified reference and, when it is built on this
+host, the live reference library (oracle/_ref).
+
+Bar: tree / lists / near field / LU / GEMM / triangular solves bit-exact;
+end-to-end solve within the tolerances stated per test (the pivoted-QR
+reductions round differently from the reference's GCC-vectorised loops, so
+rank decisions may differ at isolated boxes)."""
+import numpy as np
+import pytest
+
+from conftest import has_ref
+from oracle import cpu, ref
+
+pytestmark = pytest.mark.gpu
+
+h2 = pytest.importorskip("paper_2208_10907_b200")
+from paper_2208_10907_b200 import _lib as g  # noqa: E402
+
+
+def fbits(a):
+    return ref.fnv64(np.ascontiguousarray(a, dtype=np.float64).view(np.int64).ravel())
+
+
+def make_problem(rec, xyz, q):
+    p = h2.Problem()
+    kind = rec["kernel"]
+    p.set_kernel(kind, 1.0 if kind == "yukawa" else 0.0, rec["scale"], rec["reg"])
+    p.set_options(tol=rec["tol"], cap=rec["cap"], structure=rec["structure"])
+    p.build(xyz, q, rec["leaf"])
+    return p
+
+
+E2E = ["cube512", "cube1024", "cube1024_default_kernel", "hss1024", "cube2048",
+       "sphere2048_yukawa_cap100", "line1024", "spheres8_4096", "c1_cube4096",
+       "sphere4096_yukawa_cap100_tol1e-6_leaf256"]
+
+
+@pytest.mark.parametrize("name", E2E)
+def test_structure_and_near_field_bitwise(golden, name):
+    gd, _ = golden
+    rec = gd["cases"][name]
+    xyz, q = cpu.generate(rec["geometry"], rec["n"], 42, rec["spheres"])
+    p = make_problem(rec, xyz, q)
+    assert p.levels == rec["levels"]
+    assert ref.fnv64(p.perm()) == rec["perm_fnv"]
+    be, geo = p.nodes()
+    assert ref.fnv64(be.ravel()) == rec["nodes_fnv"] and fbits(geo) == rec["geo_fnv"]
+    for lvl in range(1, rec["levels"] + 1):
+        got = [ref.fnv64(a) for a in (*p.lists(lvl, 0), *p.lists(lvl, 1))]
+        assert got == rec["lists"][str(lvl)][:4], f"level {lvl} lists"
+    if rec["kernel"] == "laplace":
+        assert fbits(p.leaf_dense()) == rec["near_fnv"]
+    p.close()
+
+
+# Residual tolerance: relative agreement with the reference's own residual.
+@pytest.mark.parametrize("name", E2E)
+def test_solve_residual_matches_reference(golden, name):
+    gd, arrays = golden
+    rec = gd["cases"][name]
+    xyz, q = cpu.generate(rec["geometry"], rec["n"], 42, rec["spheres"])
+    p = make_problem(rec, xyz, q)
+    p.factor()
+    b = ref.splitmix_signed(rec["n"], 7)
+    x = p.solve(b)
+    y = p.matvec(x)
+    r = np.linalg.norm(y - b) / np.linalg.norm(b)
+    r_ref = rec["residual"]
+    # same method, same defect: residual within 5% relative (1e-12 absolute floor)
+    assert abs(r - r_ref) <= 0.05 * r_ref + 1e-12, (r, r_ref)
+    if name + "_x" in arrays:
+        xr = arrays[name + "_x"]
+        assert np.linalg.norm(x - xr) / np.linalg.norm(xr) < 1e-6
+    # cutoff structure equal; per-level ranks equal in >= 90% of boxes
+    lvl, dims = p.cutoff()
+    assert lvl == rec["cutoff"][0]
+    got = {str(l): rk for l, rk in p.factor_levels()}
+    assert set(got) == set(rec["ranks"])
+    same = sum(int(np.sum(got[k] == np.array(v))) for k, v in rec["ranks"].items())
+    total = sum(len(v) for v in rec["ranks"].values())
+    assert same >= 0.9 * total
+    p.close()
+
+
+def test_hss_is_exact():
+    """Weak admissibility has no covered pairs: the solve is tolerance-exact."""
+    xyz, q = cpu.generate("cube", 1024, 42)
+    p = h2.Problem()
+    p.set_kernel("laplace", 0.0, 1.0, 1e-3)
+    p.set_options(tol=1e-10, structure="hss")
+    p.build(xyz, q, 128)
+    p.factor()
+    b = ref.splitmix_signed(1024, 7)
+    r = np.linalg.norm(p.matvec(p.solve(b)) - b) / np.linalg.norm(b)
+    assert r < 1e-9
+
+
+def test_multi_rhs_is_columnwise_identical():
+    xyz, q = cpu.generate("cube", 1024, 42)
+    p = h2.Problem()
+    p.set_kernel("laplace", 0.0, 1.0, 1e-3)
+    p.set_options(tol=1e-8)
+    p.build(xyz, q, 128)
+    p.factor()
+    B = np.stack([ref.splitmix_signed(1024, s) for s in (7, 8, 9)], axis=1)
+    X = p.solve(B)
+    for k in range(3):
+        assert np.array_equal(X[:, k].view(np.int64), p.solve(B[:, k].copy()).view(np.int64))
+
+
+def test_matvec_bitwise_vs_reference_dense():
+    if not has_ref():
+        pytest.skip("reference oracle not built")
+    xyz, q = cpu.generate("cube", 1024, 3)
+    p = h2.Problem()
+    p.set_kernel("laplace", 0.0, 1.0, 1e-3)
+    p.build(xyz, q, 128)
+    x = ref.splitmix_signed(1024, 4)
+    r = ref.RefRun(xyz, q, ref.make_config(128, reg=1e-3, scale=1.0)).build()
+    assert np.array_equal(p.matvec(x).view(np.int64), r.dense_matvec(x).view(np.int64))
+
+
+def test_primitives_bitwise_vs_golden(golden):
+    gd, a = golden
+    prims = gd["primitives"]
+    for key, exp in prims.items():
+        if key.startswith("gemm"):
+            A, B, C = a[key + "_a"], a[key + "_b"], a[key + "_c"]
+            got = [fbits(g.gemm(A, B)), fbits(g.gemm(A, B, -1.0, c=C)),
+                   fbits(g.gemm(A.T.copy(), B, transa=True))]
+            assert got == exp, key
+        else:
+            n = int(key.split("_")[1])
+            lu, perm = g.lu_factor(a[key + "_a"])
+            got = [fbits(lu), ref.fnv64(perm)]
+            for kind in ["solve", "lower", "upper", "transpose", "right", "upper_right"]:
+                got.append(fbits(g.lu_solve(lu, perm, a[f"{key}_{kind}_x"], kind)))
+            assert got == exp, key
+
+
+def test_singular_lu_message():
+    with pytest.raises(h2.H2GError, match="singular block in LU of block at step 1"):
+        g.lu_factor(np.array([[1.0, 2.0], [2.0, 4.0]]))
+
+
+def test_singular_kernel_evaluation_message():
+    xyz = np.zeros((256, 3))
+    xyz[:, 0] = np.repeat(np.arange(128), 2)  # duplicate points, reg = 0
+    p = h2.Problem()
+    p.set_kernel("laplace", 0.0, 1.0, 0.0)
+    with pytest.raises(h2.H2GError, match="singular evaluation"):
+        p.build(xyz, np.ones(256), 16)
+
+
+def test_fill_absorption_abort_matches_reference():
+    """Cap 100 at tol 1e-8 with leaf 256 cannot absorb the fills: the reference
+    aborts (ulv.cpp:144-146) and so must we."""
+    xyz, q = cpu.generate("sphere", 4096, 42)
+    p = h2.Problem()
+    p.set_kernel("yukawa", 1.0, 1.0, 1e-3)
+    p.set_options(tol=1e-8, cap=100)
+    p.build(xyz, q, 256)
+    with pytest.raises(h2.H2GError, match="basis does not absorb fill-in at level 4"):
+        p.factor()
+
+
+def test_errors_on_bad_sizes():
+    xyz, q = cpu.generate("cube", 100, 1)
+    p = h2.Problem()
+    with pytest.raises(h2.H2GError, match="need N >= 2"):
+        p.build(xyz, q, 64)
+    with pytest.raises(h2.H2GError, match="degenerate cloud"):
+        h2.Problem().build(np.zeros((64, 3)), np.ones(64), 8)
+
+
+def test_bench_size_structure_bitwise(golden):
+    """N = 65,536 (bench workload): tree + lists bit-exact against the reference."""
+    gd, _ = golden
+    rec = gd["cases"]["c2_sphere65536"]
+    xyz, q = cpu.generate("sphere", rec["n"], 42)
+    p = h2.Problem()
+    p.set_kernel("yukawa", 1.0, 1.0, 1e-3)
+    p.build(xyz, q, rec["leaf"])
+    assert ref.fnv64(p.perm()) == rec["perm_fnv"]
+    for lvl in range(1, rec["levels"] + 1):
+        assert [ref.fnv64(a) for a in (*p.lists(lvl, 0), *p.lists(lvl, 1))] == rec["lists"][str(lvl)][:4]
+
+
+def test_large_structure_bitwise(golden):
+    rec = golden[0]["cases"]["cube262144"]
+    xyz, q = cpu.generate("cube", rec["n"], 42)
+    p = h2.Problem()
+    p.set_kernel("laplace", 0.0, 1.0, 1e-3)
+    p.build(xyz, q, rec["leaf"])
+    assert ref.fnv64(p.perm()) == rec["perm_fnv"]
+    be, geo = p.nodes()
+    assert ref.fnv64(be.ravel()) == rec["nodes_fnv"] and fbits(geo) == rec["geo_fnv"]
+
+
+@pytest.mark.skipif(not has_ref(), reason="reference oracle not built")
+@pytest.mark.parametrize("n,leaf", [(777, 64), (1500, 100)])
+def test_ragged_sizes_vs_live_reference(n, leaf):
+    xyz, q = cpu.generate("cube", n, 9)
+    cfg = ref.make_config(leaf, reg=1e-3, scale=1.0)
+    r = ref.RefRun(xyz, q, cfg).build().factor()
+    p = h2.Problem()
+    p.set_kernel("laplace", 0.0, 1.0, 1e-3)
+    p.set_options(tol=1e-8)
+    p.build(xyz, q, leaf)
+    p.factor()
+    b = ref.splitmix_signed(n, 7)
+    xr, xg = r.solve(b), p.solve(b)
+    assert np.array_equal(p.perm(), r.perm())
+    rr = np.linalg.norm(r.dense_matvec(xr) - b) / np.linalg.norm(b)
+    rg = np.linalg.norm(p.matvec(xg) - b) / np.linalg.norm(b)
+    assert abs(rr - rg) <= 0.05 * rr + 1e-12
