@@ -90,12 +90,19 @@ __global__ void norms_kernel(const NormJob* __restrict__ jobs, int njobs) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= njobs) return;
   const NormJob job = jobs[t];
+  // GCC's vectorised reduction (see k_qr.cu, pattern P2): 4-wide groups of
+  // rounded squares added in order; tails (and sizes <= 3) fused.
+  const int64_t rows = job.a.rows, tc = rows * job.a.cols;
+  auto get = [&](int64_t e) { const double d = job.a.at(e % rows, e / rows); return d; };
   double s = 0.0;
-  for (int j = 0; j < job.a.cols; ++j)
-    for (int i = 0; i < job.a.rows; ++i) {
-      const double d = job.a.at(i, j);
-      s = fma(d, d, s);
-    }
+  if (tc <= 3) {
+    for (int64_t e = 0; e < tc; ++e) { const double d = get(e); s = fma(d, d, s); }
+  } else {
+    const int64_t v4 = tc & ~int64_t(3);
+    int64_t e = 0;
+    for (; e < v4; ++e) { const double d = get(e); s = s + d * d; }
+    for (; e < tc; ++e) { const double d = get(e); s = fma(d, d, s); }
+  }
   *job.out = sqrt(s);
 }
 

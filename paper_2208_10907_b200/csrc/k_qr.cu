@@ -16,6 +16,65 @@ namespace {
 
 constexpr int NT = 512;
 
+// The reference's reductions as GCC -O3 -mavx2 -mfma compiles them
+// (linalg.cpp; disassembly of oracle/_ref, verified bit-exact on random
+// members in tests). In every vectorised loop the 4-wide groups round each
+// product and add in order; the loops differ only in their tails:
+//   H : trailing pair rounded-and-added, odd last element fused
+//       (apply_reflector dot, vnormsq for tc >= 2, solve_transpose);
+//   P2: tc <= 3 all fused; otherwise each remainder element fused
+//       (column norms, make_reflector normsq, downdate recompute).
+template <class G>
+__device__ __forceinline__ double red_h(G get, int i0, int tc, double s) {
+  const int v4 = tc & ~3;
+  int i = 0;
+  for (; i < v4; ++i) {
+    double a, b;
+    get(i0 + i, a, b);
+    s = s + a * b;
+  }
+  if ((tc & 3) >= 2) {
+    double a, b;
+    get(i0 + i, a, b);
+    s = s + a * b;
+    get(i0 + i + 1, a, b);
+    s = s + a * b;
+    i += 2;
+  }
+  if (tc & 1) {
+    double a, b;
+    get(i0 + i, a, b);
+    s = fma(a, b, s);
+  }
+  return s;
+}
+
+template <class G>
+__device__ __forceinline__ double red_p2(G get, int i0, int tc) {
+  double s = 0.0;
+  if (tc <= 3) {
+    for (int i = 0; i < tc; ++i) {
+      double a, b;
+      get(i0 + i, a, b);
+      s = fma(a, b, s);
+    }
+    return s;
+  }
+  const int v4 = tc & ~3;
+  int i = 0;
+  for (; i < v4; ++i) {
+    double a, b;
+    get(i0 + i, a, b);
+    s = s + a * b;
+  }
+  for (; i < tc; ++i) {
+    double a, b;
+    get(i0 + i, a, b);
+    s = fma(a, b, s);
+  }
+  return s;
+}
+
 struct Scratch {
   double* cn2;
   double* cn2o;
@@ -99,11 +158,7 @@ __global__ void __launch_bounds__(NT) qr_kernel(const QrJob* __restrict__ jobs) 
   }
   __syncthreads();
   for (int j = tid; j < n; j += NT) {
-    double s = 0.0;
-    for (int i = 0; i < m; ++i) {
-      const double a = W[i * ldw + j];
-      s = fma(a, a, s);
-    }
+    const double s = red_p2([&](int i, double& a, double& b) { a = b = W[i * ldw + j]; }, 0, m);
     S.cn2[j] = s;
     S.cn2o[j] = s;
     S.piv[j] = j;
@@ -167,11 +222,8 @@ __global__ void __launch_bounds__(NT) qr_kernel(const QrJob* __restrict__ jobs) 
     // make_reflector (linalg.cpp:152-178), sequential on one thread.
     double* vk = S.V + int64_t(k) * m;
     if (tid == 0) {
-      double normsq = 0.0;
-      for (int i = k; i < m; ++i) {
-        const double a = W[i * ldw + k];
-        normsq = fma(a, a, normsq);
-      }
+      const double normsq =
+          red_p2([&](int i, double& a, double& b) { a = b = W[i * ldw + k]; }, k, m - k);
       const double norm = sqrt(normsq);
       for (int i = 0; i < k; ++i) vk[i] = 0.0;
       double tau = 0.0;
@@ -182,9 +234,12 @@ __global__ void __launch_bounds__(NT) qr_kernel(const QrJob* __restrict__ jobs) 
         const double alpha = (a0 >= 0.0) ? -norm : norm;
         vk[k] = a0 - alpha;
         double vn = vk[k] * vk[k];
-        for (int i = k + 1; i < m; ++i) {
-          vk[i] = W[i * ldw + k];
-          vn = fma(vk[i], vk[i], vn);
+        for (int i = k + 1; i < m; ++i) vk[i] = W[i * ldw + k];
+        const int tcv = m - k - 1;
+        if (tcv == 1) {
+          vn = vn + vk[k + 1] * vk[k + 1];
+        } else if (tcv > 1) {
+          vn = red_h([&](int i, double& a, double& b) { a = b = vk[i]; }, k + 1, tcv, vn);
         }
         tau = (vn == 0.0) ? 0.0 : 2.0 / vn;
         W[k * ldw + k] = alpha;
@@ -200,20 +255,17 @@ __global__ void __launch_bounds__(NT) qr_kernel(const QrJob* __restrict__ jobs) 
     // apply_reflector to columns k+1.. (linalg.cpp:137-149) + norm downdate.
     for (int j = k + 1 + tid; j < n; j += NT) {
       if (tau != 0.0) {
-        double dot = 0.0;
-        for (int i = k; i < m; ++i) dot = fma(vsh[i], W[i * ldw + j], dot);
+        const double dot =
+            red_h([&](int i, double& a, double& b) { a = vsh[i]; b = W[i * ldw + j]; }, k, m - k, 0.0);
         const double s = tau * dot;
         for (int i = k; i < m; ++i) W[i * ldw + j] = fma(-s, vsh[i], W[i * ldw + j]);
       }
+      // GCC computes rkj*rkj once (rounded) for the norm and member downdates.
       const double rkj = W[k * ldw + j];
-      double upd = fma(-rkj, rkj, S.cn2[j]);
-      if (upd < 1e-8 * S.cn2o[j]) {
-        upd = 0.0;
-        for (int i = k + 1; i < m; ++i) {
-          const double a = W[i * ldw + j];
-          upd = fma(a, a, upd);
-        }
-      }
+      const double sq = rkj * rkj;
+      double upd = S.cn2[j] - sq;
+      if (upd < 1e-8 * S.cn2o[j])
+        upd = red_p2([&](int i, double& a, double& b) { a = b = W[i * ldw + j]; }, k + 1, m - k - 1);
       S.cn2[j] = fmax(0.0, upd);
     }
     __syncthreads();
@@ -224,7 +276,7 @@ __global__ void __launch_bounds__(NT) qr_kernel(const QrJob* __restrict__ jobs) 
       for (int j = k + 1; j < n; ++j) {
         const double rkj = rowk[j];
         const int g = S.mof[j];
-        double v = fma(-rkj, rkj, S.mm[g]);
+        const double v = S.mm[g] - rkj * rkj;
         S.mm[g] = v < 0.0 ? 0.0 : v;
       }
       const int gk = S.mof[k];
@@ -246,8 +298,8 @@ __global__ void __launch_bounds__(NT) qr_kernel(const QrJob* __restrict__ jobs) 
     for (int i = tid; i < m; i += NT) vsh[i] = vk[i];
     __syncthreads();
     for (int j = tid; j < m; j += NT) {
-      double dot = 0.0;
-      for (int i = k; i < m; ++i) dot = fma(vsh[i], Q[int64_t(i) * m + j], dot);
+      const double dot = red_h(
+          [&](int i, double& a, double& b) { a = vsh[i]; b = Q[int64_t(i) * m + j]; }, k, m - k, 0.0);
       const double s = tau * dot;
       for (int i = k; i < m; ++i) Q[int64_t(i) * m + j] = fma(-s, vsh[i], Q[int64_t(i) * m + j]);
     }
