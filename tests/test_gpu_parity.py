@@ -2,10 +2,11 @@
 golden fixtures of the unmodified reference and, when it is built on this
 host, the live reference library (oracle/_ref).
 
-Bar: tree / lists / near field / LU / GEMM / triangular solves bit-exact;
-end-to-end solve within the tolerances stated per test (the pivoted-QR
-reductions round differently from the reference's GCC-vectorised loops, so
-rank decisions may differ at isolated boxes)."""
+Bar: for the Laplace kernel every stage is bit-exact — tree, lists, near
+field, fills, pivoted-QR bases (ranks and Q), elimination factors, the top LU
+and the solution x (FNV of the bits equals the reference's). For Yukawa the
+kernel entries use CUDA exp (<= 1 ulp from glibc), so x is compared with a
+relative tolerance of 1e-10 and the residual to 1e-6 relative."""
 import numpy as np
 import pytest
 
@@ -67,19 +68,18 @@ def test_solve_residual_matches_reference(golden, name):
     y = p.matvec(x)
     r = np.linalg.norm(y - b) / np.linalg.norm(b)
     r_ref = rec["residual"]
-    # same method, same defect: residual within 5% relative (1e-12 absolute floor)
-    assert abs(r - r_ref) <= 0.05 * r_ref + 1e-12, (r, r_ref)
-    if name + "_x" in arrays:
-        xr = arrays[name + "_x"]
-        assert np.linalg.norm(x - xr) / np.linalg.norm(xr) < 1e-6
-    # cutoff structure equal; per-level ranks equal in >= 90% of boxes
     lvl, dims = p.cutoff()
-    assert lvl == rec["cutoff"][0]
-    got = {str(l): rk for l, rk in p.factor_levels()}
-    assert set(got) == set(rec["ranks"])
-    same = sum(int(np.sum(got[k] == np.array(v))) for k, v in rec["ranks"].items())
-    total = sum(len(v) for v in rec["ranks"].values())
-    assert same >= 0.9 * total
+    assert lvl == rec["cutoff"][0] and dims.tolist() == rec["cutoff"][1]
+    got = {str(l): rk.tolist() for l, rk in p.factor_levels()}
+    assert got == rec["ranks"]  # every discrete rank decision identical
+    if rec["kernel"] == "laplace":
+        assert fbits(x) == rec["x_fnv"], "solution differs from the reference bit pattern"
+        assert fbits(np.array([r])) == fbits(np.array([r_ref])) or abs(r - r_ref) <= 1e-15 * r_ref
+    else:
+        assert abs(r - r_ref) <= 1e-6 * r_ref + 1e-14, (r, r_ref)
+        if name + "_x" in arrays:
+            xr = arrays[name + "_x"]
+            assert np.linalg.norm(x - xr) / np.linalg.norm(xr) < 1e-10
     p.close()
 
 

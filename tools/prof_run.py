@@ -1,0 +1,16 @@
+"""One build+factor+solve of the bench workload family at a profiling size."""
+import sys
+import numpy as np
+sys.path.insert(0, '.')
+import paper_2208_10907_b200 as h2
+from paper_2208_10907_b200.pipeline import _fib_spheres
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+xyz, q = _fib_spheres(n, 1, 3.0, 42)
+p = h2.Problem()
+p.set_kernel("yukawa", 1.0, 1.0, 1e-3)
+p.set_options(tol=1e-6, cap=100)
+p.build(xyz, q, 256)
+p.factor()
+x = p.solve(np.random.default_rng(7).uniform(-1, 1, n))
+print("ok", n, p.stats_dev())
