@@ -92,6 +92,9 @@ int h2g_stats_dev(h2g_problem* p, double* t3);
 /* Per-kernel-family CUDA-event timing: enable, reset, and read family idx
  * (returns 0 past the end): total ms, launches, algorithmic flops and bytes. */
 int h2g_set_profile(h2g_problem* p, int on);
+/* Host wall seconds per reference phase (fill_precompute, basis, skeleton,
+ * factorize, assemble); returns 0 past the end. */
+int h2g_phase_seconds(h2g_problem* p, int idx, char* name, int name_len, double* sec);
 int h2g_reset_profile(h2g_problem* p);
 int h2g_kernel_stats(h2g_problem* p, int idx, char* name, int name_len, double* ms,
                      int64_t* launches, double* flops, double* bytes);

@@ -36,7 +36,7 @@ EXPORTS = [
     "h2g_factor_level", "h2g_cutoff", "h2g_top_n", "h2g_top", "h2g_basis",
     "h2g_max_fill_residual", "h2g_stats", "h2g_matvec", "h2g_lu_factor",
     "h2g_basis_from_members", "h2g_lu_solve", "h2g_gemm", "h2g_stats_dev", "h2g_set_profile",
-    "h2g_reset_profile", "h2g_kernel_stats", "h2g_set_stream",
+    "h2g_reset_profile", "h2g_kernel_stats", "h2g_set_stream", "h2g_phase_seconds",
 ]
 
 
@@ -86,6 +86,7 @@ def lib():
         L.h2g_gemm.argtypes = [i64, i64, i64, f64, P, ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P]
         L.h2g_stats_dev.argtypes = [P, P]
         L.h2g_set_stream.argtypes = [P, P]
+        L.h2g_phase_seconds.argtypes = [P, ctypes.c_int, ctypes.c_char_p, ctypes.c_int, P]
         L.h2g_set_profile.argtypes = [P, ctypes.c_int]
         L.h2g_reset_profile.argtypes = [P]
         L.h2g_kernel_stats.argtypes = [P, ctypes.c_int, ctypes.c_char_p, ctypes.c_int, P, P, P, P]
@@ -249,6 +250,18 @@ class Problem:
                                            ctypes.byref(fl), ctypes.byref(by)):
                 break
             out[name.value.decode()] = dict(ms=ms.value, launches=n.value, flops=fl.value, bytes=by.value)
+            idx += 1
+        return out
+
+    def phase_seconds(self):
+        out = {}
+        idx = 0
+        while True:
+            name = ctypes.create_string_buffer(64)
+            sec = ctypes.c_double()
+            if not self.L.h2g_phase_seconds(self.h, idx, name, 64, ctypes.byref(sec)):
+                break
+            out[name.value.decode()] = sec.value
             idx += 1
         return out
 

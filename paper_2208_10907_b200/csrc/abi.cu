@@ -263,6 +263,17 @@ int h2g_stats_dev(h2g_problem* p, double* t3) {
   return 0;
 }
 
+int h2g_phase_seconds(h2g_problem* p, int idx, char* name, int name_len, double* sec) {
+  int i = 0;
+  for (auto& [k, v] : p->P.stats.phase_seconds) {
+    if (i++ != idx) continue;
+    std::snprintf(name, size_t(name_len), "%s", k.c_str());
+    *sec = v;
+    return 1;
+  }
+  return 0;
+}
+
 int h2g_set_profile(h2g_problem* p, int on) {
   p->P.c.prof = on != 0;
   return 0;

@@ -343,7 +343,7 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
     Slab ko;
     int64_t* doffs = upload(c, offs_all, ko);
     char* at = static_cast<char*>(work.get());
-    int max_m = 1;
+    int max_m = 1, max_nmem = 1;
     double fl = 0;
     for (size_t t = t0; t < t1; ++t) {
       const auto& it = items[t];
@@ -360,12 +360,12 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
       j.tol = it.tol;
       j.member_tol = it.tol * 0.5;  // BasisBuildOptions::member_tol_factor (compression.hpp:67)
       j.cap = it.cap;
-      if (it.inplace) {
+      if (it.inplace) {  // column-major concat factored in place
         j.work = it.concat.m.p;
-        j.ldw = it.concat.m.rs;
+        j.ldw = it.concat.m.cs;
       } else {
         j.work = reinterpret_cast<double*>(at);
-        j.ldw = it.n;
+        j.ldw = it.m;
         at += sizeof(double) * size_t(it.m) * it.n;
       }
       j.scratch = reinterpret_cast<double*>(at);
@@ -374,13 +374,14 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
       j.rank_out = static_cast<int*>(rk.get()) + t;
       jobs.push_back(j);
       max_m = std::max(max_m, it.m);
+      max_nmem = std::max(max_nmem, j.nmem);
       fl += 2.0 * it.m * double(it.n);  // column norms
     }
     c.add_flops(fl);
     Slab kj;
     auto* dj = upload(c, jobs, kj);
     auto ev = c.prof_begin();
-    launch_qr(dj, int(jobs.size()), max_m, c.stream);
+    launch_qr(dj, int(jobs.size()), max_m, max_nmem, c.stream);
     c.prof_end("qr", ev, 0.0, 0.0);
     qr_recs.push_back({c.prof ? c.prec.size() - 1 : size_t(-1), t0, t1});
     c.launches++;

@@ -72,6 +72,15 @@ bool Structure::is_far(int l, int64_t i, int64_t j) const {
 
 Problem::Problem() {
   cuda_check(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking), "stream");
+  // Keep freed stream-ordered memory in the pool: the factorization reuses
+  // tens of GB of panel memory level after level, and re-mapping it from
+  // the driver at every synchronisation costs seconds.
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "device");
+  cudaMemPool_t pool;
+  cuda_check(cudaDeviceGetDefaultMemPool(&pool, dev), "mempool");
+  uint64_t keep = ~uint64_t(0);
+  cuda_check(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep), "mempool attr");
   cuda_check(cudaMalloc(&c.err, sizeof(ErrWord)), "err");
   cuda_check(cudaMemset(c.err, 0, sizeof(ErrWord)), "err");
 }
@@ -299,8 +308,8 @@ struct Driver {
   }
 
   // ---- basis_from_members (compression.cpp:111-146) batched -----------------
-  // A member list is realised straight into a row-major dim x width concat
-  // that the QR then factors in place. Boxes are processed in chunks so the
+  // A member list is realised straight into a column-major dim x width
+  // concat that the QR then factors in place. Boxes are processed in chunks so the
   // concatenations (O(N) wide in the reference's exact-member scheme) never
   // exceed the memory budget.
   struct Members {
@@ -309,7 +318,7 @@ struct Driver {
     std::vector<int64_t> offs{0};
     DMat concat;
     Mat slice(int off, int w) const {
-      return Mat{concat.m.p + off, dim, w, width > 0 ? width : 1, 1};
+      return Mat{concat.m.p + int64_t(off) * std::max(dim, 1), dim, w, 1, std::max(dim, 1)};
     }
     int add(int w) {
       const int off = width;
@@ -317,11 +326,13 @@ struct Driver {
       offs.push_back(width);
       return off;
     }
-    size_t bytes() const { return sizeof(double) * size_t(dim) * size_t(width); }
+    // Column-major (ld = dim): each member column is contiguous, so the QR's
+    // column tiles are contiguous HBM ranges.
+    size_t bytes() const { return sizeof(double) * size_t(dim) * size_t(std::max(width, 1)); }
   };
   void alloc_concat(Members& M) {
-    M.concat = alloc_mat(c, M.dim, std::max(M.width, 1));
-    M.concat.m = Mat{M.concat.m.p, M.dim, M.width, std::max(M.width, 1), 1};
+    M.concat = alloc_mat(c, std::max(M.dim, 1), std::max(M.width, 1));
+    M.concat.m = Mat{M.concat.m.p, M.dim, M.width, 1, std::max(M.dim, 1)};
   }
 
   using FillFn = std::function<void(int64_t, int64_t)>;

@@ -14,7 +14,7 @@ namespace h2g {
 
 namespace {
 
-constexpr int NT = 512;
+constexpr int NT = 256;
 
 // The reference's reductions as GCC -O3 -mavx2 -mfma compiles them
 // (linalg.cpp; disassembly of oracle/_ref, verified bit-exact on random
@@ -78,6 +78,7 @@ __device__ __forceinline__ double red_p2(G get, int i0, int tc) {
 struct Scratch {
   double* cn2;
   double* cn2o;
+  double* sq;
   int* piv;
   int* mof;
   double* mm;
@@ -93,7 +94,8 @@ __host__ __device__ inline Scratch carve(double* s, int m, int n, int nmem) {
   c.cn2o = s + n;
   c.piv = reinterpret_cast<int*>(s + 2 * int64_t(n));
   c.mof = c.piv + n;
-  c.mm = s + 3 * int64_t(n);
+  c.sq = s + 3 * int64_t(n);
+  c.mm = s + 4 * int64_t(n);
   c.mt = c.mm + nmem;
   c.tau = c.mt + nmem;
   c.V = c.tau + kmax0;
@@ -134,8 +136,75 @@ __device__ int block_min_int(int v, int* red) {
   return r;
 }
 
-__global__ void __launch_bounds__(NT) qr_kernel(const QrJob* __restrict__ jobs) {
-  extern __shared__ double vsh[];  // reflector, m doubles
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+
+// red_h over a shared-memory column (stride ld) with 8-deep load prefetch:
+// the dependent add chain then runs at FP64 latency, not LDS latency.
+__device__ __forceinline__ double red_h_smem(const double* __restrict__ v,
+                                             const double* __restrict__ col, int ld, int tc) {
+  double s = 0.0;
+  const int v4 = tc & ~3;
+  int i = 0;
+  for (; i + 8 <= v4; i += 8) {
+    double p[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) p[u] = v[i + u] * col[(i + u) * ld];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = s + p[u];
+  }
+  for (; i < v4; ++i) s = s + v[i] * col[i * ld];
+  if ((tc & 3) >= 2) {
+    s = s + v[i] * col[i * ld];
+    s = s + v[i + 1] * col[(i + 1) * ld];
+    i += 2;
+  }
+  if (tc & 1) s = fma(v[i], col[i * ld], s);
+  return s;
+}
+
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+}
+
+// Column-major panel W (element (i, j) at W[j * ldw + i]): a tile of
+// whole column segments [k, m) is one contiguous HBM range, loaded with
+// cp.async into shared memory at an odd pitch (conflict-free per-thread
+// column walks), updated there, and written back: one read + one write of
+// the trailing panel per Householder step.
+// Warp w copies columns w, w + NT/32, ...; lanes walk the contiguous
+// segment (no per-element index division).
+__device__ __forceinline__ void load_tile(double* T, int pitch, const double* W, int64_t ldw,
+                                          int k, int rows, int jt, int tw) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = warp; c < tw; c += NT / 32) {
+    const double* src = W + int64_t(jt + c) * ldw + k;
+    double* dst = T + c * pitch;
+    for (int r = lane; r < rows; r += 32) cp_async8(dst + r, src + r);
+  }
+  cp_async_wait_all();
+}
+
+__device__ __forceinline__ void store_tile(const double* T, int pitch, double* W, int64_t ldw,
+                                           int k, int rows, int jt, int tw) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = warp; c < tw; c += NT / 32) {
+    double* dst = W + int64_t(jt + c) * ldw + k;
+    const double* src = T + c * pitch;
+    for (int r = lane; r < rows; r += 32) dst[r] = src[r];
+  }
+}
+
+// Dynamic shared memory: [ v (m) | member masses (nmem) | column tile ].
+__global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ jobs, int tile_doubles,
+                                                   int nmem_cap) {
+  extern __shared__ double dsm[];
   __shared__ double redd[32];
   __shared__ int redi[32];
   __shared__ double sh_tau;
@@ -144,26 +213,40 @@ __global__ void __launch_bounds__(NT) qr_kernel(const QrJob* __restrict__ jobs) 
   double* W = job.work;
   const int64_t ldw = job.ldw;
   const int tid = threadIdx.x;
+  double* vsh = dsm;
+  double* mmsh = dsm + m;
+  double* T = dsm + m + nmem_cap;
   Scratch S = carve(job.scratch, m, n, nmem);
   const int kmax0 = m < n ? m : n;
   int kmax = kmax0;
   if (job.cap > 0 && job.cap < kmax) kmax = job.cap;
 
-  // R = A (skipped when factoring in place), column norms.
-  if (!(job.A.p == W && job.A.rs == ldw && job.A.cs == 1)) {
+  // R = A (skipped when factoring in place).
+  if (!(job.A.p == W && job.A.rs == 1 && job.A.cs == ldw)) {
     for (int64_t e = tid; e < int64_t(m) * n; e += NT) {
-      const int i = int(e / n), j = int(e % n);
-      W[i * ldw + j] = job.A.at(i, j);
+      const int j = int(e / m), i = int(e % m);
+      W[j * ldw + i] = job.A.at(i, j);
+    }
+    __syncthreads();
+  }
+  // Column norms (pattern P2 over all rows), tile by tile.
+  {
+    const int pitch = m | 1;
+    const int twmax = max(1, min(NT, tile_doubles / pitch));
+    for (int jt = 0; jt < n; jt += twmax) {
+      const int tw = min(twmax, n - jt);
+      load_tile(T, pitch, W, ldw, 0, m, jt, tw);
+      __syncthreads();
+      if (tid < tw) {
+        const double* col = T + tid * pitch;
+        const double s = red_p2([&](int i, double& a, double& b) { a = b = col[i]; }, 0, m);
+        S.cn2[jt + tid] = s;
+        S.cn2o[jt + tid] = s;
+        S.piv[jt + tid] = jt + tid;
+      }
+      __syncthreads();
     }
   }
-  __syncthreads();
-  for (int j = tid; j < n; j += NT) {
-    const double s = red_p2([&](int i, double& a, double& b) { a = b = W[i * ldw + j]; }, 0, m);
-    S.cn2[j] = s;
-    S.cn2o[j] = s;
-    S.piv[j] = j;
-  }
-  __syncthreads();
   const bool members = nmem >= 1;
   if (members) {
     for (int g = tid; g < nmem; g += NT) {
@@ -172,7 +255,7 @@ __global__ void __launch_bounds__(NT) qr_kernel(const QrJob* __restrict__ jobs) 
         S.mof[j] = g;
         mass += S.cn2[j];
       }
-      S.mm[g] = mass;
+      mmsh[g] = mass;
       S.mt[g] = job.member_tol * job.member_tol * mass;
     }
   }
@@ -190,16 +273,15 @@ __global__ void __launch_bounds__(NT) qr_kernel(const QrJob* __restrict__ jobs) 
     for (int j = k + tid; j < n; j += NT)
       if (S.cn2[j] >= tie) cand = min(cand, S.piv[j]);
     const int sel_orig = block_min_int(cand, redi);
-    // Locate the position holding original column sel_orig (unique).
     int selpos = 0x7fffffff;
     for (int j = k + tid; j < n; j += NT)
       if (S.piv[j] == sel_orig && S.cn2[j] >= tie) selpos = j;
     const int sel = block_min_int(selpos, redi);
     if (sel != k) {
       for (int i = tid; i < m; i += NT) {
-        const double t = W[i * ldw + k];
-        W[i * ldw + k] = W[i * ldw + sel];
-        W[i * ldw + sel] = t;
+        const double t = W[int64_t(k) * ldw + i];
+        W[int64_t(k) * ldw + i] = W[int64_t(sel) * ldw + i];
+        W[int64_t(sel) * ldw + i] = t;
       }
       if (tid == 0) {
         double t = S.cn2[k]; S.cn2[k] = S.cn2[sel]; S.cn2[sel] = t;
@@ -214,27 +296,27 @@ __global__ void __launch_bounds__(NT) qr_kernel(const QrJob* __restrict__ jobs) 
     const bool diag_done = pivot_norm <= job.tol * r11;
     int not_done = 0;
     if (members)
-      for (int g = tid; g < nmem; g += NT) not_done |= (S.mm[g] > S.mt[g]);
+      for (int g = tid; g < nmem; g += NT) not_done |= (mmsh[g] > S.mt[g]);
     const bool members_done = !__syncthreads_or(not_done);
     const bool floor_hit = pivot_norm <= 1e-15 * r11;
     if ((diag_done && members_done) || floor_hit) break;
 
     // make_reflector (linalg.cpp:152-178), sequential on one thread.
     double* vk = S.V + int64_t(k) * m;
+    double* wk = W + int64_t(k) * ldw;
     if (tid == 0) {
-      const double normsq =
-          red_p2([&](int i, double& a, double& b) { a = b = W[i * ldw + k]; }, k, m - k);
+      const double normsq = red_p2([&](int i, double& a, double& b) { a = b = wk[i]; }, k, m - k);
       const double norm = sqrt(normsq);
       for (int i = 0; i < k; ++i) vk[i] = 0.0;
       double tau = 0.0;
       if (norm == 0.0) {
         for (int i = k; i < m; ++i) vk[i] = 0.0;
       } else {
-        const double a0 = W[k * ldw + k];
+        const double a0 = wk[k];
         const double alpha = (a0 >= 0.0) ? -norm : norm;
         vk[k] = a0 - alpha;
         double vn = vk[k] * vk[k];
-        for (int i = k + 1; i < m; ++i) vk[i] = W[i * ldw + k];
+        for (int i = k + 1; i < m; ++i) vk[i] = wk[i];
         const int tcv = m - k - 1;
         if (tcv == 1) {
           vn = vn + vk[k + 1] * vk[k + 1];
@@ -242,8 +324,8 @@ __global__ void __launch_bounds__(NT) qr_kernel(const QrJob* __restrict__ jobs) 
           vn = red_h([&](int i, double& a, double& b) { a = b = vk[i]; }, k + 1, tcv, vn);
         }
         tau = (vn == 0.0) ? 0.0 : 2.0 / vn;
-        W[k * ldw + k] = alpha;
-        for (int i = k + 1; i < m; ++i) W[i * ldw + k] = 0.0;
+        wk[k] = alpha;
+        for (int i = k + 1; i < m; ++i) wk[i] = 0.0;
       }
       S.tau[k] = tau;
       sh_tau = tau;
@@ -253,36 +335,72 @@ __global__ void __launch_bounds__(NT) qr_kernel(const QrJob* __restrict__ jobs) 
     __syncthreads();
     const double tau = sh_tau;
     // apply_reflector to columns k+1.. (linalg.cpp:137-149) + norm downdate.
-    for (int j = k + 1 + tid; j < n; j += NT) {
-      if (tau != 0.0) {
-        const double dot =
-            red_h([&](int i, double& a, double& b) { a = vsh[i]; b = W[i * ldw + j]; }, k, m - k, 0.0);
-        const double s = tau * dot;
-        for (int i = k; i < m; ++i) W[i * ldw + j] = fma(-s, vsh[i], W[i * ldw + j]);
+    const int rows = m - k;
+    const int pitch = rows | 1;
+    const int twmax = max(1, min(NT, tile_doubles / pitch));
+    for (int jt = k + 1; jt < n; jt += twmax) {
+      const int tw = min(twmax, n - jt);
+      load_tile(T, pitch, W, ldw, k, rows, jt, tw);
+      __syncthreads();
+      if (tid < tw) {
+        double* col = T + tid * pitch;
+        if (tau != 0.0) {
+          const double dot = red_h_smem(vsh + k, col, 1, rows);
+          const double sc = -(tau * dot);
+#pragma unroll 8
+          for (int r = 0; r < rows; ++r) col[r] = fma(sc, vsh[k + r], col[r]);
+        }
+        // GCC computes rkj*rkj once (rounded) for the norm and member downdates.
+        const int j = jt + tid;
+        const double rkj = col[0];
+        const double sq = rkj * rkj;
+        double upd = S.cn2[j] - sq;
+        if (upd < 1e-8 * S.cn2o[j])
+          upd = red_p2([&](int r, double& a, double& b) { a = b = col[r]; }, 1, rows - 1);
+        S.cn2[j] = fmax(0.0, upd);
+        S.sq[j] = sq;
       }
-      // GCC computes rkj*rkj once (rounded) for the norm and member downdates.
-      const double rkj = W[k * ldw + j];
-      const double sq = rkj * rkj;
-      double upd = S.cn2[j] - sq;
-      if (upd < 1e-8 * S.cn2o[j])
-        upd = red_p2([&](int i, double& a, double& b) { a = b = W[i * ldw + j]; }, k + 1, m - k - 1);
-      S.cn2[j] = fmax(0.0, upd);
+      __syncthreads();
+      store_tile(T, pitch, W, ldw, k, rows, jt, tw);
+      __syncthreads();
     }
-    __syncthreads();
     ++rank;
-    if (members && tid == 0) {
-      // member_mass[g] -= rkj^2 in column order (linalg.cpp:312-315).
-      const double* rowk = W + k * ldw;
-      for (int j = k + 1; j < n; ++j) {
-        const double rkj = rowk[j];
-        const int g = S.mof[j];
-        const double v = S.mm[g] - rkj * rkj;
-        S.mm[g] = v < 0.0 ? 0.0 : v;
+    if (members && tid < 32) {
+      // member_mass[g] -= rkj^2 in column order (linalg.cpp:312-315). Warp 0
+      // stages 256 (rkj^2, group) pairs at a time in shared memory; lane 0
+      // runs the ordered chain with the running group value in a register.
+      double* st_r = T;
+      int* st_g = reinterpret_cast<int*>(T + 256);
+      int cur = -1;
+      double val = 0.0;
+      for (int j0 = k + 1; j0 < n; j0 += 256) {
+        const int cnt = min(256, n - j0);
+        for (int u = tid; u < cnt; u += 32) {
+          st_r[u] = S.sq[j0 + u];
+          st_g[u] = S.mof[j0 + u];
+        }
+        __syncwarp();
+        if (tid == 0) {
+          for (int u = 0; u < cnt; ++u) {
+            const int g = st_g[u];
+            if (g != cur) {
+              if (cur >= 0) mmsh[cur] = val;
+              cur = g;
+              val = mmsh[g];
+            }
+            const double v = val - st_r[u];
+            val = v < 0.0 ? 0.0 : v;
+          }
+        }
+        __syncwarp();
       }
-      const int gk = S.mof[k];
-      double v = S.mm[gk] - S.cn2[k];
-      S.mm[gk] = v < 0.0 ? 0.0 : v;
-      S.cn2[k] = 0.0;
+      if (tid == 0) {
+        if (cur >= 0) mmsh[cur] = val;
+        const int gk = S.mof[k];
+        const double v = mmsh[gk] - S.cn2[k];
+        mmsh[gk] = v < 0.0 ? 0.0 : v;
+        S.cn2[k] = 0.0;
+      }
     }
     __syncthreads();
   }
@@ -312,17 +430,25 @@ __global__ void __launch_bounds__(NT) qr_kernel(const QrJob* __restrict__ jobs) 
 
 size_t qr_scratch_doubles(int m, int n, int nmem) {
   const size_t kmax0 = size_t(m < n ? m : n);
-  return 3 * size_t(n) + 2 * size_t(nmem) + kmax0 + size_t(m) * kmax0 + 8;
+  return 4 * size_t(n) + 2 * size_t(nmem) + kmax0 + size_t(m) * kmax0 + 8;
 }
 
-void launch_qr(const QrJob* jobs, int njobs, int max_m, cudaStream_t st) {
+void launch_qr(const QrJob* jobs, int njobs, int max_m, int max_nmem, cudaStream_t st) {
   if (njobs <= 0) return;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  qr_kernel<<<njobs, NT, sizeof(double) * size_t(max_m > 0 ? max_m : 1), st>>>(jobs);
+  // Two CTAs per SM (~100 KB of shared memory each, most of it the tile) so
+  // one CTA's load/compute/store phases overlap the other's.
+  const size_t budget = 100 * 1024;
+  const size_t fixed = sizeof(double) * size_t(max_m + max_nmem);
+  size_t tile = budget > fixed + 8192 ? (budget - fixed) / sizeof(double) : 1024;
+  if (tile < size_t(max_m | 1)) tile = size_t(max_m | 1);  // at least one column
+  if (tile < 384) tile = 384;                               // member staging
+  const size_t smem = fixed + tile * sizeof(double);
+  qr_kernel<<<njobs, NT, smem, st>>>(jobs, int(tile), max_nmem);
 }
 
 }  // namespace h2g

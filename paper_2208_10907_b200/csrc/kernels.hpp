@@ -128,18 +128,18 @@ int solve_chunk_width(int m);
 // basis_from_members (compression.cpp:111-146).
 struct QrJob {
   Mat A;               // input members concatenation, m x n (any strides)
-  int m, n;
+  int m, n;            // work: column-major m x n, element (i, j) at work[j * ldw + i]
   const int64_t* member_off;  // nmem + 1 offsets (device)
   int nmem;
   double tol, member_tol;
   int cap;             // <= 0: none
-  double* work;        // m x n row-major working copy (R)
+  double* work;        // m x n column-major working copy (R), may alias A
   int64_t ldw;
   double* scratch;     // >= 3 n + nmem*2 doubles + m*kmax reflectors
   double* Q;           // output m x m row-major (Q[i*m + j])
   int* rank_out;
 };
-void launch_qr(const QrJob* jobs, int njobs, int max_m, cudaStream_t st);
+void launch_qr(const QrJob* jobs, int njobs, int max_m, int max_nmem, cudaStream_t st);
 size_t qr_scratch_doubles(int m, int n, int nmem);
 
 }  // namespace h2g

@@ -31,4 +31,5 @@ for n, leaf, geom in [(int(a), int(b), c) for a, b, c in (x.split(':') for x in 
             k, v['ms'], v['launches'], v['flops'], v['bytes'], v['bytes'] / v['ms'] / 1e6 if v['ms'] else 0,
             v['flops'] / v['ms'] / 1e9 if v['ms'] else 0))
     print('   stats', p.stats(), flush=True)
+    print('   phases', p.phase_seconds(), flush=True)
     p.close()
