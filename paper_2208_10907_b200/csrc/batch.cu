@@ -1,6 +1,8 @@
 // Host-side batch launchers (see batch.hpp).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "batch.hpp"
 
@@ -378,10 +380,29 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
       fl += 2.0 * it.m * double(it.n);  // column norms
     }
     c.add_flops(fl);
+    Slab kdbg;
+    double* ddbg = nullptr;
+    if (getenv("H2G_QR_DEBUG")) {
+      kdbg = c.alloc(sizeof(double) * 8 * jobs.size());
+      ddbg = static_cast<double*>(kdbg.get());
+      cudaMemsetAsync(ddbg, 0, sizeof(double) * 8 * jobs.size(), c.stream);
+      for (size_t q = 0; q < jobs.size(); ++q) jobs[q].dbg = ddbg + 8 * q;
+    }
     Slab kj;
     auto* dj = upload(c, jobs, kj);
     auto ev = c.prof_begin();
     launch_qr(dj, int(jobs.size()), max_m, max_nmem, c.stream);
+    if (ddbg) {
+      std::vector<double> h(8 * jobs.size());
+      cudaMemcpyAsync(h.data(), ddbg, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c.stream);
+      cudaStreamSynchronize(c.stream);
+      double a[7] = {0};
+      for (size_t q = 0; q < jobs.size(); ++q)
+        for (int u = 0; u < 7; ++u) a[u] += h[8 * q + u];
+      fprintf(stderr, "QRDBG jobs=%zu avg: piv %.3g refl %.3g tile %.3g mem %.3g rank %.1f n %.0f formq %.3g (cycles)\n",
+              jobs.size(), a[0] / jobs.size(), a[1] / jobs.size(), a[2] / jobs.size(), a[3] / jobs.size(),
+              a[4] / jobs.size(), a[5] / jobs.size(), a[6] / jobs.size());
+    }
     c.prof_end("qr", ev, 0.0, 0.0);
     qr_recs.push_back({c.prof ? c.prec.size() - 1 : size_t(-1), t0, t1});
     c.launches++;

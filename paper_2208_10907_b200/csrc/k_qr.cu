@@ -263,7 +263,9 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
 
   double r11 = -1.0;
   int rank = 0;
+  long long t_piv = 0, t_refl = 0, t_tile = 0, t_mem = 0, t0c;
   for (int k = 0; k < kmax; ++k) {
+    t0c = clock64();
     double mx = -1.0;
     for (int j = k + tid; j < n; j += NT) mx = fmax(mx, S.cn2[j]);
     const double best = block_max(mx, redd);
@@ -301,6 +303,7 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
     const bool floor_hit = pivot_norm <= 1e-15 * r11;
     if ((diag_done && members_done) || floor_hit) break;
 
+    t_piv += clock64() - t0c; t0c = clock64();
     // make_reflector (linalg.cpp:152-178), sequential on one thread.
     double* vk = S.V + int64_t(k) * m;
     double* wk = W + int64_t(k) * ldw;
@@ -334,54 +337,134 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
     for (int i = tid; i < m; i += NT) vsh[i] = vk[i];
     __syncthreads();
     const double tau = sh_tau;
+    t_refl += clock64() - t0c; t0c = clock64();
     // apply_reflector to columns k+1.. (linalg.cpp:137-149) + norm downdate.
-    const int rows = m - k;
-    const int pitch = rows | 1;
-    const int twmax = max(1, min(NT, tile_doubles / pitch));
-    for (int jt = k + 1; jt < n; jt += twmax) {
-      const int tw = min(twmax, n - jt);
-      load_tile(T, pitch, W, ldw, k, rows, jt, tw);
-      __syncthreads();
-      if (tid < tw) {
-        double* col = T + tid * pitch;
-        if (tau != 0.0) {
-          const double dot = red_h_smem(vsh + k, col, 1, rows);
-          const double sc = -(tau * dot);
-#pragma unroll 8
-          for (int r = 0; r < rows; ++r) col[r] = fma(sc, vsh[k + r], col[r]);
+    // Every warp streams its own column tiles through a private slice of the
+    // shared tile (cp.async load -> per-lane column update -> store), with no
+    // CTA barrier inside the step, so loads, dot chains and stores of
+    // different warps overlap.
+    {
+      const int rows = m - k;
+      const int pitch = rows | 1;
+      const int warp = tid >> 5, lane = tid & 31;
+      constexpr int NW = NT / 32;
+      const int per_warp = tile_doubles / NW;
+      const int cw = max(1, min(32, per_warp / pitch));
+      double* Tw = T + warp * per_warp;
+      for (int jt = k + 1 + warp * cw; jt < n; jt += NW * cw) {
+        const int tw = min(cw, n - jt);
+        for (int c = 0; c < tw; ++c) {
+          const double* src = W + int64_t(jt + c) * ldw + k;
+          for (int r = lane; r < rows; r += 32) cp_async8(Tw + c * pitch + r, src + r);
         }
-        // GCC computes rkj*rkj once (rounded) for the norm and member downdates.
-        const int j = jt + tid;
-        const double rkj = col[0];
-        const double sq = rkj * rkj;
-        double upd = S.cn2[j] - sq;
-        if (upd < 1e-8 * S.cn2o[j])
-          upd = red_p2([&](int r, double& a, double& b) { a = b = col[r]; }, 1, rows - 1);
-        S.cn2[j] = fmax(0.0, upd);
-        S.sq[j] = sq;
+        cp_async_wait_all();
+        __syncwarp();
+        if (lane < tw) {
+          double* col = Tw + lane * pitch;
+          if (tau != 0.0) {
+            const double dot = red_h_smem(vsh + k, col, 1, rows);
+            const double sc = -(tau * dot);
+#pragma unroll 8
+            for (int r = 0; r < rows; ++r) col[r] = fma(sc, vsh[k + r], col[r]);
+          }
+          // GCC computes rkj*rkj once (rounded) for the norm and member downdates.
+          const int j = jt + lane;
+          const double rkj = col[0];
+          const double sq = rkj * rkj;
+          double upd = S.cn2[j] - sq;
+          if (upd < 1e-8 * S.cn2o[j])
+            upd = red_p2([&](int r, double& a, double& b) { a = b = col[r]; }, 1, rows - 1);
+          S.cn2[j] = fmax(0.0, upd);
+          S.sq[j] = sq;
+        }
+        __syncwarp();
+        for (int c = 0; c < tw; ++c) {
+          double* dst = W + int64_t(jt + c) * ldw + k;
+          for (int r = lane; r < rows; r += 32) dst[r] = Tw[c * pitch + r];
+        }
+        __syncwarp();
       }
       __syncthreads();
-      store_tile(T, pitch, W, ldw, k, rows, jt, tw);
-      __syncthreads();
     }
+    t_tile += clock64() - t0c; t0c = clock64();
     ++rank;
     if (members && tid < 32) {
       // member_mass[g] -= rkj^2 in column order (linalg.cpp:312-315). Warp 0
-      // stages 256 (rkj^2, group) pairs at a time in shared memory; lane 0
+      // streams (rkj^2, group) pairs through double-buffered shared staging
+      // (cp.async prefetch of chunk i+1 while chunk i is consumed); lane 0
       // runs the ordered chain with the running group value in a register.
-      double* st_r = T;
-      int* st_g = reinterpret_cast<int*>(T + 256);
+      constexpr int CH = 512;
+      double* st_r0 = T;
+      int* st_g0 = reinterpret_cast<int*>(T + 2 * CH);
       int cur = -1;
       double val = 0.0;
-      for (int j0 = k + 1; j0 < n; j0 += 256) {
-        const int cnt = min(256, n - j0);
+      auto stage = [&](int j0, int b) {
+        const int cnt = min(CH, n - j0);
         for (int u = tid; u < cnt; u += 32) {
-          st_r[u] = S.sq[j0 + u];
-          st_g[u] = S.mof[j0 + u];
+          cp_async8(st_r0 + b * CH + u, S.sq + j0 + u);
+          const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(st_g0 + b * CH + u));
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(S.mof + j0 + u));
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+      };
+      int buf = 0;
+      if (k + 1 < n) stage(k + 1, 0);
+      for (int j0 = k + 1; j0 < n; j0 += CH, buf ^= 1) {
+        const int cnt = min(CH, n - j0);
+        if (j0 + CH < n) {
+          stage(j0 + CH, buf ^ 1);
+          asm volatile("cp.async.wait_group 1;\n" ::);
+        } else {
+          asm volatile("cp.async.wait_group 0;\n" ::);
         }
         __syncwarp();
+        const double* st_r = st_r0 + buf * CH;
+        const int* st_g = st_g0 + buf * CH;
         if (tid == 0) {
-          for (int u = 0; u < cnt; ++u) {
+          // Fast path for runs of 8 of one member (the common case: members are
+          // contiguous column ranges).
+          int u = 0;
+          for (; u + 8 <= cnt; u += 8) {
+            int gg[8];
+            double ss[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              gg[q] = st_g[u + q];
+              ss[q] = st_r[u + q];
+            }
+            bool same = true;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) same &= gg[q] == cur;
+            if (same) {
+              // Unclamped chain (pure DADD latency); the clamp is a no-op
+              // unless an intermediate goes negative, checked off the chain.
+              double t[8];
+              double x = val;
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                x = x - ss[q];
+                t[q] = x;
+              }
+              bool neg = false;
+#pragma unroll
+              for (int q = 0; q < 8; ++q) neg |= t[q] < 0.0;
+              if (!neg) {
+                val = x;
+                continue;
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              if (gg[q] != cur) {
+                if (cur >= 0) mmsh[cur] = val;
+                cur = gg[q];
+                val = mmsh[cur];
+              }
+              const double v = val - ss[q];
+              val = v < 0.0 ? 0.0 : v;
+            }
+          }
+          for (; u < cnt; ++u) {
             const int g = st_g[u];
             if (g != cur) {
               if (cur >= 0) mmsh[cur] = val;
@@ -403,7 +486,13 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
       }
     }
     __syncthreads();
+    t_mem += clock64() - t0c;
   }
+  if (tid == 0 && job.dbg) {
+    job.dbg[0] = double(t_piv); job.dbg[1] = double(t_refl); job.dbg[2] = double(t_tile);
+    job.dbg[3] = double(t_mem); job.dbg[4] = double(rank); job.dbg[5] = double(n);
+  }
+  long long tq = clock64();
 
   // form_q (linalg.cpp:181-185): Q = I, reflectors applied backward.
   double* Q = job.Q;
@@ -424,6 +513,7 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
     __syncthreads();
   }
   if (tid == 0) *job.rank_out = rank;
+  if (tid == 0 && job.dbg) job.dbg[6] = double(clock64() - tq);
 }
 
 }  // namespace
@@ -446,7 +536,7 @@ void launch_qr(const QrJob* jobs, int njobs, int max_m, int max_nmem, cudaStream
   const size_t fixed = sizeof(double) * size_t(max_m + max_nmem);
   size_t tile = budget > fixed + 8192 ? (budget - fixed) / sizeof(double) : 1024;
   if (tile < size_t(max_m | 1)) tile = size_t(max_m | 1);  // at least one column
-  if (tile < 384) tile = 384;                               // member staging
+  if (tile < 1536) tile = 1536;                             // member staging (2 x 512)
   const size_t smem = fixed + tile * sizeof(double);
   qr_kernel<<<njobs, NT, smem, st>>>(jobs, int(tile), max_nmem);
 }

@@ -138,6 +138,7 @@ struct QrJob {
   double* scratch;     // >= 3 n + nmem*2 doubles + m*kmax reflectors
   double* Q;           // output m x m row-major (Q[i*m + j])
   int* rank_out;
+  double* dbg = nullptr;  // optional per-job phase cycle counters (profiling)
 };
 void launch_qr(const QrJob* jobs, int njobs, int max_m, int max_nmem, cudaStream_t st);
 size_t qr_scratch_doubles(int m, int n, int nmem);
