@@ -142,6 +142,9 @@ void GemmBatch::run(Ctx& c, int tag) {
   if (jobs.empty()) return;
   std::vector<GemmTile> tiles;
   double fl = 0;
+  int max_rows = 0;
+  for (auto& j : jobs) max_rows = std::max(max_rows, j.C.rows);
+  const int bm = gemm_tile_rows(max_rows);
   for (size_t j = 0; j < jobs.size(); ++j) {
     const Mat& C = jobs[j].C;
     if (C.rows <= 0 || C.cols <= 0) continue;
@@ -150,7 +153,7 @@ void GemmBatch::run(Ctx& c, int tag) {
       fl += 2.0 * C.rows * double(sg.A.cols) * C.cols;
       if (sg.gen) fl += double(sg.A.cols) * C.cols * (c.kp.kind == 0 ? 9 : 11);
     }
-    const int tm = (C.rows + 63) / 64, tn = (C.cols + 63) / 64;
+    const int tm = (C.rows + bm - 1) / bm, tn = (C.cols + 63) / 64;
     for (int a = 0; a < tm; ++a)
       for (int b = 0; b < tn; ++b) tiles.push_back({int(j), a, b});
   }
@@ -172,8 +175,8 @@ void GemmBatch::run(Ctx& c, int tag) {
     }
   }
   auto ev = c.prof_begin();
-  launch_gemm(dj, ds, dt, int(tiles.size()), c.kp, c.cloud, c.err, tag, c.stream);
-  c.prof_end("gemm", ev, fl, by);
+  launch_gemm(dj, ds, dt, int(tiles.size()), bm, c.kp, c.cloud, c.err, tag, c.stream);
+  c.prof_end(c.prof_detail ? ("gemm@" + c.phase).c_str() : "gemm", ev, fl, by);
   c.launches++;
   cuda_check(cudaGetLastError(), "gemm launch");
 }
@@ -274,8 +277,112 @@ void LuBatch::run(Ctx& c) {
   c.sync();
 }
 
+// Blocked left solve (forward/backward substitution with GEMM updates between
+// 32-row diagonal blocks) for wide right-hand sides.
+static void run_blocked(Ctx& c, const std::vector<SolveJob>& bj) {
+  if (bj.empty()) return;
+  constexpr int NB = 32;
+  // X <- P X for the permuted kinds.
+  {
+    std::vector<std::pair<int, int>> shapes;
+    std::vector<size_t> idx;
+    for (size_t t = 0; t < bj.size(); ++t)
+      if (bj[t].kind == SOLVE_FULL || bj[t].kind == SOLVE_LOWER) {
+        shapes.push_back({bj[t].X.rows, bj[t].X.cols});
+        idx.push_back(t);
+      }
+    if (!idx.empty()) {
+      auto tmp = alloc_mats(c, shapes);
+      CopyBatch cb;
+      std::vector<GatherJob> gj;
+      std::vector<int2> tiles;
+      for (size_t u = 0; u < idx.size(); ++u) {
+        const SolveJob& s = bj[idx[u]];
+        cb.copy(tmp[u].m, s.X);
+        gj.push_back({s.X, tmp[u].m, s.perm});
+        const int64_t tot = int64_t(s.X.rows) * s.X.cols;
+        for (int64_t e = 0; e < tot; e += 4096) tiles.push_back(make_int2(int(gj.size() - 1), int(e / 4096)));
+      }
+      cb.run(c);
+      Slab k1, k2;
+      auto* dg = upload(c, gj, k1);
+      auto* dt = upload(c, tiles, k2);
+      launch_gather_rows(dg, dt, int(tiles.size()), c.stream);
+      c.launches++;
+      cuda_check(cudaGetLastError(), "gather rows");
+    }
+  }
+  int maxm = 0;
+  for (auto& s : bj) maxm = std::max(maxm, s.lu.rows);
+  const int nblk = (maxm + NB - 1) / NB;
+  auto block_step = [&](const std::vector<SolveJob>& js, int b, bool lower) {
+    if (js.empty()) return;
+    std::vector<TrsmBlockJob> tj;
+    std::vector<int2> tiles;
+    GemmBatch gb;
+    for (const SolveJob& s : js) {
+      const int m = s.lu.rows;
+      const int kb = b * NB;
+      if (kb >= m) continue;
+      const int nb = std::min(NB, m - kb);
+      tj.push_back({s.lu, s.X, kb, nb, lower ? 1 : 0});
+      for (int g = 0; g < (s.X.cols + 127) / 128; ++g) tiles.push_back(make_int2(int(tj.size() - 1), g));
+    }
+    Slab k1, k2;
+    auto* dj = upload(c, tj, k1);
+    auto* dt = upload(c, tiles, k2);
+    launch_trsm_block(dj, dt, int(tiles.size()), c.stream);
+    c.launches++;
+    cuda_check(cudaGetLastError(), "trsm block");
+    for (const SolveJob& s : js) {
+      const int m = s.lu.rows;
+      const int kb = b * NB;
+      if (kb >= m) continue;
+      const int nb = std::min(NB, m - kb);
+      const Mat& L = s.lu;
+      const Mat& X = s.X;
+      if (lower) {
+        if (kb + nb >= m) continue;
+        // rows below: x[i] -= sum_k L(i,k) x[k], k ascending
+        gb.job(X.sub(kb + nb, 0, m - kb - nb, X.cols), true);
+        gb.seg(L.sub(kb + nb, kb, m - kb - nb, nb), X.sub(kb, 0, nb, X.cols), -1.0);
+      } else {
+        if (kb == 0) continue;
+        // rows above: k descending -> reversed column / row views
+        const Mat Arev{&L.at(0, kb + nb - 1), kb, nb, L.rs, -L.cs};
+        const Mat Brev{&X.at(kb + nb - 1, 0), nb, X.cols, -X.rs, X.cs};
+        gb.job(X.sub(0, 0, kb, X.cols), true);
+        gb.seg(Arev, Brev, -1.0);
+      }
+    }
+    gb.run(c);
+  };
+  // Forward sweep for FULL/LOWER, backward sweep for FULL/UPPER.
+  std::vector<SolveJob> fwd, bwd;
+  for (auto& s : bj) {
+    if (s.kind != SOLVE_UPPER) fwd.push_back(s);
+    if (s.kind != SOLVE_LOWER) bwd.push_back(s);
+  }
+  for (int b = 0; b < nblk; ++b) block_step(fwd, b, true);
+  for (int b = nblk - 1; b >= 0; --b) block_step(bwd, b, false);
+}
+
 void SolveBatch::run(Ctx& c) {
   if (jobs.empty()) return;
+  {
+    // Wide left solves go through the blocked path (GEMM updates).
+    std::vector<SolveJob> blocked, rest;
+    for (auto& s : jobs) {
+      const bool left = s.kind == SOLVE_FULL || s.kind == SOLVE_LOWER || s.kind == SOLVE_UPPER;
+      if (left && s.X.cols >= 48 && s.lu.rows >= 64) blocked.push_back(s);
+      else rest.push_back(s);
+    }
+    if (!blocked.empty()) {
+      run_blocked(c, blocked);  // flops counted by its GEMM + block launches
+      jobs = rest;
+      if (jobs.empty()) return;
+    }
+  }
   std::vector<SolveChunk> chunks;
   size_t smem = 1;
   double fl = 0;
@@ -298,7 +405,8 @@ void SolveBatch::run(Ctx& c) {
   for (auto& s : jobs) by += 8.0 * s.lu.rows * double(s.lu.rows) + 16.0 * s.X.rows * double(s.X.cols);
   auto ev = c.prof_begin();
   launch_solve(dj, dc, int(chunks.size()), smem, c.stream);
-  c.prof_end("solve", ev, fl, by);
+  static const char* kinds[] = {"full", "lower", "upper", "trans", "right", "upper_right"};
+  c.prof_end(c.prof_detail ? ("solve@" + c.phase + ":" + kinds[jobs[0].kind]).c_str() : "solve", ev, fl, by);
   c.launches++;
   cuda_check(cudaGetLastError(), "solve launch");
 }
@@ -325,11 +433,11 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
   while (t0 < n_items) {
     // Chunk so the working copies + scratch stay under the budget.
     size_t bytes = 0, t1 = t0;
-    while (t1 < n_items) {
+    while (t1 < n_items) {  // (+32 B per item: 16-byte alignment padding)
       const auto& it = items[t1];
-      const size_t need = sizeof(double) * ((it.inplace ? 0 : size_t(it.m) * it.n) +
+      const size_t need = sizeof(double) * ((it.inplace ? 0 : size_t((it.m + 1) & ~1) * it.n) +
                                             qr_scratch_doubles(it.m, it.n, int(it.offs.size()) - 1)) +
-                          sizeof(int64_t) * it.offs.size() + 1024;
+                          sizeof(int64_t) * it.offs.size() + 1024 + 32;
       if (t1 > t0 && bytes + need > mem_budget) break;
       bytes += need;
       ++t1;
@@ -345,7 +453,7 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
     Slab ko;
     int64_t* doffs = upload(c, offs_all, ko);
     char* at = static_cast<char*>(work.get());
-    int max_m = 1, max_nmem = 1;
+    int max_m = 1, max_nmem = 1, min_n = 1 << 30;
     double fl = 0;
     for (size_t t = t0; t < t1; ++t) {
       const auto& it = items[t];
@@ -367,16 +475,19 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
         j.ldw = it.concat.m.cs;
       } else {
         j.work = reinterpret_cast<double*>(at);
-        j.ldw = it.m;
-        at += sizeof(double) * size_t(it.m) * it.n;
+        j.ldw = (it.m + 1) & ~1;  // even: 16-byte aligned column segments
+        at += sizeof(double) * size_t(j.ldw) * it.n;
+        at = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(at) + 15) & ~uintptr_t(15));
       }
       j.scratch = reinterpret_cast<double*>(at);
       at += sizeof(double) * qr_scratch_doubles(it.m, it.n, j.nmem);
+      at = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(at) + 15) & ~uintptr_t(15));
       j.Q = Q[t].m.p;
       j.rank_out = static_cast<int*>(rk.get()) + t;
       jobs.push_back(j);
       max_m = std::max(max_m, it.m);
       max_nmem = std::max(max_nmem, j.nmem);
+      min_n = std::min(min_n, it.n);
       fl += 2.0 * it.m * double(it.n);  // column norms
     }
     c.add_flops(fl);
@@ -391,7 +502,9 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
     Slab kj;
     auto* dj = upload(c, jobs, kj);
     auto ev = c.prof_begin();
-    launch_qr(dj, int(jobs.size()), max_m, max_nmem, c.stream);
+    const int cl = getenv("H2G_QR_CLUSTER") ? atoi(getenv("H2G_QR_CLUSTER"))
+                                            : qr_cluster_size(int(jobs.size()), min_n);
+    launch_qr(dj, int(jobs.size()), max_m, max_nmem, cl, c.stream);
     if (ddbg) {
       std::vector<double> h(8 * jobs.size());
       cudaMemcpyAsync(h.data(), ddbg, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c.stream);

@@ -4,6 +4,7 @@
 // jobs, uploads the descriptors once and launches one kernel per job type.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -49,6 +50,7 @@ struct Ctx {
     double flops, bytes;
   };
   bool prof = false;
+  bool prof_detail = getenv("H2G_PROF_DETAIL") != nullptr;  // per-phase kernel names
   std::vector<ProfRec> prec;
   std::map<std::string, ProfAgg> pagg;
   cudaEvent_t prof_begin();

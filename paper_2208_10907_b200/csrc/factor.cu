@@ -8,6 +8,8 @@
 // so factors and solutions are bitwise equal to the reference (Laplace).
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <functional>
 #include <set>
@@ -318,7 +320,8 @@ struct Driver {
     std::vector<int64_t> offs{0};
     DMat concat;
     Mat slice(int off, int w) const {
-      return Mat{concat.m.p + int64_t(off) * std::max(dim, 1), dim, w, 1, std::max(dim, 1)};
+      const int ld = std::max(2, (dim + 1) & ~1);
+      return Mat{concat.m.p + int64_t(off) * ld, dim, w, 1, ld};
     }
     int add(int w) {
       const int off = width;
@@ -328,11 +331,16 @@ struct Driver {
     }
     // Column-major (ld = dim): each member column is contiguous, so the QR's
     // column tiles are contiguous HBM ranges.
-    size_t bytes() const { return sizeof(double) * size_t(dim) * size_t(std::max(width, 1)); }
+    size_t bytes() const {
+      return sizeof(double) * size_t(std::max(2, (dim + 1) & ~1)) * size_t(std::max(width, 1));
+    }
   };
+  // Column stride = dim rounded up to even: 16-byte aligned column segments
+  // for the QR's TMA bulk copies.
+  static int ldc(int dim) { return std::max(2, (dim + 1) & ~1); }
   void alloc_concat(Members& M) {
-    M.concat = alloc_mat(c, std::max(M.dim, 1), std::max(M.width, 1));
-    M.concat.m = Mat{M.concat.m.p, M.dim, M.width, 1, std::max(M.dim, 1)};
+    M.concat = alloc_mat(c, ldc(M.dim), std::max(M.width, 1));
+    M.concat.m = Mat{M.concat.m.p, M.dim, M.width, 1, ldc(M.dim)};
   }
 
   using FillFn = std::function<void(int64_t, int64_t)>;
@@ -355,11 +363,16 @@ struct Driver {
         bytes += need;
         ++k1;
       }
+      const bool hp = getenv("H2G_HOST_PROF") != nullptr;
+      double ht0 = now_s();
       for (int64_t k = k0; k < k1; ++k) {
         alloc_concat(rows[k]);
         if (cols) alloc_concat((*cols)[k]);
       }
+      double ht1 = now_s();
       fill(k0, k1);
+      if (hp) c.sync();
+      double ht2 = now_s();
       QrBatch qb;
       for (int64_t k = k0; k < k1; ++k)
         qb.add(rows[k].concat, rows[k].dim, rows[k].width, rows[k].offs, opt.tol, opt.cap, true);
@@ -370,6 +383,7 @@ struct Driver {
       std::vector<DMat> Q;
       std::vector<int> rank;
       qb.run(c, Q, rank, opt.qr_mem_budget);
+      double ht3 = now_s();
       const int64_t nk = k1 - k0;
       for (int64_t k = k0; k < k1; ++k) {
         const Mat qc = cols ? Q[nk + (k - k0)].m : Mat{};
@@ -378,9 +392,15 @@ struct Driver {
       }
       // Drain the sink's copies before the Q's and concats are released.
       c.sync();
+      double ht4 = now_s();
       for (int64_t k = k0; k < k1; ++k) {
         rows[k].concat = DMat{};
         if (cols) (*cols)[k].concat = DMat{};
+      }
+      if (hp) {
+        c.sync();
+        fprintf(stderr, "HOSTPROF run_bases boxes=%ld alloc %.3f fill %.3f qr %.3f sink %.3f free %.3f\n",
+                long(k1 - k0), ht1 - ht0, ht2 - ht1, ht3 - ht2, ht4 - ht3, now_s() - ht4);
       }
       k0 = k1;
     }

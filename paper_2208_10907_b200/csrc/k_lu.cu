@@ -227,7 +227,72 @@ __global__ void __launch_bounds__(256) solve_kernel(const SolveJob* __restrict__
   }
 }
 
+// One diagonal block of a blocked left triangular solve, for every RHS
+// column (one thread per column; the nb x nb factor block staged in shared
+// memory). lower: unit-lower forward steps k in [kb, kb+nb); upper: divide and
+// backward steps k from kb+nb-1 down to kb. Together with the GEMM updates
+// between blocks (accumulated in the same k order) every element sees the
+// reference's exact update sequence (linalg.cpp:404-542).
+__global__ void __launch_bounds__(128) trsm_block_kernel(const TrsmBlockJob* __restrict__ jobs,
+                                                         const int2* __restrict__ tiles) {
+  __shared__ double blk[32 * 32];
+  const int2 t = tiles[blockIdx.x];
+  const TrsmBlockJob job = jobs[t.x];
+  const int kb = job.kb, nb = job.nb;
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int i = e % nb, kk = e / nb;
+    blk[kk * 32 + i] = job.lu.at(kb + i, kb + kk);
+  }
+  __syncthreads();
+  const int c = t.y * blockDim.x + threadIdx.x;
+  if (c >= job.X.cols) return;
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = i < nb ? job.X.at(kb + i, c) : 0.0;
+  if (job.lower) {
+#pragma unroll
+    for (int kk = 0; kk < 32; ++kk) {
+      if (kk >= nb) break;
+      const double xk = x[kk];
+#pragma unroll
+      for (int i = kk + 1; i < 32; ++i)
+        if (i < nb) x[i] = fma(-blk[kk * 32 + i], xk, x[i]);
+    }
+  } else {
+#pragma unroll
+    for (int kk = 31; kk >= 0; --kk) {
+      if (kk >= nb) continue;
+      x[kk] = x[kk] / blk[kk * 32 + kk];
+      const double xk = x[kk];
+#pragma unroll
+      for (int i = 0; i < kk; ++i) x[i] = fma(-blk[kk * 32 + i], xk, x[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (i < nb) job.X.at(kb + i, c) = x[i];
+}
+
+__global__ void gather_rows_kernel(const GatherJob* __restrict__ jobs, const int2* __restrict__ tiles) {
+  const int2 t = tiles[blockIdx.x];
+  const GatherJob job = jobs[t.x];
+  const int64_t e0 = int64_t(t.y) * 4096;
+  const int64_t tot = int64_t(job.dst.rows) * job.dst.cols;
+  for (int64_t e = e0 + threadIdx.x; e < min(tot, e0 + 4096); e += blockDim.x) {
+    const int i = int(e % job.dst.rows), j = int(e / job.dst.rows);
+    job.dst.at(i, j) = job.src.at(job.perm[i], j);
+  }
+}
+
 }  // namespace
+
+void launch_trsm_block(const TrsmBlockJob* jobs, const int2* tiles, int ntiles, cudaStream_t st) {
+  if (ntiles > 0) trsm_block_kernel<<<ntiles, 128, 0, st>>>(jobs, tiles);
+}
+
+void launch_gather_rows(const GatherJob* jobs, const int2* tiles, int ntiles, cudaStream_t st) {
+  if (ntiles > 0) gather_rows_kernel<<<ntiles, 256, 0, st>>>(jobs, tiles);
+}
 
 void launch_lu(const LuJob* jobs, int njobs, ErrWord* err, int tag, cudaStream_t st) {
   if (njobs > 0) lu_kernel<<<njobs, NT, 0, st>>>(jobs, err, tag);

@@ -8,7 +8,11 @@
 // writes coalesced rows. Column norms, downdates, the 4e-15 tie rule, the
 // member masses and the stopping tests all follow the reference's operation
 // order, so ranks and Q are bitwise equal to the reference's.
+#include <cooperative_groups.h>
+
 #include "kernels.hpp"
+
+namespace cg = cooperative_groups;
 
 namespace h2g {
 
@@ -169,6 +173,46 @@ __device__ __forceinline__ double red_h_smem(const double* __restrict__ v,
   return s;
 }
 
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)),
+               "r"(bytes));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
+      "r"(parity));
+}
+// TMA bulk copies (UBLKCP): global -> shared completing on an mbarrier, and
+// shared -> global in a bulk group.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
+               "r"(smem_addr(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
 }
@@ -201,6 +245,21 @@ __device__ __forceinline__ void store_tile(const double* T, int pitch, double* W
   }
 }
 
+// Cluster-split QR: the G CTAs of a thread-block cluster share one basis;
+// column blocks of CB columns are owned round-robin (owner = (j / CB) % G).
+// Per Householder step: cluster-wide pivot reductions through distributed
+// shared memory, the swap and the reflector by CTA 0, every CTA sweeps its own
+// columns, CTA 0 runs the ordered member-mass chain. Global data written by
+// one CTA is read by the others only across cluster barriers
+// (barrier.cluster release/acquire).
+constexpr int CB = NT;
+
+struct ClSlots {
+  double d;
+  int piv, pos;
+  int flag;
+};
+
 // Dynamic shared memory: [ v (m) | member masses (nmem) | column tile ].
 __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ jobs, int tile_doubles,
                                                    int nmem_cap) {
@@ -208,78 +267,129 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
   __shared__ double redd[32];
   __shared__ int redi[32];
   __shared__ double sh_tau;
-  const QrJob job = jobs[blockIdx.x];
+  __shared__ ClSlots slot;
+  __shared__ __align__(8) uint64_t mbar[NT / 32][2];
+  __shared__ unsigned mpar[NT / 32][2];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int G = int(cluster.num_blocks());
+  const int cr = int(cluster.block_rank());
+  const QrJob job = jobs[blockIdx.x / G];
   const int m = job.m, n = job.n, nmem = job.nmem;
   double* W = job.work;
   const int64_t ldw = job.ldw;
   const int tid = threadIdx.x;
   double* vsh = dsm;
   double* mmsh = dsm + m;
-  double* T = dsm + m + nmem_cap;
+  double* T = dsm + ((m + nmem_cap + 1) & ~1);  // 16-byte aligned tile
   Scratch S = carve(job.scratch, m, n, nmem);
   const int kmax0 = m < n ? m : n;
   int kmax = kmax0;
   if (job.cap > 0 && job.cap < kmax) kmax = job.cap;
+  const bool lead = cr == 0;
+  if (tid < NT / 32) {
+    mbar_init(&mbar[tid][0], 1);
+    mbar_init(&mbar[tid][1], 1);
+    mpar[tid][0] = mpar[tid][1] = 0;
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
 
-  // R = A (skipped when factoring in place).
+  // R = A (skipped when factoring in place): own columns.
   if (!(job.A.p == W && job.A.rs == 1 && job.A.cs == ldw)) {
-    for (int64_t e = tid; e < int64_t(m) * n; e += NT) {
-      const int j = int(e / m), i = int(e % m);
-      W[j * ldw + i] = job.A.at(i, j);
-    }
+    for (int b = cr; b * CB < n; b += G)
+      for (int j = b * CB; j < min(n, (b + 1) * CB); ++j)
+        for (int i = tid; i < m; i += NT) W[int64_t(j) * ldw + i] = job.A.at(i, j);
     __syncthreads();
   }
-  // Column norms (pattern P2 over all rows), tile by tile.
+  // Column norms of own columns (pattern P2 over all rows), tile by tile.
   {
     const int pitch = m | 1;
     const int twmax = max(1, min(NT, tile_doubles / pitch));
-    for (int jt = 0; jt < n; jt += twmax) {
-      const int tw = min(twmax, n - jt);
-      load_tile(T, pitch, W, ldw, 0, m, jt, tw);
-      __syncthreads();
-      if (tid < tw) {
-        const double* col = T + tid * pitch;
-        const double s = red_p2([&](int i, double& a, double& b) { a = b = col[i]; }, 0, m);
-        S.cn2[jt + tid] = s;
-        S.cn2o[jt + tid] = s;
-        S.piv[jt + tid] = jt + tid;
+    for (int b = cr; b * CB < n; b += G) {
+      const int j1 = min(n, (b + 1) * CB);
+      for (int jt = b * CB; jt < j1; jt += twmax) {
+        const int tw = min(twmax, j1 - jt);
+        load_tile(T, pitch, W, ldw, 0, m, jt, tw);
+        __syncthreads();
+        if (tid < tw) {
+          const double* col = T + tid * pitch;
+          const double s = red_p2([&](int i, double& a, double& b2) { a = b2 = col[i]; }, 0, m);
+          S.cn2[jt + tid] = s;
+          S.cn2o[jt + tid] = s;
+          S.piv[jt + tid] = jt + tid;
+        }
+        __syncthreads();
       }
-      __syncthreads();
     }
   }
+  cluster.sync();
   const bool members = nmem >= 1;
-  if (members) {
-    for (int g = tid; g < nmem; g += NT) {
-      double mass = 0.0;
-      for (int64_t j = job.member_off[g]; j < job.member_off[g + 1]; ++j) {
-        S.mof[j] = g;
-        mass += S.cn2[j];
+  if (lead) {
+    if (members) {
+      for (int g = tid; g < nmem; g += NT) {
+        double mass = 0.0;
+        for (int64_t j = job.member_off[g]; j < job.member_off[g + 1]; ++j) {
+          S.mof[j] = g;
+          mass += S.cn2[j];
+        }
+        mmsh[g] = mass;
+        S.mt[g] = job.member_tol * job.member_tol * mass;
       }
-      mmsh[g] = mass;
-      S.mt[g] = job.member_tol * job.member_tol * mass;
     }
+    __syncthreads();
+    int not_done = 0;
+    if (members)
+      for (int g = tid; g < nmem; g += NT) not_done |= (mmsh[g] > S.mt[g]);
+    not_done = __syncthreads_or(not_done);
+    if (tid == 0) slot.flag = not_done;
   }
-  __syncthreads();
 
   double r11 = -1.0;
   int rank = 0;
   long long t_piv = 0, t_refl = 0, t_tile = 0, t_mem = 0, t0c;
   for (int k = 0; k < kmax; ++k) {
     t0c = clock64();
+    // Pivot: cluster-wide max of the remaining norms, then the lowest
+    // original index within the 4e-15 tie band (linalg.cpp:263-274).
     double mx = -1.0;
-    for (int j = k + tid; j < n; j += NT) mx = fmax(mx, S.cn2[j]);
-    const double best = block_max(mx, redd);
+    for (int b = cr; b * CB < n; b += G) {
+      const int j = max(k, b * CB) + tid;
+      if (j < min(n, (b + 1) * CB)) mx = fmax(mx, S.cn2[j]);
+    }
+    mx = block_max(mx, redd);
+    if (tid == 0) slot.d = mx;
+    cluster.sync();
+    double best = -1.0;
+    for (int q = 0; q < G; ++q) best = fmax(best, cluster.map_shared_rank(&slot, q)->d);
+    const int members_not_done = cluster.map_shared_rank(&slot, 0)->flag;
     if (best <= 0.0) break;
     const double tie = best * (1.0 - 4e-15);
     int cand = 0x7fffffff;
-    for (int j = k + tid; j < n; j += NT)
-      if (S.cn2[j] >= tie) cand = min(cand, S.piv[j]);
-    const int sel_orig = block_min_int(cand, redi);
-    int selpos = 0x7fffffff;
-    for (int j = k + tid; j < n; j += NT)
-      if (S.piv[j] == sel_orig && S.cn2[j] >= tie) selpos = j;
-    const int sel = block_min_int(selpos, redi);
-    if (sel != k) {
+    for (int b = cr; b * CB < n; b += G) {
+      const int j = max(k, b * CB) + tid;
+      if (j < min(n, (b + 1) * CB) && S.cn2[j] >= tie) cand = min(cand, S.piv[j]);
+    }
+    cand = block_min_int(cand, redi);
+    int cpos = 0x7fffffff;
+    for (int b = cr; b * CB < n; b += G) {
+      const int j = max(k, b * CB) + tid;
+      if (j < min(n, (b + 1) * CB) && S.piv[j] == cand && S.cn2[j] >= tie) cpos = j;
+    }
+    cpos = block_min_int(cpos, redi);
+    if (tid == 0) {
+      slot.piv = cand;
+      slot.pos = cpos;
+    }
+    cluster.sync();
+    int sel_orig = 0x7fffffff, sel = 0x7fffffff;
+    for (int q = 0; q < G; ++q) {
+      const ClSlots* o = cluster.map_shared_rank(&slot, q);
+      if (o->piv < sel_orig) {
+        sel_orig = o->piv;
+        sel = o->pos;
+      }
+    }
+    if (lead && sel != k) {
       for (int i = tid; i < m; i += NT) {
         const double t = W[int64_t(k) * ldw + i];
         W[int64_t(k) * ldw + i] = W[int64_t(sel) * ldw + i];
@@ -292,22 +402,19 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
         if (members) { ti = S.mof[k]; S.mof[k] = S.mof[sel]; S.mof[sel] = ti; }
       }
     }
-    __syncthreads();
-    const double pivot_norm = sqrt(fmax(0.0, S.cn2[k]));
+    cluster.sync();
+    const double pivot_norm = sqrt(fmax(0.0, __ldcg(&S.cn2[k])));
     if (k == 0) r11 = pivot_norm;
     const bool diag_done = pivot_norm <= job.tol * r11;
-    int not_done = 0;
-    if (members)
-      for (int g = tid; g < nmem; g += NT) not_done |= (mmsh[g] > S.mt[g]);
-    const bool members_done = !__syncthreads_or(not_done);
+    const bool members_done = !members_not_done;
     const bool floor_hit = pivot_norm <= 1e-15 * r11;
     if ((diag_done && members_done) || floor_hit) break;
 
     t_piv += clock64() - t0c; t0c = clock64();
-    // make_reflector (linalg.cpp:152-178), sequential on one thread.
+    // make_reflector (linalg.cpp:152-178), sequential on one thread of CTA 0.
     double* vk = S.V + int64_t(k) * m;
     double* wk = W + int64_t(k) * ldw;
-    if (tid == 0) {
+    if (lead && tid == 0) {
       const double normsq = red_p2([&](int i, double& a, double& b) { a = b = wk[i]; }, k, m - k);
       const double norm = sqrt(normsq);
       for (int i = 0; i < k; ++i) vk[i] = 0.0;
@@ -331,18 +438,19 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
         for (int i = k + 1; i < m; ++i) wk[i] = 0.0;
       }
       S.tau[k] = tau;
-      sh_tau = tau;
     }
-    __syncthreads();
-    for (int i = tid; i < m; i += NT) vsh[i] = vk[i];
+    cluster.sync();
+    for (int i = tid; i < m; i += NT) vsh[i] = __ldcg(&vk[i]);
+    if (tid == 0) sh_tau = __ldcg(&S.tau[k]);
     __syncthreads();
     const double tau = sh_tau;
     t_refl += clock64() - t0c; t0c = clock64();
-    // apply_reflector to columns k+1.. (linalg.cpp:137-149) + norm downdate.
+    // apply_reflector to own columns k+1.. (linalg.cpp:137-149) + downdate.
     // Every warp streams its own column tiles through a private slice of the
     // shared tile (cp.async load -> per-lane column update -> store), with no
-    // CTA barrier inside the step, so loads, dot chains and stores of
-    // different warps overlap.
+    // CTA barrier inside the step. (A TMA bulk-copy variant with double
+    // buffering measured 1.9x slower here: the per-column segments are only
+    // 2 KB and the buffer turnaround serialises.)
     {
       const int rows = m - k;
       const int pitch = rows | 1;
@@ -351,44 +459,47 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
       const int per_warp = tile_doubles / NW;
       const int cw = max(1, min(32, per_warp / pitch));
       double* Tw = T + warp * per_warp;
-      for (int jt = k + 1 + warp * cw; jt < n; jt += NW * cw) {
-        const int tw = min(cw, n - jt);
-        for (int c = 0; c < tw; ++c) {
-          const double* src = W + int64_t(jt + c) * ldw + k;
-          for (int r = lane; r < rows; r += 32) cp_async8(Tw + c * pitch + r, src + r);
-        }
-        cp_async_wait_all();
-        __syncwarp();
-        if (lane < tw) {
-          double* col = Tw + lane * pitch;
-          if (tau != 0.0) {
-            const double dot = red_h_smem(vsh + k, col, 1, rows);
-            const double sc = -(tau * dot);
-#pragma unroll 8
-            for (int r = 0; r < rows; ++r) col[r] = fma(sc, vsh[k + r], col[r]);
+      for (int b = cr; b * CB < n; b += G) {
+        const int j0 = max(k + 1, b * CB), j1 = min(n, (b + 1) * CB);
+        for (int jt = j0 + warp * cw; jt < j1; jt += NW * cw) {
+          const int tw = min(cw, j1 - jt);
+          for (int c = 0; c < tw; ++c) {
+            const double* src = W + int64_t(jt + c) * ldw + k;
+            for (int r = lane; r < rows; r += 32) cp_async8(Tw + c * pitch + r, src + r);
           }
-          // GCC computes rkj*rkj once (rounded) for the norm and member downdates.
-          const int j = jt + lane;
-          const double rkj = col[0];
-          const double sq = rkj * rkj;
-          double upd = S.cn2[j] - sq;
-          if (upd < 1e-8 * S.cn2o[j])
-            upd = red_p2([&](int r, double& a, double& b) { a = b = col[r]; }, 1, rows - 1);
-          S.cn2[j] = fmax(0.0, upd);
-          S.sq[j] = sq;
+          cp_async_wait_all();
+          __syncwarp();
+          if (lane < tw) {
+            double* col = Tw + lane * pitch;
+            if (tau != 0.0) {
+              const double dot = red_h_smem(vsh + k, col, 1, rows);
+              const double sc = -(tau * dot);
+#pragma unroll 8
+              for (int r = 0; r < rows; ++r) col[r] = fma(sc, vsh[k + r], col[r]);
+            }
+            // GCC computes rkj*rkj once (rounded) for the norm and member downdates.
+            const int j = jt + lane;
+            const double rkj = col[0];
+            const double sq = rkj * rkj;
+            double upd = S.cn2[j] - sq;
+            if (upd < 1e-8 * S.cn2o[j])
+              upd = red_p2([&](int r, double& a, double& b2) { a = b2 = col[r]; }, 1, rows - 1);
+            S.cn2[j] = fmax(0.0, upd);
+            S.sq[j] = sq;
+          }
+          __syncwarp();
+          for (int c = 0; c < tw; ++c) {
+            double* dst = W + int64_t(jt + c) * ldw + k;
+            for (int r = lane; r < rows; r += 32) dst[r] = Tw[c * pitch + r];
+          }
+          __syncwarp();
         }
-        __syncwarp();
-        for (int c = 0; c < tw; ++c) {
-          double* dst = W + int64_t(jt + c) * ldw + k;
-          for (int r = lane; r < rows; r += 32) dst[r] = Tw[c * pitch + r];
-        }
-        __syncwarp();
       }
-      __syncthreads();
     }
+    cluster.sync();
     t_tile += clock64() - t0c; t0c = clock64();
     ++rank;
-    if (members && tid < 32) {
+    if (lead && members && tid < 32) {
       // member_mass[g] -= rkj^2 in column order (linalg.cpp:312-315). Warp 0
       // streams (rkj^2, group) pairs through double-buffered shared staging
       // (cp.async prefetch of chunk i+1 while chunk i is consumed); lane 0
@@ -421,8 +532,8 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
         const double* st_r = st_r0 + buf * CH;
         const int* st_g = st_g0 + buf * CH;
         if (tid == 0) {
-          // Fast path for runs of 8 of one member (the common case: members are
-          // contiguous column ranges).
+          // Fast path for runs of 8 of one member (members are contiguous
+          // column ranges): unclamped chain, clamp checked off the chain.
           int u = 0;
           for (; u + 8 <= cnt; u += 8) {
             int gg[8];
@@ -436,8 +547,6 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
 #pragma unroll
             for (int q = 0; q < 8; ++q) same &= gg[q] == cur;
             if (same) {
-              // Unclamped chain (pure DADD latency); the clamp is a no-op
-              // unless an intermediate goes negative, checked off the chain.
               double t[8];
               double x = val;
 #pragma unroll
@@ -485,9 +594,19 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
         S.cn2[k] = 0.0;
       }
     }
-    __syncthreads();
+    if (lead) {
+      __syncthreads();
+      int not_done = 0;
+      if (members)
+        for (int g = tid; g < nmem; g += NT) not_done |= (mmsh[g] > S.mt[g]);
+      not_done = __syncthreads_or(not_done);
+      if (tid == 0) slot.flag = not_done;
+    }
     t_mem += clock64() - t0c;
   }
+  // No CTA may leave while others can still read its slots.
+  cluster.sync();
+  if (!lead) return;
   if (tid == 0 && job.dbg) {
     job.dbg[0] = double(t_piv); job.dbg[1] = double(t_refl); job.dbg[2] = double(t_tile);
     job.dbg[3] = double(t_mem); job.dbg[4] = double(rank); job.dbg[5] = double(n);
@@ -499,10 +618,10 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
   for (int64_t e = tid; e < int64_t(m) * m; e += NT) Q[e] = (e / m == e % m) ? 1.0 : 0.0;
   __syncthreads();
   for (int k = rank - 1; k >= 0; --k) {
-    const double tau = S.tau[k];
+    const double tau = __ldcg(&S.tau[k]);
     if (tau == 0.0) continue;
     const double* vk = S.V + int64_t(k) * m;
-    for (int i = tid; i < m; i += NT) vsh[i] = vk[i];
+    for (int i = tid; i < m; i += NT) vsh[i] = __ldcg(&vk[i]);
     __syncthreads();
     for (int j = tid; j < m; j += NT) {
       const double dot = red_h(
@@ -523,7 +642,8 @@ size_t qr_scratch_doubles(int m, int n, int nmem) {
   return 4 * size_t(n) + 2 * size_t(nmem) + kmax0 + size_t(m) * kmax0 + 8;
 }
 
-void launch_qr(const QrJob* jobs, int njobs, int max_m, int max_nmem, cudaStream_t st) {
+void launch_qr(const QrJob* jobs, int njobs, int max_m, int max_nmem, int cluster,
+               cudaStream_t st) {
   if (njobs <= 0) return;
   static bool attr = false;
   if (!attr) {
@@ -533,12 +653,34 @@ void launch_qr(const QrJob* jobs, int njobs, int max_m, int max_nmem, cudaStream
   // Two CTAs per SM (~100 KB of shared memory each, most of it the tile) so
   // one CTA's load/compute/store phases overlap the other's.
   const size_t budget = 100 * 1024;
-  const size_t fixed = sizeof(double) * size_t(max_m + max_nmem);
+  const size_t fixed = sizeof(double) * size_t((max_m + max_nmem + 1) & ~1);
   size_t tile = budget > fixed + 8192 ? (budget - fixed) / sizeof(double) : 1024;
-  if (tile < size_t(max_m | 1)) tile = size_t(max_m | 1);  // at least one column
+  // Every warp needs two buffers of at least one (even-padded) column.
+  const size_t min_tile = size_t(NT / 32) * 2 * size_t((max_m + 2) & ~1);
+  if (tile < min_tile) tile = min_tile;
   if (tile < 1536) tile = 1536;                             // member staging (2 x 512)
   const size_t smem = fixed + tile * sizeof(double);
-  qr_kernel<<<njobs, NT, smem, st>>>(jobs, int(tile), max_nmem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(njobs * cluster));
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = unsigned(cluster);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, qr_kernel, jobs, int(tile), max_nmem);
+}
+
+int qr_cluster_size(int njobs, int min_n) {
+  // Aim for ~2 CTAs per SM over 148 SMs; split a basis only when its panel is
+  // wide enough to give every CTA whole column blocks.
+  int g = 1;
+  while (g < 8 && njobs * g * 2 <= 296 && min_n >= 4 * CB * g) g *= 2;
+  return g;
 }
 
 }  // namespace h2g

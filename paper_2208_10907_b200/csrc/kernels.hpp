@@ -37,8 +37,10 @@ struct GemmJob {
 struct GemmTile {
   int job, tm, tn;
 };
+// tm indexes BM-row tiles; BM = gemm_tile_rows(max C rows in the batch).
+int gemm_tile_rows(int max_rows);
 void launch_gemm(const GemmJob* jobs, const GemmSeg* segs, const GemmTile* tiles, int ntiles,
-                 KernelParams kp, Cloud cloud, ErrWord* err, int tag, cudaStream_t st);
+                 int bm, KernelParams kp, Cloud cloud, ErrWord* err, int tag, cudaStream_t st);
 
 // ---- batched kernel-block evaluation (k_eval.cu) ---------------------------
 // out(i, j) = K(x[rb + i], x[cb + j]) (assemble_block, kernels.cpp:242-268).
@@ -123,6 +125,21 @@ void launch_solve(const SolveJob* jobs, const SolveChunk* chunks, int nchunks,
                   size_t smem_doubles, cudaStream_t st);
 int solve_chunk_width(int m);
 
+// Blocked left solves: one diagonal block [kb, kb + nb) (nb <= 32) for all
+// RHS columns; tiles = (job, 128-column group).
+struct TrsmBlockJob {
+  Mat lu, X;
+  int kb, nb;
+  int lower;
+};
+void launch_trsm_block(const TrsmBlockJob* jobs, const int2* tiles, int ntiles, cudaStream_t st);
+// dst(i, :) = src(perm[i], :); tiles = (job, 4096-element chunk).
+struct GatherJob {
+  Mat dst, src;
+  const int64_t* perm;
+};
+void launch_gather_rows(const GatherJob* jobs, const int2* tiles, int ntiles, cudaStream_t st);
+
 // ---- batched column-pivoted Householder QR with member stopping (k_qr.cu)
 // run_pivoted_qr + form_q (linalg.cpp:137-185, :216-332) as used by
 // basis_from_members (compression.cpp:111-146).
@@ -140,7 +157,10 @@ struct QrJob {
   int* rank_out;
   double* dbg = nullptr;  // optional per-job phase cycle counters (profiling)
 };
-void launch_qr(const QrJob* jobs, int njobs, int max_m, int max_nmem, cudaStream_t st);
+void launch_qr(const QrJob* jobs, int njobs, int max_m, int max_nmem, int cluster,
+               cudaStream_t st);
+// CTAs per basis (thread-block cluster size) for a batch of njobs bases.
+int qr_cluster_size(int njobs, int min_n);
 size_t qr_scratch_doubles(int m, int n, int nmem);
 
 }  // namespace h2g
