@@ -82,11 +82,13 @@ __device__ __forceinline__ double red_p2(G get, int i0, int tc) {
 struct Scratch {
   double* cn2;
   double* cn2o;
-  double* sq;
-  int* piv;
-  int* mof;
+  double* sq;  // rkj^2 of the current step, by position
+  int* piv;   // position -> original column
+  int* grp;   // original column -> member (static)
   double* mm;
   double* mt;
+  double* pn2;  // pivot column's norm^2 at each step (after the swap)
+  int* swp;     // pivot position selected at each step
   double* V;
   double* tau;
 };
@@ -97,11 +99,13 @@ __host__ __device__ inline Scratch carve(double* s, int m, int n, int nmem) {
   c.cn2 = s;
   c.cn2o = s + n;
   c.piv = reinterpret_cast<int*>(s + 2 * int64_t(n));
-  c.mof = c.piv + n;
+  c.grp = c.piv + n;
   c.sq = s + 3 * int64_t(n);
   c.mm = s + 4 * int64_t(n);
   c.mt = c.mm + nmem;
-  c.tau = c.mt + nmem;
+  c.pn2 = c.mt + nmem;
+  c.swp = reinterpret_cast<int*>(c.pn2 + kmax0);  // [0, kmax0): list D, [kmax0, 2 kmax0): pivots
+  c.tau = c.pn2 + 2 * int64_t(kmax0);
   c.V = c.tau + kmax0;
   return c;
 }
@@ -254,10 +258,43 @@ __device__ __forceinline__ void store_tile(const double* T, int pitch, double* W
 // (barrier.cluster release/acquire).
 constexpr int CB = NT;
 
+// Member-mass downdates of one step (linalg.cpp:312-321), lead CTA. Members
+// are contiguous ranges of original columns, and position j initially holds
+// column j; only pivot swaps displace columns, so the positions (> s) where
+// a column of another member sits form a short sorted list D. Each thread
+// owns whole members and runs each member's ordered chain over its range
+// (skipping D) merged with its own displaced columns — every member's chain
+// sees the reference's position order, members run in parallel.
+__device__ void member_step(const Scratch& S, int s, int nmem, const int64_t* off,
+                            const int* D, int nd, double* mmsh) {
+  for (int g = threadIdx.x; g < nmem; g += NT) {
+    const int a = max(s + 1, int(off[g])), b = int(off[g + 1]);
+    double val = mmsh[g];
+    auto step = [&](int j) {
+      const double v = val - S.sq[j];
+      val = v < 0.0 ? 0.0 : v;
+    };
+    int p = 0;
+    for (; p < nd && D[p] < a; ++p)
+      if (S.grp[S.piv[D[p]]] == g) step(D[p]);
+    for (int j = a; j < b; ++j) {
+      if (p < nd && D[p] == j) {
+        ++p;
+        continue;
+      }
+      step(j);
+    }
+    for (; p < nd; ++p)
+      if (D[p] >= b && S.grp[S.piv[D[p]]] == g) step(D[p]);
+    mmsh[g] = val;
+  }
+}
+
 struct ClSlots {
   double d;
   int piv, pos;
   int flag;
+  int nd;
 };
 
 // Dynamic shared memory: [ v (m) | member masses (nmem) | column tile ].
@@ -329,7 +366,7 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
       for (int g = tid; g < nmem; g += NT) {
         double mass = 0.0;
         for (int64_t j = job.member_off[g]; j < job.member_off[g + 1]; ++j) {
-          S.mof[j] = g;
+          S.grp[j] = g;
           mass += S.cn2[j];
         }
         mmsh[g] = mass;
@@ -346,6 +383,7 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
 
   double r11 = -1.0;
   int rank = 0;
+  int nd = 0;  // length of the displaced-position list D
   long long t_piv = 0, t_refl = 0, t_tile = 0, t_mem = 0, t0c;
   for (int k = 0; k < kmax; ++k) {
     t0c = clock64();
@@ -399,16 +437,19 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
         double t = S.cn2[k]; S.cn2[k] = S.cn2[sel]; S.cn2[sel] = t;
         t = S.cn2o[k]; S.cn2o[k] = S.cn2o[sel]; S.cn2o[sel] = t;
         int ti = S.piv[k]; S.piv[k] = S.piv[sel]; S.piv[sel] = ti;
-        if (members) { ti = S.mof[k]; S.mof[k] = S.mof[sel]; S.mof[sel] = ti; }
       }
+    }
+    if (lead && tid == 0) {
+      S.swp[kmax0 + k] = sel;
+      S.pn2[k] = S.cn2[k];
     }
     cluster.sync();
     const double pivot_norm = sqrt(fmax(0.0, __ldcg(&S.cn2[k])));
     if (k == 0) r11 = pivot_norm;
     const bool diag_done = pivot_norm <= job.tol * r11;
-    const bool members_done = !members_not_done;
     const bool floor_hit = pivot_norm <= 1e-15 * r11;
-    if ((diag_done && members_done) || floor_hit) break;
+    if (floor_hit) break;
+    if (diag_done && !members_not_done) break;
 
     t_piv += clock64() - t0c; t0c = clock64();
     // make_reflector (linalg.cpp:152-178), sequential on one thread of CTA 0.
@@ -469,14 +510,20 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
           }
           cp_async_wait_all();
           __syncwarp();
+          if (tau != 0.0) {
+            // Sequential dot chain: one lane per column. The rank-1 update is
+            // element-wise, so the whole warp applies it column by column.
+            double sc = 0.0;
+            if (lane < tw) sc = -(tau * red_h_smem(vsh + k, Tw + lane * pitch, 1, rows));
+            for (int c = 0; c < tw; ++c) {
+              const double s_c = __shfl_sync(0xffffffffu, sc, c);
+              double* colc = Tw + c * pitch;
+              for (int r = lane; r < rows; r += 32) colc[r] = fma(s_c, vsh[k + r], colc[r]);
+            }
+            __syncwarp();
+          }
           if (lane < tw) {
             double* col = Tw + lane * pitch;
-            if (tau != 0.0) {
-              const double dot = red_h_smem(vsh + k, col, 1, rows);
-              const double sc = -(tau * dot);
-#pragma unroll 8
-              for (int r = 0; r < rows; ++r) col[r] = fma(sc, vsh[k + r], col[r]);
-            }
             // GCC computes rkj*rkj once (rounded) for the norm and member downdates.
             const int j = jt + lane;
             const double rkj = col[0];
@@ -499,106 +546,38 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
     cluster.sync();
     t_tile += clock64() - t0c; t0c = clock64();
     ++rank;
-    if (lead && members && tid < 32) {
-      // member_mass[g] -= rkj^2 in column order (linalg.cpp:312-315). Warp 0
-      // streams (rkj^2, group) pairs through double-buffered shared staging
-      // (cp.async prefetch of chunk i+1 while chunk i is consumed); lane 0
-      // runs the ordered chain with the running group value in a register.
-      constexpr int CH = 512;
-      double* st_r0 = T;
-      int* st_g0 = reinterpret_cast<int*>(T + 2 * CH);
-      int cur = -1;
-      double val = 0.0;
-      auto stage = [&](int j0, int b) {
-        const int cnt = min(CH, n - j0);
-        for (int u = tid; u < cnt; u += 32) {
-          cp_async8(st_r0 + b * CH + u, S.sq + j0 + u);
-          const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(st_g0 + b * CH + u));
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(S.mof + j0 + u));
-        }
-        asm volatile("cp.async.commit_group;\n" ::);
-      };
-      int buf = 0;
-      if (k + 1 < n) stage(k + 1, 0);
-      for (int j0 = k + 1; j0 < n; j0 += CH, buf ^= 1) {
-        const int cnt = min(CH, n - j0);
-        if (j0 + CH < n) {
-          stage(j0 + CH, buf ^ 1);
-          asm volatile("cp.async.wait_group 1;\n" ::);
-        } else {
-          asm volatile("cp.async.wait_group 0;\n" ::);
-        }
-        __syncwarp();
-        const double* st_r = st_r0 + buf * CH;
-        const int* st_g = st_g0 + buf * CH;
-        if (tid == 0) {
-          // Fast path for runs of 8 of one member (members are contiguous
-          // column ranges): unclamped chain, clamp checked off the chain.
-          int u = 0;
-          for (; u + 8 <= cnt; u += 8) {
-            int gg[8];
-            double ss[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              gg[q] = st_g[u + q];
-              ss[q] = st_r[u + q];
-            }
-            bool same = true;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) same &= gg[q] == cur;
-            if (same) {
-              double t[8];
-              double x = val;
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                x = x - ss[q];
-                t[q] = x;
-              }
-              bool neg = false;
-#pragma unroll
-              for (int q = 0; q < 8; ++q) neg |= t[q] < 0.0;
-              if (!neg) {
-                val = x;
-                continue;
-              }
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              if (gg[q] != cur) {
-                if (cur >= 0) mmsh[cur] = val;
-                cur = gg[q];
-                val = mmsh[cur];
-              }
-              const double v = val - ss[q];
-              val = v < 0.0 ? 0.0 : v;
-            }
-          }
-          for (; u < cnt; ++u) {
-            const int g = st_g[u];
-            if (g != cur) {
-              if (cur >= 0) mmsh[cur] = val;
-              cur = g;
-              val = mmsh[g];
-            }
-            const double v = val - st_r[u];
-            val = v < 0.0 ? 0.0 : v;
-          }
-        }
-        __syncwarp();
-      }
+    if (lead && members) {
+      // D: positions > k holding a column of another member (sorted). The
+      // swap of step k moved the column from position k to position sel.
+      int* D = S.swp;
       if (tid == 0) {
-        if (cur >= 0) mmsh[cur] = val;
-        const int gk = S.mof[k];
-        const double v = mmsh[gk] - S.cn2[k];
-        mmsh[gk] = v < 0.0 ? 0.0 : v;
-        S.cn2[k] = 0.0;
+        const int sel = S.swp[kmax0 + k];
+        int w = 0;
+        for (int q = 0; q < nd; ++q)
+          if (D[q] > k && D[q] != sel) D[w++] = D[q];
+        if (sel > k && S.grp[S.piv[sel]] != S.grp[sel]) {
+          int q = w;
+          while (q > 0 && D[q - 1] > sel) {
+            D[q] = D[q - 1];
+            --q;
+          }
+          D[q] = sel;
+          ++w;
+        }
+        slot.nd = w;
       }
-    }
-    if (lead) {
+      __syncthreads();
+      nd = slot.nd;
+      member_step(S, k, nmem, job.member_off, D, nd, mmsh);
+      __syncthreads();
+      if (tid == 0) {
+        const int gk = S.grp[S.piv[k]];
+        const double v = mmsh[gk] - S.pn2[k];
+        mmsh[gk] = v < 0.0 ? 0.0 : v;
+      }
       __syncthreads();
       int not_done = 0;
-      if (members)
-        for (int g = tid; g < nmem; g += NT) not_done |= (mmsh[g] > S.mt[g]);
+      for (int g = tid; g < nmem; g += NT) not_done |= (mmsh[g] > S.mt[g]);
       not_done = __syncthreads_or(not_done);
       if (tid == 0) slot.flag = not_done;
     }
@@ -639,7 +618,7 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
 
 size_t qr_scratch_doubles(int m, int n, int nmem) {
   const size_t kmax0 = size_t(m < n ? m : n);
-  return 4 * size_t(n) + 2 * size_t(nmem) + kmax0 + size_t(m) * kmax0 + 8;
+  return 4 * size_t(n) + 2 * size_t(nmem) + 3 * kmax0 + size_t(m) * kmax0 + 8;
 }
 
 void launch_qr(const QrJob* jobs, int njobs, int max_m, int max_nmem, int cluster,
