@@ -494,27 +494,29 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
     Slab kdbg;
     double* ddbg = nullptr;
     if (getenv("H2G_QR_DEBUG")) {
-      kdbg = c.alloc(sizeof(double) * 8 * jobs.size());
+      kdbg = c.alloc(sizeof(double) * 16 * jobs.size());
       ddbg = static_cast<double*>(kdbg.get());
-      cudaMemsetAsync(ddbg, 0, sizeof(double) * 8 * jobs.size(), c.stream);
-      for (size_t q = 0; q < jobs.size(); ++q) jobs[q].dbg = ddbg + 8 * q;
+      cudaMemsetAsync(ddbg, 0, sizeof(double) * 16 * jobs.size(), c.stream);
+      for (size_t q = 0; q < jobs.size(); ++q) jobs[q].dbg = ddbg + 16 * q;
     }
     Slab kj;
     auto* dj = upload(c, jobs, kj);
     auto ev = c.prof_begin();
     const int cl = getenv("H2G_QR_CLUSTER") ? atoi(getenv("H2G_QR_CLUSTER"))
-                                            : qr_cluster_size(int(jobs.size()), min_n);
+                                            : qr_cluster_size(int(jobs.size()), min_n, max_m, max_nmem);
     launch_qr(dj, int(jobs.size()), max_m, max_nmem, cl, c.stream);
     if (ddbg) {
-      std::vector<double> h(8 * jobs.size());
+      std::vector<double> h(16 * jobs.size());
       cudaMemcpyAsync(h.data(), ddbg, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c.stream);
       cudaStreamSynchronize(c.stream);
-      double a[7] = {0};
+      double a[12] = {0};
       for (size_t q = 0; q < jobs.size(); ++q)
-        for (int u = 0; u < 7; ++u) a[u] += h[8 * q + u];
+        for (int u = 0; u < 12; ++u) a[u] += h[16 * q + u];
       fprintf(stderr, "QRDBG jobs=%zu avg: piv %.3g refl %.3g tile %.3g mem %.3g rank %.1f n %.0f formq %.3g (cycles)\n",
               jobs.size(), a[0] / jobs.size(), a[1] / jobs.size(), a[2] / jobs.size(), a[3] / jobs.size(),
               a[4] / jobs.size(), a[5] / jobs.size(), a[6] / jobs.size());
+      fprintf(stderr, "QRDBG   warp0 per tile: wait %.0f chain %.0f store %.0f tiles %.0f\n",
+              a[8] / a[11], a[9] / a[11], a[10] / a[11], a[11] / jobs.size());
     }
     c.prof_end("qr", ev, 0.0, 0.0);
     qr_recs.push_back({c.prof ? c.prec.size() - 1 : size_t(-1), t0, t1});

@@ -2,12 +2,12 @@
 // followed by full Q formation: run_pivoted_qr + form_q (linalg.cpp:137-185,
 // :216-332) as driven by basis_from_members (compression.cpp:111-146).
 //
-// One CTA per basis. The working copy R is row-major so that the
-// thread-per-column reflector application (each column's dot product and
-// update run sequentially over rows, exactly as the reference) reads and
-// writes coalesced rows. Column norms, downdates, the 4e-15 tie rule, the
-// member masses and the stopping tests all follow the reference's operation
-// order, so ranks and Q are bitwise equal to the reference's.
+// One thread-block cluster per basis; the working copy R is column-major in
+// HBM and streamed through shared memory once per Householder step. Each
+// column's reflector dot product runs sequentially over rows in one lane,
+// exactly as the reference; column norms, downdates, the 4e-15 tie rule,
+// the member masses and the stopping tests all follow the reference's
+// operation order, so ranks and Q are bitwise equal to the reference's.
 #include <cooperative_groups.h>
 
 #include "kernels.hpp"
@@ -16,9 +16,11 @@ namespace cg = cooperative_groups;
 
 namespace h2g {
 
+void cuda_check(cudaError_t e, const char* what);  // batch.cu
+
 namespace {
 
-constexpr int NT = 256;
+constexpr int NT = 128;
 
 // The reference's reductions as GCC -O3 -mavx2 -mfma compiles them
 // (linalg.cpp; disassembly of oracle/_ref, verified bit-exact on random
@@ -146,146 +148,126 @@ __device__ int block_min_int(int v, int* red) {
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void st_global16(double* p, double x, double y) {
+  asm volatile("st.global.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(x), "d"(y) : "memory");
 }
 
-// red_h over a shared-memory column (stride ld) with 8-deep load prefetch:
-// the dependent add chain then runs at FP64 latency, not LDS latency.
-__device__ __forceinline__ double red_h_smem(const double* __restrict__ v,
-                                             const double* __restrict__ col, int ld, int tc) {
+// red_h (above) over a shared-memory column against v, streamed as 16-byte
+// pairs: element t is col[off + t] * vb[off + t], t < tc, with col and vb
+// 16-byte aligned and off in {0, 1}. Every element is a rounded product
+// added in order except an odd last one, which is fused.
+__device__ __forceinline__ double dot_h_pairs(const double* __restrict__ col,
+                                              const double* __restrict__ vb, int off, int tc) {
   double s = 0.0;
-  const int v4 = tc & ~3;
-  int i = 0;
-  for (; i + 8 <= v4; i += 8) {
-    double p[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) p[u] = v[i + u] * col[(i + u) * ld];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) s = s + p[u];
+  if (tc <= 0) return s;
+  const bool lastf = tc & 1;
+  const int nu = lastf ? tc - 1 : tc;
+  int t = 0;
+  if (off == 1 && nu >= 1) {
+    s = s + col[1] * vb[1];
+    t = 1;
   }
-  for (; i < v4; ++i) s = s + v[i] * col[i * ld];
-  if ((tc & 3) >= 2) {
-    s = s + v[i] * col[i * ld];
-    s = s + v[i + 1] * col[(i + 1) * ld];
-    i += 2;
+  const double2* c2 = reinterpret_cast<const double2*>(col + off + t);
+  const double2* v2 = reinterpret_cast<const double2*>(vb + off + t);
+  const int npair = (nu - t) >> 1;
+  int q = 0;
+  for (; q + 4 <= npair; q += 4) {
+    double2 x[4], y[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      x[w] = c2[q + w];
+      y[w] = v2[q + w];
+    }
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      s = s + x[w].x * y[w].x;
+      s = s + x[w].y * y[w].y;
+    }
   }
-  if (tc & 1) s = fma(v[i], col[i * ld], s);
+  for (; q < npair; ++q) {
+    const double2 x = c2[q], y = v2[q];
+    s = s + x.x * y.x;
+    s = s + x.y * y.y;
+  }
+  t += 2 * npair;
+  if (t < nu) {
+    s = s + col[off + t] * vb[off + t];
+    ++t;
+  }
+  if (lastf) s = fma(col[off + t], vb[off + t], s);
   return s;
-}
-
-__device__ __forceinline__ unsigned smem_addr(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)),
-               "r"(bytes));
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n.reg .pred p;\nWAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(bar)),
-      "r"(parity));
-}
-// TMA bulk copies (UBLKCP): global -> shared completing on an mbarrier, and
-// shared -> global in a bulk group.
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
-               "r"(smem_addr(src)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() {
-  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
 }
 
-// Column-major panel W (element (i, j) at W[j * ldw + i]): a tile of
-// whole column segments [k, m) is one contiguous HBM range, loaded with
-// cp.async into shared memory at an odd pitch (conflict-free per-thread
-// column walks), updated there, and written back: one read + one write of
-// the trailing panel per Householder step.
-// Warp w copies columns w, w + NT/32, ...; lanes walk the contiguous
-// segment (no per-element index division).
-__device__ __forceinline__ void load_tile(double* T, int pitch, const double* W, int64_t ldw,
-                                          int k, int rows, int jt, int tw) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int c = warp; c < tw; c += NT / 32) {
-    const double* src = W + int64_t(jt + c) * ldw + k;
-    double* dst = T + c * pitch;
-    for (int r = lane; r < rows; r += 32) cp_async8(dst + r, src + r);
+// Column ownership inside a cluster: blocks of CB consecutive positions go
+// round-robin to the G CTAs (owner = (j / CB) % G). A CTA walks its own
+// positions through a dense local index li.
+constexpr int CB = 256;
+struct Own {
+  int G, cr;
+  __device__ __forceinline__ int l2g(int li) const {
+    return ((li / CB) * G + cr) * CB + li % CB;
   }
-  cp_async_wait_all();
-}
-
-__device__ __forceinline__ void store_tile(const double* T, int pitch, double* W, int64_t ldw,
-                                           int k, int rows, int jt, int tw) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int c = warp; c < tw; c += NT / 32) {
-    double* dst = W + int64_t(jt + c) * ldw + k;
-    const double* src = T + c * pitch;
-    for (int r = lane; r < rows; r += 32) dst[r] = src[r];
+  // Number of own positions < x.
+  __device__ __forceinline__ int below(int x) const {
+    const int bx = x / CB;
+    int c = bx > cr ? ((bx - cr + G - 1) / G) * CB : 0;
+    if (bx % G == cr) c += x % CB;
+    return c;
   }
-}
-
-// Cluster-split QR: the G CTAs of a thread-block cluster share one basis;
-// column blocks of CB columns are owned round-robin (owner = (j / CB) % G).
-// Per Householder step: cluster-wide pivot reductions through distributed
-// shared memory, the swap and the reflector by CTA 0, every CTA sweeps its own
-// columns, CTA 0 runs the ordered member-mass chain. Global data written by
-// one CTA is read by the others only across cluster barriers
-// (barrier.cluster release/acquire).
-constexpr int CB = NT;
+};
 
 // Member-mass downdates of one step (linalg.cpp:312-321), lead CTA. Members
-// are contiguous ranges of original columns, and position j initially holds
+// are contiguous ranges of original columns and position j initially holds
 // column j; only pivot swaps displace columns, so the positions (> s) where
-// a column of another member sits form a short sorted list D. Each thread
-// owns whole members and runs each member's ordered chain over its range
-// (skipping D) merged with its own displaced columns — every member's chain
-// sees the reference's position order, members run in parallel.
-__device__ void member_step(const Scratch& S, int s, int nmem, const int64_t* off,
-                            const int* D, int nd, double* mmsh) {
+// a column of another member sits form a short sorted list D (positions Dp,
+// their columns' members Dg, both in shared memory). Each thread owns whole
+// members and runs each member's chain over its range (skipping D) merged
+// with its displaced columns, i.e. in the reference's position order; the
+// range's rkj^2 are fetched eight at a time ahead of the dependent chain.
+__device__ __forceinline__ double mass_sub(double val, double x) {
+  const double v = val - x;
+  return v < 0.0 ? 0.0 : v;
+}
+__device__ void member_step(const double* __restrict__ sq, int s, int nmem, const int64_t* off,
+                            const int* Dp, const int* Dg, int nd, double* mmsh) {
   for (int g = threadIdx.x; g < nmem; g += NT) {
     const int a = max(s + 1, int(off[g])), b = int(off[g + 1]);
     double val = mmsh[g];
-    auto step = [&](int j) {
-      const double v = val - S.sq[j];
-      val = v < 0.0 ? 0.0 : v;
-    };
     int p = 0;
-    for (; p < nd && D[p] < a; ++p)
-      if (S.grp[S.piv[D[p]]] == g) step(D[p]);
-    for (int j = a; j < b; ++j) {
-      if (p < nd && D[p] == j) {
-        ++p;
-        continue;
+    for (; p < nd && Dp[p] < a; ++p)
+      if (Dg[p] == g) val = mass_sub(val, __ldcg(&sq[Dp[p]]));
+    int nextd = p < nd ? Dp[p] : 0x7fffffff;
+    for (int j0 = a; j0 < b; j0 += 8) {
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = j0 + u < b ? __ldcg(&sq[j0 + u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + u;
+        if (j < b) {
+          if (j == nextd) {
+            ++p;
+            nextd = p < nd ? Dp[p] : 0x7fffffff;
+          } else {
+            val = mass_sub(val, x[u]);
+          }
+        }
       }
-      step(j);
     }
     for (; p < nd; ++p)
-      if (D[p] >= b && S.grp[S.piv[D[p]]] == g) step(D[p]);
+      if (Dp[p] >= b && Dg[p] == g) val = mass_sub(val, __ldcg(&sq[Dp[p]]));
     mmsh[g] = val;
   }
 }
@@ -294,69 +276,82 @@ struct ClSlots {
   double d;
   int piv, pos;
   int flag;
-  int nd;
 };
 
-// Dynamic shared memory: [ v (m) | member masses (nmem) | column tile ].
-__global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ jobs, int tile_doubles,
-                                                   int nmem_cap) {
-  extern __shared__ double dsm[];
+// Cluster-split QR: the G CTAs of a thread-block cluster share one basis.
+// Per Householder step: cluster-wide pivot reductions through distributed
+// shared memory, the swap and the reflector by CTA 0, every CTA sweeps its
+// own columns, CTA 0 runs the member-mass chains. Global data written by one
+// CTA is read by the others only across cluster barriers (barrier.cluster
+// release/acquire).
+//
+// Column sweep: each warp streams tiles of up to 32 columns through its own
+// slice of shared memory. Lane c runs column c's sequential dot chain (the
+// reference's rounding order), the whole warp then writes the updated
+// column straight from the FMA to global memory and refills the slot with
+// the next tile's column (cp.async), so loads overlap the stores.
+//
+// Dynamic shared memory: [ v (m) | member masses (nmem) | D (2 kmax ints) | column tiles ].
+__global__ void __launch_bounds__(NT, 1) qr_kernel(const QrJob* __restrict__ jobs, int tile_doubles,
+                                                   int nmem_cap, int m_cap) {
+  extern __shared__ __align__(16) double dsm[];
   __shared__ double redd[32];
   __shared__ int redi[32];
   __shared__ double sh_tau;
+  __shared__ int sh_nd;
   __shared__ ClSlots slot;
-  __shared__ __align__(8) uint64_t mbar[NT / 32][2];
-  __shared__ unsigned mpar[NT / 32][2];
   cg::cluster_group cluster = cg::this_cluster();
   const int G = int(cluster.num_blocks());
   const int cr = int(cluster.block_rank());
+  const Own own{G, cr};
   const QrJob job = jobs[blockIdx.x / G];
   const int m = job.m, n = job.n, nmem = job.nmem;
   double* W = job.work;
   const int64_t ldw = job.ldw;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int NW = NT / 32;
+  const int vcap = (m_cap + 3) & ~1;  // v, plus one pad row for pair reads
   double* vsh = dsm;
-  double* mmsh = dsm + m;
-  double* T = dsm + ((m + nmem_cap + 1) & ~1);  // 16-byte aligned tile
+  double* mmsh = dsm + vcap;
+  int* Dp = reinterpret_cast<int*>(mmsh + nmem_cap);
+  int* Dg = Dp + m_cap;
+  double* T = dsm + ((vcap + m_cap + nmem_cap + 1) & ~1);  // 16-byte aligned tiles
   Scratch S = carve(job.scratch, m, n, nmem);
   const int kmax0 = m < n ? m : n;
   int kmax = kmax0;
   if (job.cap > 0 && job.cap < kmax) kmax = job.cap;
   const bool lead = cr == 0;
-  if (tid < NT / 32) {
-    mbar_init(&mbar[tid][0], 1);
-    mbar_init(&mbar[tid][1], 1);
-    mpar[tid][0] = mpar[tid][1] = 0;
-  }
-  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  __syncthreads();
+  const int nloc = own.below(n);
 
   // R = A (skipped when factoring in place): own columns.
   if (!(job.A.p == W && job.A.rs == 1 && job.A.cs == ldw)) {
-    for (int b = cr; b * CB < n; b += G)
-      for (int j = b * CB; j < min(n, (b + 1) * CB); ++j)
-        for (int i = tid; i < m; i += NT) W[int64_t(j) * ldw + i] = job.A.at(i, j);
+    for (int li = 0; li < nloc; ++li) {
+      const int j = own.l2g(li);
+      for (int i = tid; i < m; i += NT) W[int64_t(j) * ldw + i] = job.A.at(i, j);
+    }
     __syncthreads();
   }
   // Column norms of own columns (pattern P2 over all rows), tile by tile.
   {
     const int pitch = m | 1;
     const int twmax = max(1, min(NT, tile_doubles / pitch));
-    for (int b = cr; b * CB < n; b += G) {
-      const int j1 = min(n, (b + 1) * CB);
-      for (int jt = b * CB; jt < j1; jt += twmax) {
-        const int tw = min(twmax, j1 - jt);
-        load_tile(T, pitch, W, ldw, 0, m, jt, tw);
-        __syncthreads();
-        if (tid < tw) {
-          const double* col = T + tid * pitch;
-          const double s = red_p2([&](int i, double& a, double& b2) { a = b2 = col[i]; }, 0, m);
-          S.cn2[jt + tid] = s;
-          S.cn2o[jt + tid] = s;
-          S.piv[jt + tid] = jt + tid;
-        }
-        __syncthreads();
+    for (int l0 = 0; l0 < nloc; l0 += twmax) {
+      const int tw = min(twmax, nloc - l0);
+      for (int c = warp; c < tw; c += NW) {
+        const double* src = W + int64_t(own.l2g(l0 + c)) * ldw;
+        for (int r = lane; r < m; r += 32) cp_async8(T + c * pitch + r, src + r);
       }
+      cp_async_wait_all();
+      __syncthreads();
+      if (tid < tw) {
+        const int j = own.l2g(l0 + tid);
+        const double* col = T + tid * pitch;
+        const double s = red_p2([&](int i, double& a, double& b) { a = b = col[i]; }, 0, m);
+        S.cn2[j] = s;
+        S.cn2o[j] = s;
+        S.piv[j] = j;
+      }
+      __syncthreads();
     }
   }
   cluster.sync();
@@ -383,17 +378,16 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
 
   double r11 = -1.0;
   int rank = 0;
-  int nd = 0;  // length of the displaced-position list D
+  int nd = 0;  // length of the displaced-position list D (lead CTA)
   long long t_piv = 0, t_refl = 0, t_tile = 0, t_mem = 0, t0c;
+  long long t_w = 0, t_c = 0, t_s = 0, n_t = 0;
   for (int k = 0; k < kmax; ++k) {
     t0c = clock64();
     // Pivot: cluster-wide max of the remaining norms, then the lowest
     // original index within the 4e-15 tie band (linalg.cpp:263-274).
+    const int lk = own.below(k);
     double mx = -1.0;
-    for (int b = cr; b * CB < n; b += G) {
-      const int j = max(k, b * CB) + tid;
-      if (j < min(n, (b + 1) * CB)) mx = fmax(mx, S.cn2[j]);
-    }
+    for (int li = lk + tid; li < nloc; li += NT) mx = fmax(mx, S.cn2[own.l2g(li)]);
     mx = block_max(mx, redd);
     if (tid == 0) slot.d = mx;
     cluster.sync();
@@ -403,15 +397,15 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
     if (best <= 0.0) break;
     const double tie = best * (1.0 - 4e-15);
     int cand = 0x7fffffff;
-    for (int b = cr; b * CB < n; b += G) {
-      const int j = max(k, b * CB) + tid;
-      if (j < min(n, (b + 1) * CB) && S.cn2[j] >= tie) cand = min(cand, S.piv[j]);
+    for (int li = lk + tid; li < nloc; li += NT) {
+      const int j = own.l2g(li);
+      if (S.cn2[j] >= tie) cand = min(cand, S.piv[j]);
     }
     cand = block_min_int(cand, redi);
     int cpos = 0x7fffffff;
-    for (int b = cr; b * CB < n; b += G) {
-      const int j = max(k, b * CB) + tid;
-      if (j < min(n, (b + 1) * CB) && S.piv[j] == cand && S.cn2[j] >= tie) cpos = j;
+    for (int li = lk + tid; li < nloc; li += NT) {
+      const int j = own.l2g(li);
+      if (S.piv[j] == cand && S.cn2[j] >= tie) cpos = j;
     }
     cpos = block_min_int(cpos, redi);
     if (tid == 0) {
@@ -486,62 +480,113 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
     __syncthreads();
     const double tau = sh_tau;
     t_refl += clock64() - t0c; t0c = clock64();
-    // apply_reflector to own columns k+1.. (linalg.cpp:137-149) + downdate.
-    // Every warp streams its own column tiles through a private slice of the
-    // shared tile (cp.async load -> per-lane column update -> store), with no
-    // CTA barrier inside the step. (A TMA bulk-copy variant with double
-    // buffering measured 1.9x slower here: the per-column segments are only
-    // 2 KB and the buffer turnaround serialises.)
+    // apply_reflector to own columns k+1.. (linalg.cpp:137-149) + norm
+    // downdates (linalg.cpp:300-311). Column segments move as 16-byte pairs
+    // of rows [k0, m), k0 = k rounded down to even (ldw is even, so every
+    // segment is 16-byte aligned); slot pitch P = 2 mod 4 doubles keeps the
+    // per-lane 16-byte shared loads conflict-free.
     {
       const int rows = m - k;
-      const int pitch = rows | 1;
-      const int warp = tid >> 5, lane = tid & 31;
-      constexpr int NW = NT / 32;
-      const int per_warp = tile_doubles / NW;
-      const int cw = max(1, min(32, per_warp / pitch));
+      const int k0 = k & ~1, off = k - k0;
+      const int np = (m - k0 + 1) >> 1;  // pairs per segment
+      const int P = (np & 1) ? 2 * np : 2 * np + 2;
+      const int per_warp = (tile_doubles / NW) & ~1;
+      const int cw = max(1, min(32, per_warp / P));
       double* Tw = T + warp * per_warp;
-      for (int b = cr; b * CB < n; b += G) {
-        const int j0 = max(k + 1, b * CB), j1 = min(n, (b + 1) * CB);
-        for (int jt = j0 + warp * cw; jt < j1; jt += NW * cw) {
-          const int tw = min(cw, j1 - jt);
-          for (int c = 0; c < tw; ++c) {
-            const double* src = W + int64_t(jt + c) * ldw + k;
-            for (int r = lane; r < rows; r += 32) cp_async8(Tw + c * pitch + r, src + r);
-          }
-          cp_async_wait_all();
-          __syncwarp();
-          if (tau != 0.0) {
-            // Sequential dot chain: one lane per column. The rank-1 update is
-            // element-wise, so the whole warp applies it column by column.
-            double sc = 0.0;
-            if (lane < tw) sc = -(tau * red_h_smem(vsh + k, Tw + lane * pitch, 1, rows));
-            for (int c = 0; c < tw; ++c) {
-              const double s_c = __shfl_sync(0xffffffffu, sc, c);
-              double* colc = Tw + c * pitch;
-              for (int r = lane; r < rows; r += 32) colc[r] = fma(s_c, vsh[k + r], colc[r]);
-            }
-            __syncwarp();
-          }
-          if (lane < tw) {
-            double* col = Tw + lane * pitch;
-            // GCC computes rkj*rkj once (rounded) for the norm and member downdates.
-            const int j = jt + lane;
-            const double rkj = col[0];
-            const double sq = rkj * rkj;
-            double upd = S.cn2[j] - sq;
-            if (upd < 1e-8 * S.cn2o[j])
-              upd = red_p2([&](int r, double& a, double& b2) { a = b2 = col[r]; }, 1, rows - 1);
-            S.cn2[j] = fmax(0.0, upd);
-            S.sq[j] = sq;
-          }
-          __syncwarp();
-          for (int c = 0; c < tw; ++c) {
-            double* dst = W + int64_t(jt + c) * ldw + k;
-            for (int r = lane; r < rows; r += 32) dst[r] = Tw[c * pitch + r];
-          }
-          __syncwarp();
-        }
+      // Store pairs start at k1 = (k + 1) rounded down to even: row k (R's
+      // final row k, never read again) may be rewritten with its own value.
+      const int k1 = (k + 1) & ~1;
+      const int nps = (m - k1 + 1) >> 1;
+      const double* vb = vsh + k0;
+      double2 vr[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int p = lane + 32 * u;
+        vr[u] = p < nps ? *reinterpret_cast<const double2*>(vsh + k1 + 2 * p) : make_double2(0.0, 0.0);
       }
+      const int l0 = own.below(k + 1);
+      auto load_col = [&](int slotc, int j) {
+        const double* src = W + int64_t(j) * ldw + k0;
+        double* dst = Tw + slotc * P;
+        if (np <= 128) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int p = lane + 32 * u;
+            if (p < np) cp_async16(dst + 2 * p, src + 2 * p);
+          }
+        } else {
+          for (int p = lane; p < np; p += 32) cp_async16(dst + 2 * p, src + 2 * p);
+        }
+      };
+      int a = l0 + warp * cw;
+      if (a < nloc) {
+        const int tw = min(cw, nloc - a);
+        for (int c = 0; c < tw; ++c) load_col(c, own.l2g(a + c));
+      }
+      for (; a < nloc; a += NW * cw) {
+        const int tw = min(cw, nloc - a);
+        long long c0 = clock64();
+        cp_async_wait_all();
+        __syncwarp();
+        long long c1 = clock64();
+        double sc = 0.0;
+        int jl = 0;
+        if (lane < tw) {
+          jl = own.l2g(a + lane);
+          const double cn2j = S.cn2[jl], cn2oj = S.cn2o[jl];  // in flight during the chain
+          const double* col = Tw + lane * P;
+          if (tau != 0.0) sc = -(tau * dot_h_pairs(col, vb, off, rows));
+          // GCC computes rkj*rkj once (rounded) for the norm and member downdates.
+          const double rkj = tau != 0.0 ? fma(sc, vsh[k], col[off]) : col[off];
+          const double sq = rkj * rkj;
+          double upd = cn2j - sq;
+          if (upd < 1e-8 * cn2oj)
+            upd = red_p2(
+                [&](int r, double& x, double& y) {
+                  x = y = tau != 0.0 ? fma(sc, vsh[k + r], col[off + r]) : col[off + r];
+                },
+                1, rows - 1);
+          S.cn2[jl] = fmax(0.0, upd);
+          S.sq[jl] = sq;
+        }
+        __syncwarp();
+        long long c2 = clock64();
+        const int an = a + NW * cw;
+        const int twn = an < nloc ? min(cw, nloc - an) : 0;
+        for (int c = 0; c < tw; ++c) {
+          const double s_c = __shfl_sync(0xffffffffu, sc, c);
+          const int j = __shfl_sync(0xffffffffu, jl, c);
+          const double* colc = Tw + c * P + (k1 - k0);
+          if (tau != 0.0) {
+            double* dst = W + int64_t(j) * ldw + k1;
+            if (nps <= 128) {
+              double2 x[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int p = lane + 32 * u;
+                x[u] = p < nps ? *reinterpret_cast<const double2*>(colc + 2 * p) : make_double2(0.0, 0.0);
+              }
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int p = lane + 32 * u;
+                if (p < nps)
+                  st_global16(dst + 2 * p, fma(s_c, vr[u].x, x[u].x), fma(s_c, vr[u].y, x[u].y));
+              }
+            } else {
+              for (int p = lane; p < nps; p += 32) {
+                const double2 x = *reinterpret_cast<const double2*>(colc + 2 * p);
+                const double2 v = *reinterpret_cast<const double2*>(vsh + k1 + 2 * p);
+                st_global16(dst + 2 * p, fma(s_c, v.x, x.x), fma(s_c, v.y, x.y));
+              }
+            }
+          }
+          if (c < twn) load_col(c, own.l2g(an + c));
+        }
+        for (int c = tw; c < twn; ++c) load_col(c, own.l2g(an + c));
+        long long c3 = clock64();
+        t_w += c1 - c0; t_c += c2 - c1; t_s += c3 - c2; ++n_t;
+      }
+      cp_async_wait_all();
     }
     cluster.sync();
     t_tile += clock64() - t0c; t0c = clock64();
@@ -549,31 +594,36 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
     if (lead && members) {
       // D: positions > k holding a column of another member (sorted). The
       // swap of step k moved the column from position k to position sel.
-      int* D = S.swp;
       if (tid == 0) {
         const int sel = S.swp[kmax0 + k];
         int w = 0;
         for (int q = 0; q < nd; ++q)
-          if (D[q] > k && D[q] != sel) D[w++] = D[q];
-        if (sel > k && S.grp[S.piv[sel]] != S.grp[sel]) {
+          if (Dp[q] > k && Dp[q] != sel) {
+            Dp[w] = Dp[q];
+            Dg[w] = Dg[q];
+            ++w;
+          }
+        const int gs = S.grp[S.piv[sel]];
+        if (sel > k && gs != S.grp[sel]) {
           int q = w;
-          while (q > 0 && D[q - 1] > sel) {
-            D[q] = D[q - 1];
+          while (q > 0 && Dp[q - 1] > sel) {
+            Dp[q] = Dp[q - 1];
+            Dg[q] = Dg[q - 1];
             --q;
           }
-          D[q] = sel;
+          Dp[q] = sel;
+          Dg[q] = gs;
           ++w;
         }
-        slot.nd = w;
+        sh_nd = w;
       }
       __syncthreads();
-      nd = slot.nd;
-      member_step(S, k, nmem, job.member_off, D, nd, mmsh);
+      nd = sh_nd;
+      member_step(S.sq, k, nmem, job.member_off, Dp, Dg, nd, mmsh);
       __syncthreads();
       if (tid == 0) {
         const int gk = S.grp[S.piv[k]];
-        const double v = mmsh[gk] - S.pn2[k];
-        mmsh[gk] = v < 0.0 ? 0.0 : v;
+        mmsh[gk] = mass_sub(mmsh[gk], S.pn2[k]);
       }
       __syncthreads();
       int not_done = 0;
@@ -589,6 +639,7 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
   if (tid == 0 && job.dbg) {
     job.dbg[0] = double(t_piv); job.dbg[1] = double(t_refl); job.dbg[2] = double(t_tile);
     job.dbg[3] = double(t_mem); job.dbg[4] = double(rank); job.dbg[5] = double(n);
+    job.dbg[8] = double(t_w); job.dbg[9] = double(t_c); job.dbg[10] = double(t_s); job.dbg[11] = double(n_t);
   }
   long long tq = clock64();
 
@@ -614,6 +665,26 @@ __global__ void __launch_bounds__(NT, 2) qr_kernel(const QrJob* __restrict__ job
   if (tid == 0 && job.dbg) job.dbg[6] = double(clock64() - tq);
 }
 
+size_t qr_fixed_doubles(int max_m, int max_nmem) {
+  return size_t((((max_m + 3) & ~1) + max_m + max_nmem + 1) & ~1);
+}
+
+// Dynamic shared memory per CTA: H2G_QR_SMEM_KB (default 110, two CTAs per
+// SM; the column tiles take everything past the fixed part).
+size_t qr_smem_bytes(int max_m, int max_nmem, size_t* tile_doubles) {
+  static const size_t budget = [] {
+    const char* e = getenv("H2G_QR_SMEM_KB");
+    return size_t(std::min(e ? atoi(e) : 110, 220)) * 1024;
+  }();
+  const size_t fixed = qr_fixed_doubles(max_m, max_nmem);
+  size_t tile = budget / sizeof(double) > fixed + 1024 ? budget / sizeof(double) - fixed : 1024;
+  // Every warp needs at least one column slot (pitch <= max_m + 4).
+  const size_t min_tile = size_t(NT / 32) * size_t(max_m + 4);
+  if (tile < min_tile) tile = min_tile;
+  if (tile_doubles) *tile_doubles = tile;
+  return (fixed + tile) * sizeof(double);
+}
+
 }  // namespace
 
 size_t qr_scratch_doubles(int m, int n, int nmem) {
@@ -621,45 +692,79 @@ size_t qr_scratch_doubles(int m, int n, int nmem) {
   return 4 * size_t(n) + 2 * size_t(nmem) + 3 * kmax0 + size_t(m) * kmax0 + 8;
 }
 
-void launch_qr(const QrJob* jobs, int njobs, int max_m, int max_nmem, int cluster,
-               cudaStream_t st) {
-  if (njobs <= 0) return;
+static void qr_attr() {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cuda_check(cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    220 * 1024),
+               "qr smem attribute");
     attr = true;
   }
-  // Two CTAs per SM (~100 KB of shared memory each, most of it the tile) so
-  // one CTA's load/compute/store phases overlap the other's.
-  const size_t budget = 100 * 1024;
-  const size_t fixed = sizeof(double) * size_t((max_m + max_nmem + 1) & ~1);
-  size_t tile = budget > fixed + 8192 ? (budget - fixed) / sizeof(double) : 1024;
-  // Every warp needs two buffers of at least one (even-padded) column.
-  const size_t min_tile = size_t(NT / 32) * 2 * size_t((max_m + 2) & ~1);
-  if (tile < min_tile) tile = min_tile;
-  if (tile < 1536) tile = 1536;                             // member staging (2 x 512)
-  const size_t smem = fixed + tile * sizeof(double);
+}
+
+static cudaLaunchConfig_t qr_config(int njobs, int cluster, size_t smem, cudaStream_t st,
+                                    cudaLaunchAttribute* at) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(unsigned(njobs * cluster));
   cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = unsigned(cluster);
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, qr_kernel, jobs, int(tile), max_nmem);
+  return cfg;
 }
 
-int qr_cluster_size(int njobs, int min_n) {
-  // Aim for ~2 CTAs per SM over 148 SMs; split a basis only when its panel is
-  // wide enough to give every CTA whole column blocks.
-  int g = 1;
-  while (g < 8 && njobs * g * 2 <= 296 && min_n >= 4 * CB * g) g *= 2;
-  return g;
+void launch_qr(const QrJob* jobs, int njobs, int max_m, int max_nmem, int cluster,
+               cudaStream_t st) {
+  if (njobs <= 0) return;
+  qr_attr();
+  size_t tile = 0;
+  const size_t smem = qr_smem_bytes(max_m, max_nmem, &tile);
+  cudaLaunchAttribute at[1];
+  cudaLaunchConfig_t cfg = qr_config(njobs, cluster, smem, st, at);
+  cudaLaunchKernelEx(&cfg, qr_kernel, jobs, int(tile), max_nmem, max_m);
+}
+
+int qr_cluster_size(int njobs, int min_n, int max_m, int max_nmem) {
+  // A basis is a ~100-step sequential sweep, so the batch runs in waves of
+  // co-resident clusters. Pick the cluster size g (CTAs per basis) that
+  // minimises waves / g, using the occupancy API for how many clusters of
+  // size g fit at once (GPC packing included); every CTA must own at least
+  // two column blocks. Ties go to the smaller cluster.
+  qr_attr();
+  const size_t smem = qr_smem_bytes(max_m, max_nmem, nullptr);
+  static int cache_key[9] = {0};
+  static int cache_val[9] = {0};
+  int best = 1;
+  double best_cost = 1e30;
+  for (int g = 1; g <= 8; ++g) {
+    if (g > 1 && min_n < 2 * CB * g) break;
+    int fit = 0;
+    if (cache_key[g] == int(smem)) {
+      fit = cache_val[g];
+    } else {
+      cudaLaunchAttribute at[1];
+      cudaLaunchConfig_t cfg = qr_config(g, g, smem, nullptr, at);
+      if (cudaOccupancyMaxActiveClusters(&fit, qr_kernel, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        fit = 0;
+      }
+      cache_key[g] = int(smem);
+      cache_val[g] = fit;
+    }
+    if (fit <= 0) continue;
+    const int waves = (njobs + fit - 1) / fit;
+    const double cost = double(waves) / g * (1.0 + 0.02 * (g - 1));
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = g;
+    }
+  }
+  return best;
 }
 
 }  // namespace h2g

@@ -160,7 +160,7 @@ struct QrJob {
 void launch_qr(const QrJob* jobs, int njobs, int max_m, int max_nmem, int cluster,
                cudaStream_t st);
 // CTAs per basis (thread-block cluster size) for a batch of njobs bases.
-int qr_cluster_size(int njobs, int min_n);
+int qr_cluster_size(int njobs, int min_n, int max_m, int max_nmem);
 size_t qr_scratch_doubles(int m, int n, int nmem);
 
 }  // namespace h2g

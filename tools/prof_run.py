@@ -9,7 +9,8 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 xyz, q = _fib_spheres(n, 1, 3.0, 42)
 p = h2.Problem()
 p.set_kernel("yukawa", 1.0, 1.0, 1e-3)
-p.set_options(tol=1e-6, cap=100)
+import os
+p.set_options(tol=1e-6, cap=100, qr_mem_budget=int(float(os.environ.get("QR_BUDGET", "0"))))
 p.build(xyz, q, 256)
 p.factor()
 x = p.solve(np.random.default_rng(7).uniform(-1, 1, n))
