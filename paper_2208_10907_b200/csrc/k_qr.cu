@@ -112,7 +112,7 @@ __host__ __device__ inline Scratch carve(double* s, int m, int n, int nmem) {
   return c;
 }
 
-__device__ double block_max(double v, double* red) {
+__device__ __forceinline__ double block_max(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   __syncthreads();
@@ -129,7 +129,7 @@ __device__ double block_max(double v, double* red) {
   return r;
 }
 
-__device__ int block_min_int(int v, int* red) {
+__device__ __forceinline__ int block_min_int(int v, int* red) {
   for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_down_sync(0xffffffffu, v, o));
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   __syncthreads();
@@ -157,7 +157,7 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void st_global16(double* p, double x, double y) {
-  asm volatile("st.global.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(x), "d"(y) : "memory");
+  asm volatile("st.global.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(x), "d"(y));
 }
 
 // red_h (above) over a shared-memory column against v, streamed as 16-byte
@@ -179,18 +179,34 @@ __device__ __forceinline__ double dot_h_pairs(const double* __restrict__ col,
   const double2* v2 = reinterpret_cast<const double2*>(vb + off + t);
   const int npair = (nu - t) >> 1;
   int q = 0;
-  for (; q + 4 <= npair; q += 4) {
+  const int ng = npair >> 2;  // groups of 4 pairs, the next group's loads in flight
+  if (ng > 0) {
     double2 x[4], y[4];
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
-      x[w] = c2[q + w];
-      y[w] = v2[q + w];
+      x[w] = c2[w];
+      y[w] = v2[w];
     }
+    for (int g = 0; g < ng; ++g) {
+      double2 xn[4], yn[4];
+      const int qn = g + 1 < ng ? 4 * (g + 1) : 4 * g;
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      s = s + x[w].x * y[w].x;
-      s = s + x[w].y * y[w].y;
+      for (int w = 0; w < 4; ++w) {
+        xn[w] = c2[qn + w];
+        yn[w] = v2[qn + w];
+      }
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        s = s + x[w].x * y[w].x;
+        s = s + x[w].y * y[w].y;
+      }
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        x[w] = xn[w];
+        y[w] = yn[w];
+      }
     }
+    q = 4 * ng;
   }
   for (; q < npair; ++q) {
     const double2 x = c2[q], y = v2[q];
@@ -204,6 +220,37 @@ __device__ __forceinline__ double dot_h_pairs(const double* __restrict__ col,
   }
   if (lastf) s = fma(col[off + t], vb[off + t], s);
   return s;
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// One-instruction column load: global -> shared bulk copy (TMA engine)
+// completing on an mbarrier.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
 __device__ __forceinline__ void cp_async_wait_all() {
@@ -228,48 +275,59 @@ struct Own {
   }
 };
 
-// Member-mass downdates of one step (linalg.cpp:312-321), lead CTA. Members
-// are contiguous ranges of original columns and position j initially holds
-// column j; only pivot swaps displace columns, so the positions (> s) where
-// a column of another member sits form a short sorted list D (positions Dp,
-// their columns' members Dg, both in shared memory). Each thread owns whole
-// members and runs each member's chain over its range (skipping D) merged
-// with its displaced columns, i.e. in the reference's position order; the
-// range's rkj^2 are fetched eight at a time ahead of the dependent chain.
+// Member masses (linalg.cpp:240-256, :312-321). Member g is owned by CTA
+// g % G of the cluster and, inside it, by one warp; members are contiguous
+// ranges of original columns and position j initially holds column j, so
+// only pivot swaps displace columns: the positions (> k) where a column of
+// another member sits form a short sorted list D (positions Dp, their
+// columns' members Dg, in shared memory, maintained identically by every
+// CTA). A member's chain runs over its range, skipping D, merged with its
+// own displaced positions: the reference's position order.
 __device__ __forceinline__ double mass_sub(double val, double x) {
   const double v = val - x;
   return v < 0.0 ? 0.0 : v;
 }
-__device__ void member_step(const double* __restrict__ sq, int s, int nmem, const int64_t* off,
-                            const int* Dp, const int* Dg, int nd, double* mmsh) {
-  for (int g = threadIdx.x; g < nmem; g += NT) {
-    const int a = max(s + 1, int(off[g])), b = int(off[g + 1]);
-    double val = mmsh[g];
-    int p = 0;
-    for (; p < nd && Dp[p] < a; ++p)
-      if (Dg[p] == g) val = mass_sub(val, __ldcg(&sq[Dp[p]]));
-    int nextd = p < nd ? Dp[p] : 0x7fffffff;
-    for (int j0 = a; j0 < b; j0 += 8) {
-      double x[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) x[u] = j0 + u < b ? __ldcg(&sq[j0 + u]) : 0.0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int j = j0 + u;
-        if (j < b) {
-          if (j == nextd) {
-            ++p;
-            nextd = p < nd ? Dp[p] : 0x7fffffff;
-          } else {
-            val = mass_sub(val, x[u]);
-          }
-        }
-      }
+
+// Ordered chain of one warp over x[a, b), skipping the positions Dp[p..]
+// (sorted; p advances past the skipped ones): val = val - x[j] clamped at 0
+// (CLAMP) or val = val + x[j]. Every lane computes the same chain; the
+// values arrive 256 at a time (8 per lane, the next 256 in flight) and are
+// broadcast by shuffles, so the dependent chain runs at FP64 latency.
+template <bool CLAMP>
+__device__ __forceinline__ double warp_chain(const double* __restrict__ x, int a, int b,
+                                             const int* Dp, int& p, int nd, double val) {
+  const int lane = threadIdx.x & 31;
+  auto fetch = [&](int j0) {
+    const int j = j0 + lane;
+    return j < b ? __ldcg(&x[j]) : 0.0;
+  };
+  // Four rounds of 32 in flight ahead of the chain.
+  double c0 = fetch(a), c1 = fetch(a + 32), c2 = fetch(a + 64), c3 = fetch(a + 96);
+  for (int base = a; base < b; base += 32) {
+    // Skip mask of these 32 positions: past b, or in D.
+    const int left = b - base;
+    unsigned skip = left >= 32 ? 0u : ~0u << left;
+    const int lim = min(base + 32, b);
+    while (p < nd && Dp[p] < lim) {
+      skip |= 1u << (Dp[p] - base);
+      ++p;
     }
-    for (; p < nd; ++p)
-      if (Dp[p] >= b && Dg[p] == g) val = mass_sub(val, __ldcg(&sq[Dp[p]]));
-    mmsh[g] = val;
+    const double cur = c0;
+    c0 = c1;
+    c1 = c2;
+    c2 = c3;
+    c3 = fetch(base + 128);
+    // A skipped position subtracts (adds) +0, which leaves val unchanged
+    // (val >= +0); masking the bits keeps the skip off the dependent chain.
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+      const double xv = __shfl_sync(0xffffffffu, cur, l);
+      const long long keep = ((skip >> l) & 1u) ? 0ll : -1ll;
+      const double xl = __longlong_as_double(__double_as_longlong(xv) & keep);
+      val = CLAMP ? mass_sub(val, xl) : val + xl;
+    }
   }
+  return val;
 }
 
 struct ClSlots {
@@ -300,6 +358,7 @@ __global__ void __launch_bounds__(NT, 1) qr_kernel(const QrJob* __restrict__ job
   __shared__ double sh_tau;
   __shared__ int sh_nd;
   __shared__ ClSlots slot;
+  __shared__ __align__(8) uint64_t wbar[NT / 32];
   cg::cluster_group cluster = cg::this_cluster();
   const int G = int(cluster.num_blocks());
   const int cr = int(cluster.block_rank());
@@ -322,6 +381,10 @@ __global__ void __launch_bounds__(NT, 1) qr_kernel(const QrJob* __restrict__ job
   if (job.cap > 0 && job.cap < kmax) kmax = job.cap;
   const bool lead = cr == 0;
   const int nloc = own.below(n);
+  if (tid < NT / 32) mbar_init(&wbar[tid], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+  unsigned wpar = 0;  // phase parity of this warp's barrier
 
   // R = A (skipped when factoring in place): own columns.
   if (!(job.A.p == W && job.A.rs == 1 && job.A.cs == ldw)) {
@@ -331,7 +394,9 @@ __global__ void __launch_bounds__(NT, 1) qr_kernel(const QrJob* __restrict__ job
     }
     __syncthreads();
   }
-  // Column norms of own columns (pattern P2 over all rows), tile by tile.
+  // Column norms of own columns (pattern P2 over all rows), tile by tile;
+  // their max is step 0's pivot value (later steps take it from the sweep).
+  double lmax = -1.0;
   {
     const int pitch = m | 1;
     const int twmax = max(1, min(NT, tile_doubles / pitch));
@@ -350,69 +415,97 @@ __global__ void __launch_bounds__(NT, 1) qr_kernel(const QrJob* __restrict__ job
         S.cn2[j] = s;
         S.cn2o[j] = s;
         S.piv[j] = j;
+        lmax = fmax(lmax, s);
       }
       __syncthreads();
     }
   }
+  {
+    const double mx = block_max(lmax, redd);
+    if (tid == 0) slot.d = mx;
+  }
   cluster.sync();
   const bool members = nmem >= 1;
-  if (lead) {
-    if (members) {
-      for (int g = tid; g < nmem; g += NT) {
-        double mass = 0.0;
-        for (int64_t j = job.member_off[g]; j < job.member_off[g + 1]; ++j) {
-          S.grp[j] = g;
-          mass += S.cn2[j];
-        }
+  if (lead && members)
+    for (int g = tid; g < nmem; g += NT)
+      for (int64_t j = job.member_off[g]; j < job.member_off[g + 1]; ++j) S.grp[j] = g;
+  // Own members: g = cr + G * (warp + NW * t).
+  auto member_of_warp = [&](int t) { return cr + G * (warp + NW * t); };
+  if (members) {
+    for (int t = 0; member_of_warp(t) < nmem; ++t) {
+      const int g = member_of_warp(t);
+      int p = 0;
+      const double mass = warp_chain<false>(S.cn2, int(job.member_off[g]),
+                                            int(job.member_off[g + 1]), Dp, p, 0, 0.0);
+      if (lane == 0) {
         mmsh[g] = mass;
         S.mt[g] = job.member_tol * job.member_tol * mass;
       }
     }
-    __syncthreads();
+  }
+  __syncthreads();
+  {
     int not_done = 0;
     if (members)
-      for (int g = tid; g < nmem; g += NT) not_done |= (mmsh[g] > S.mt[g]);
+      for (int g = cr + G * tid; g < nmem; g += G * NT) not_done |= (mmsh[g] > S.mt[g]);
     not_done = __syncthreads_or(not_done);
     if (tid == 0) slot.flag = not_done;
   }
 
   double r11 = -1.0;
   int rank = 0;
-  int nd = 0;  // length of the displaced-position list D (lead CTA)
+  int nd = 0;  // length of the displaced-position list D
   long long t_piv = 0, t_refl = 0, t_tile = 0, t_mem = 0, t0c;
   long long t_w = 0, t_c = 0, t_s = 0, n_t = 0;
   for (int k = 0; k < kmax; ++k) {
     t0c = clock64();
-    // Pivot: cluster-wide max of the remaining norms, then the lowest
-    // original index within the 4e-15 tie band (linalg.cpp:263-274).
+    // Pivot: cluster-wide max of the remaining norms (each CTA's max was
+    // published by its previous sweep), then the lowest original index
+    // within the 4e-15 tie band (linalg.cpp:263-274): one scan for the
+    // minimum candidate and its position.
     const int lk = own.below(k);
-    double mx = -1.0;
-    for (int li = lk + tid; li < nloc; li += NT) mx = fmax(mx, S.cn2[own.l2g(li)]);
-    mx = block_max(mx, redd);
-    if (tid == 0) slot.d = mx;
-    cluster.sync();
     double best = -1.0;
     for (int q = 0; q < G; ++q) best = fmax(best, cluster.map_shared_rank(&slot, q)->d);
-    const int members_not_done = cluster.map_shared_rank(&slot, 0)->flag;
     if (best <= 0.0) break;
     const double tie = best * (1.0 - 4e-15);
-    int cand = 0x7fffffff;
-    for (int li = lk + tid; li < nloc; li += NT) {
-      const int j = own.l2g(li);
-      if (S.cn2[j] >= tie) cand = min(cand, S.piv[j]);
+    int cand = 0x7fffffff, cpos = 0x7fffffff;
+    {
+      int li = lk + tid;
+      for (; li + 3 * NT < nloc; li += 4 * NT) {
+        int jj[4];
+        double cv[4];
+        int pv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          jj[u] = own.l2g(li + u * NT);
+          cv[u] = __ldcg(&S.cn2[jj[u]]);
+          pv[u] = __ldcg(&S.piv[jj[u]]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (cv[u] >= tie && pv[u] < cand) {
+            cand = pv[u];
+            cpos = jj[u];
+          }
+      }
+      for (; li < nloc; li += NT) {
+        const int j = own.l2g(li);
+        const int pv = __ldcg(&S.piv[j]);
+        if (__ldcg(&S.cn2[j]) >= tie && pv < cand) {
+          cand = pv;
+          cpos = j;
+        }
+      }
     }
-    cand = block_min_int(cand, redi);
-    int cpos = 0x7fffffff;
-    for (int li = lk + tid; li < nloc; li += NT) {
-      const int j = own.l2g(li);
-      if (S.piv[j] == cand && S.cn2[j] >= tie) cpos = j;
-    }
-    cpos = block_min_int(cpos, redi);
+    const int cmin = block_min_int(cand, redi);
+    cpos = block_min_int(cand == cmin ? cpos : 0x7fffffff, redi);
     if (tid == 0) {
-      slot.piv = cand;
+      slot.piv = cmin;
       slot.pos = cpos;
     }
     cluster.sync();
+    int members_not_done = 0;
+    for (int q = 0; q < G; ++q) members_not_done |= cluster.map_shared_rank(&slot, q)->flag;
     int sel_orig = 0x7fffffff, sel = 0x7fffffff;
     for (int q = 0; q < G; ++q) {
       const ClSlots* o = cluster.map_shared_rank(&slot, q);
@@ -485,6 +578,7 @@ __global__ void __launch_bounds__(NT, 1) qr_kernel(const QrJob* __restrict__ job
     // of rows [k0, m), k0 = k rounded down to even (ldw is even, so every
     // segment is 16-byte aligned); slot pitch P = 2 mod 4 doubles keeps the
     // per-lane 16-byte shared loads conflict-free.
+    lmax = -1.0;
     {
       const int rows = m - k;
       const int k0 = k & ~1, off = k - k0;
@@ -505,29 +599,24 @@ __global__ void __launch_bounds__(NT, 1) qr_kernel(const QrJob* __restrict__ job
         vr[u] = p < nps ? *reinterpret_cast<const double2*>(vsh + k1 + 2 * p) : make_double2(0.0, 0.0);
       }
       const int l0 = own.below(k + 1);
-      auto load_col = [&](int slotc, int j) {
-        const double* src = W + int64_t(j) * ldw + k0;
-        double* dst = Tw + slotc * P;
-        if (np <= 128) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int p = lane + 32 * u;
-            if (p < np) cp_async16(dst + 2 * p, src + 2 * p);
-          }
-        } else {
-          for (int p = lane; p < np; p += 32) cp_async16(dst + 2 * p, src + 2 * p);
+      // Tile loads: one bulk copy per column (lane c issues column c) on the
+      // warp's mbarrier; lane 0 arms it with the tile's byte count first.
+      const unsigned colbytes = unsigned(16 * np);
+      auto load_tile = [&](int abase, int cnt) {
+        if (lane == 0) mbar_expect_tx(&wbar[warp], colbytes * unsigned(cnt));
+        __syncwarp();
+        if (lane < cnt) {
+          fence_proxy_async();
+          bulk_load(Tw + lane * P, W + int64_t(own.l2g(abase + lane)) * ldw + k0, colbytes, &wbar[warp]);
         }
       };
       int a = l0 + warp * cw;
-      if (a < nloc) {
-        const int tw = min(cw, nloc - a);
-        for (int c = 0; c < tw; ++c) load_col(c, own.l2g(a + c));
-      }
+      if (a < nloc) load_tile(a, min(cw, nloc - a));
       for (; a < nloc; a += NW * cw) {
         const int tw = min(cw, nloc - a);
         long long c0 = clock64();
-        cp_async_wait_all();
-        __syncwarp();
+        mbar_wait(&wbar[warp], wpar);
+        wpar ^= 1u;
         long long c1 = clock64();
         double sc = 0.0;
         int jl = 0;
@@ -546,56 +635,78 @@ __global__ void __launch_bounds__(NT, 1) qr_kernel(const QrJob* __restrict__ job
                   x = y = tau != 0.0 ? fma(sc, vsh[k + r], col[off + r]) : col[off + r];
                 },
                 1, rows - 1);
-          S.cn2[jl] = fmax(0.0, upd);
+          const double nc = fmax(0.0, upd);
+          S.cn2[jl] = nc;
           S.sq[jl] = sq;
+          lmax = fmax(lmax, nc);
         }
         __syncwarp();
         long long c2 = clock64();
         const int an = a + NW * cw;
         const int twn = an < nloc ? min(cw, nloc - an) : 0;
-        for (int c = 0; c < tw; ++c) {
-          const double s_c = __shfl_sync(0xffffffffu, sc, c);
-          const int j = __shfl_sync(0xffffffffu, jl, c);
-          const double* colc = Tw + c * P + (k1 - k0);
-          if (tau != 0.0) {
-            double* dst = W + int64_t(j) * ldw + k1;
+        // Update + store, two columns per pass: the stores carry no memory
+        // clobber, so the next column's shared loads issue ahead of them.
+        // The slots are refilled only after every lane's reads (syncwarp).
+        if (tau != 0.0) {
+          for (int c = 0; c < tw; c += 2) {
+            const bool two = c + 1 < tw;
+            const double s_0 = __shfl_sync(0xffffffffu, sc, c);
+            const int j_0 = __shfl_sync(0xffffffffu, jl, c);
+            const double s_1 = __shfl_sync(0xffffffffu, sc, two ? c + 1 : c);
+            const int j_1 = __shfl_sync(0xffffffffu, jl, two ? c + 1 : c);
+            const double* col0 = Tw + c * P + (k1 - k0);
+            const double* col1 = col0 + P;
+            double* dst0 = W + int64_t(j_0) * ldw + k1;
+            double* dst1 = W + int64_t(j_1) * ldw + k1;
             if (nps <= 128) {
-              double2 x[4];
+              double2 x0[4], x1[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int p = lane + 32 * u;
-                x[u] = p < nps ? *reinterpret_cast<const double2*>(colc + 2 * p) : make_double2(0.0, 0.0);
+                x0[u] = p < nps ? *reinterpret_cast<const double2*>(col0 + 2 * p) : make_double2(0.0, 0.0);
+                x1[u] = (two && p < nps) ? *reinterpret_cast<const double2*>(col1 + 2 * p)
+                                         : make_double2(0.0, 0.0);
               }
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int p = lane + 32 * u;
-                if (p < nps)
-                  st_global16(dst + 2 * p, fma(s_c, vr[u].x, x[u].x), fma(s_c, vr[u].y, x[u].y));
+                if (p < nps) {
+                  st_global16(dst0 + 2 * p, fma(s_0, vr[u].x, x0[u].x), fma(s_0, vr[u].y, x0[u].y));
+                  if (two)
+                    st_global16(dst1 + 2 * p, fma(s_1, vr[u].x, x1[u].x), fma(s_1, vr[u].y, x1[u].y));
+                }
               }
             } else {
               for (int p = lane; p < nps; p += 32) {
-                const double2 x = *reinterpret_cast<const double2*>(colc + 2 * p);
                 const double2 v = *reinterpret_cast<const double2*>(vsh + k1 + 2 * p);
-                st_global16(dst + 2 * p, fma(s_c, v.x, x.x), fma(s_c, v.y, x.y));
+                const double2 x = *reinterpret_cast<const double2*>(col0 + 2 * p);
+                st_global16(dst0 + 2 * p, fma(s_0, v.x, x.x), fma(s_0, v.y, x.y));
+                if (two) {
+                  const double2 y = *reinterpret_cast<const double2*>(col1 + 2 * p);
+                  st_global16(dst1 + 2 * p, fma(s_1, v.x, y.x), fma(s_1, v.y, y.y));
+                }
               }
             }
           }
-          if (c < twn) load_col(c, own.l2g(an + c));
         }
-        for (int c = tw; c < twn; ++c) load_col(c, own.l2g(an + c));
+        __syncwarp();
+        if (twn > 0) load_tile(an, twn);
         long long c3 = clock64();
         t_w += c1 - c0; t_c += c2 - c1; t_s += c3 - c2; ++n_t;
       }
-      cp_async_wait_all();
+    }
+    {
+      const double mx = block_max(lmax, redd);
+      if (tid == 0) slot.d = mx;  // next step's pivot value
     }
     cluster.sync();
     t_tile += clock64() - t0c; t0c = clock64();
     ++rank;
-    if (lead && members) {
+    if (members) {
       // D: positions > k holding a column of another member (sorted). The
       // swap of step k moved the column from position k to position sel.
       if (tid == 0) {
-        const int sel = S.swp[kmax0 + k];
+        const int sel = __ldcg(&S.swp[kmax0 + k]);
         int w = 0;
         for (int q = 0; q < nd; ++q)
           if (Dp[q] > k && Dp[q] != sel) {
@@ -603,8 +714,8 @@ __global__ void __launch_bounds__(NT, 1) qr_kernel(const QrJob* __restrict__ job
             Dg[w] = Dg[q];
             ++w;
           }
-        const int gs = S.grp[S.piv[sel]];
-        if (sel > k && gs != S.grp[sel]) {
+        const int gs = __ldcg(&S.grp[__ldcg(&S.piv[sel])]);
+        if (sel > k && gs != __ldcg(&S.grp[sel])) {
           int q = w;
           while (q > 0 && Dp[q - 1] > sel) {
             Dp[q] = Dp[q - 1];
@@ -619,50 +730,79 @@ __global__ void __launch_bounds__(NT, 1) qr_kernel(const QrJob* __restrict__ job
       }
       __syncthreads();
       nd = sh_nd;
-      member_step(S.sq, k, nmem, job.member_off, Dp, Dg, nd, mmsh);
+      for (int t = 0; member_of_warp(t) < nmem; ++t) {
+        const int g = member_of_warp(t);
+        const int a = max(k + 1, int(job.member_off[g])), b = int(job.member_off[g + 1]);
+        double val = mmsh[g];
+        int p = 0;
+        for (; p < nd && Dp[p] < a; ++p)
+          if (Dg[p] == g) val = mass_sub(val, __ldcg(&S.sq[Dp[p]]));
+        val = warp_chain<true>(S.sq, a, b, Dp, p, nd, val);
+        for (; p < nd; ++p)
+          if (Dg[p] == g) val = mass_sub(val, __ldcg(&S.sq[Dp[p]]));
+        __syncwarp();
+        if (lane == 0) mmsh[g] = val;
+      }
       __syncthreads();
       if (tid == 0) {
-        const int gk = S.grp[S.piv[k]];
-        mmsh[gk] = mass_sub(mmsh[gk], S.pn2[k]);
+        // The processed column's leftover mass is gone entirely.
+        const int gk = __ldcg(&S.grp[__ldcg(&S.piv[k])]);
+        if (gk % G == cr) mmsh[gk] = mass_sub(mmsh[gk], __ldcg(&S.pn2[k]));
       }
       __syncthreads();
       int not_done = 0;
-      for (int g = tid; g < nmem; g += NT) not_done |= (mmsh[g] > S.mt[g]);
+      for (int g = cr + G * tid; g < nmem; g += G * NT) not_done |= (mmsh[g] > S.mt[g]);
       not_done = __syncthreads_or(not_done);
       if (tid == 0) slot.flag = not_done;
     }
     t_mem += clock64() - t0c;
   }
-  // No CTA may leave while others can still read its slots.
+  // No CTA may reuse its slots while others can still read them.
   cluster.sync();
-  if (!lead) return;
-  if (tid == 0 && job.dbg) {
+  if (lead && tid == 0 && job.dbg) {
     job.dbg[0] = double(t_piv); job.dbg[1] = double(t_refl); job.dbg[2] = double(t_tile);
     job.dbg[3] = double(t_mem); job.dbg[4] = double(rank); job.dbg[5] = double(n);
     job.dbg[8] = double(t_w); job.dbg[9] = double(t_c); job.dbg[10] = double(t_s); job.dbg[11] = double(n_t);
   }
   long long tq = clock64();
 
-  // form_q (linalg.cpp:181-185): Q = I, reflectors applied backward.
-  double* Q = job.Q;
-  for (int64_t e = tid; e < int64_t(m) * m; e += NT) Q[e] = (e / m == e % m) ? 1.0 : 0.0;
-  __syncthreads();
-  for (int k = rank - 1; k >= 0; --k) {
-    const double tau = __ldcg(&S.tau[k]);
-    if (tau == 0.0) continue;
-    const double* vk = S.V + int64_t(k) * m;
-    for (int i = tid; i < m; i += NT) vsh[i] = __ldcg(&vk[i]);
-    __syncthreads();
-    for (int j = tid; j < m; j += NT) {
-      const double dot = red_h(
-          [&](int i, double& a, double& b) { a = vsh[i]; b = Q[int64_t(i) * m + j]; }, k, m - k, 0.0);
-      const double s = tau * dot;
-      for (int i = k; i < m; ++i) Q[int64_t(i) * m + j] = fma(-s, vsh[i], Q[int64_t(i) * m + j]);
+  // form_q (linalg.cpp:181-185): Q = I, reflectors applied backward. Every
+  // column of Q evolves independently, so the cluster's CTAs split the
+  // columns and each lane carries one column in shared memory through all
+  // reflectors (dot chain and update in the reference's order).
+  {
+    double* Q = job.Q;
+    const int jc0 = (m * cr) / G, jc1 = (m * (cr + 1)) / G;
+    const int pitch = m | 1;
+    const int per_warp = tile_doubles / NW;
+    const int cwq = max(1, min(32, per_warp / pitch));
+    for (int jb = jc0; jb < jc1; jb += NW * cwq) {
+      const int jw = jb + warp * cwq;
+      const int tw = max(0, min(cwq, jc1 - jw));
+      const bool act = lane < tw;
+      const int j = jw + lane;
+      double* q = T + warp * per_warp + lane * pitch;
+      if (act)
+        for (int i = 0; i < m; ++i) q[i] = (i == j) ? 1.0 : 0.0;
+      for (int k = rank - 1; k >= 0; --k) {
+        __syncthreads();
+        for (int i = tid; i < m; i += NT) vsh[i] = __ldcg(&S.V[int64_t(k) * m + i]);
+        if (tid == 0) sh_tau = __ldcg(&S.tau[k]);
+        __syncthreads();
+        const double tau = sh_tau;
+        if (tau == 0.0 || !act) continue;
+        const double dot = red_h([&](int i, double& x, double& y) { x = vsh[i]; y = q[i]; }, k, m - k, 0.0);
+        const double sk = tau * dot;
+        for (int i = k; i < m; ++i) q[i] = fma(-sk, vsh[i], q[i]);
+      }
+      __syncwarp();
+      for (int i = 0; i < m; ++i)
+        if (act) Q[int64_t(i) * m + j] = q[i];
+      __syncthreads();
     }
-    __syncthreads();
   }
-  if (tid == 0) *job.rank_out = rank;
-  if (tid == 0 && job.dbg) job.dbg[6] = double(clock64() - tq);
+  if (lead && tid == 0) *job.rank_out = rank;
+  if (lead && tid == 0 && job.dbg) job.dbg[6] = double(clock64() - tq);
 }
 
 size_t qr_fixed_doubles(int max_m, int max_nmem) {
