@@ -51,18 +51,23 @@ struct Cloud {
 // kernel_eval / assemble_block entry (kernels.cpp:232-268): bitwise equal to
 // the reference for Laplace (r = sqrt(fma(dz,dz,fma(dx,dx,dy*dy))), IEEE
 // sqrt and division). Yukawa uses CUDA exp (<= 1 ulp from glibc).
-__device__ __forceinline__ double kernel_entry(const KernelParams& kp, const Cloud& c, int64_t i,
-                                               int64_t j, int* singular) {
-  const double dx = c.x[i] - c.x[j], dy = c.y[i] - c.y[j], dz = c.z[i] - c.z[j];
+__device__ __forceinline__ double kernel_pair(const KernelParams& kp, double xi, double yi,
+                                              double zi, double xj, double yj, double zj,
+                                              double qj, int* singular) {
+  const double dx = xi - xj, dy = yi - yj, dz = zi - zj;
   const double r = sqrt(fma(dz, dz, fma(dx, dx, dy * dy)));
   const double denom = kp.scale * (r + kp.reg);
   if (denom == 0.0) {
     *singular = 1;
     return 0.0;
   }
-  const double qj = c.q[j];
   if (kp.kind == 0) return qj / denom;
   return qj * exp(-kp.alpha_m * r) / denom;
+}
+
+__device__ __forceinline__ double kernel_entry(const KernelParams& kp, const Cloud& c, int64_t i,
+                                               int64_t j, int* singular) {
+  return kernel_pair(kp, c.x[i], c.y[i], c.z[i], c.x[j], c.y[j], c.z[j], c.q[j], singular);
 }
 
 // Device-wide error word: first nonzero code wins (host reads after sync).

@@ -2,25 +2,29 @@
 // multi-segment accumulation and an optional kernel-function generator for
 // the B operand (fused evaluate-and-project).
 //
-// Bit-exactness: mma.sync.m8n8k4.f64 rounds exactly like four sequential
-// FMAs in ascending k (measured on the B200: 0 / 128,000 mismatches,
-// tools/microbench/dmma_order.cu), so accumulating the k4 steps in order
-// over segments in order reproduces the reference gemm_core / gemm_acc
-// sequence c = fma(a, alpha*b, c) bit for bit (linalg.cpp:17-62). Ragged K
-// is padded with a = +0, b = -0: that product adds an exact -0, which leaves
-// every c (including -0.0) unchanged (tools/microbench/dmma_zero.cu).
+// Bit-exactness: mma.sync.m16n8k16.f64 rounds exactly like sixteen
+// sequential FMAs in ascending k (measured on the B200: 0 / 256,000
+// mismatches, tools/microbench/dmma16_order.cu), so accumulating the k16
+// steps in order over segments in order reproduces the reference gemm_core /
+// gemm_acc sequence c = fma(a, alpha*b, c) bit for bit (linalg.cpp:17-62).
+// Ragged K is padded with a = +0, b = -0: that product adds an exact -0,
+// which leaves every c (including -0.0) unchanged
+// (tools/microbench/dmma_zero.cu).
 //
-// Tiling: CTA tile BM x 64, BK = 16, 2*BM threads (warp tile 32 x 32),
-// operands staged in shared memory, the next chunk prefetched into
-// registers; per warp and k4 step 4 x 4 m8n8k4 MMAs. BM = 128 is used when the batch has
-// tall C blocks so a kernel-generated B tile is evaluated once per 128 rows.
+// Tiling: CTA tile BM x 64, BK = 16 (one MMA k-step), 2*BM threads, warp
+// tile 32 x 32 (2 m16 x 4 n8 fragments). Operands go through two shared-
+// memory stages (one barrier per k-step); the next chunk is prefetched into
+// registers while the current one feeds the MMAs. Row strides of 132 / 68
+// doubles (= 4 mod 16) make every fragment load conflict-free. BM = 128 is
+// used when the batch has tall C blocks so a kernel-generated B tile is
+// evaluated once per 128 rows.
 #include "kernels.hpp"
 
 namespace h2g {
 
 namespace {
 
-constexpr int BN = 64, BK = 16, PAD = 8;
+constexpr int BN = 64, BK = 16;
 
 __device__ __forceinline__ bool masked(const GenB& g, int j) {
   for (int t = 0; t < g.nmask; ++t)
@@ -28,13 +32,25 @@ __device__ __forceinline__ bool masked(const GenB& g, int j) {
   return false;
 }
 
-__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
+// D = A(16x16) B(16x8) + D. Fragments (PTX ISA, .f64; g = lane>>2, t = lane&3):
+// a_i = A[g + 8(i%2)][t + 4(i/2)], b_i = B[t + 4i][g], c_i = C[g + 8(i/2)][2t + i%2].
+__device__ __forceinline__ void dmma16(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
+      "{%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+        "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
 }
 
-// Warp tile 32 x 32 (4 x 4 m8n8 fragments); BM/32 x 2 warps -> 2*BM threads.
+template <int BM>
+struct Smem {
+  static constexpr int SA = BM + 4, SB = BN + 4;  // = 4 (mod 16): conflict-free fragments
+  double A[2][BK][SA];
+  double B[2][BK][SB];
+  unsigned char Bmask[BN];
+};
+
 template <int BM>
 __global__ void __launch_bounds__(2 * BM) gemm_kernel(const GemmJob* __restrict__ jobs,
                                                   const GemmSeg* __restrict__ segs,
@@ -42,46 +58,59 @@ __global__ void __launch_bounds__(2 * BM) gemm_kernel(const GemmJob* __restrict_
                                                   KernelParams kp, Cloud cloud, ErrWord* err,
                                                   int tag) {
   constexpr int NT = 2 * BM;
-  constexpr int WM = 32;            // warp tile rows
-  constexpr int FM = WM / 8;        // m8 fragments per warp
-  constexpr int FN = 4;             // n8 fragments per warp (32 columns)
-  constexpr int AE = BM * BK / NT;  // A elements per thread per chunk
+  constexpr int AE = BM * BK / NT;  // A elements per thread per chunk (8)
   constexpr int BE = BK * BN / NT;  // B elements per thread per chunk
-  __shared__ double As[BK][BM + PAD];
-  __shared__ double Bs[BK][BN + PAD];
-  __shared__ unsigned char Bmask[BN];
+  extern __shared__ __align__(16) unsigned char smraw[];
+  Smem<BM>& sm = *reinterpret_cast<Smem<BM>*>(smraw);
   const GemmTile tile = tiles[blockIdx.x];
   const GemmJob job = jobs[tile.job];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = warp % (BM / 32), wn = warp / (BM / 32);
+  const int g = lane >> 2, t = lane & 3;
   const int m0 = tile.tm * BM, n0 = tile.tn * BN;
   const Mat C = job.C;
-  // Accumulators: fragment (fm, fn) holds C rows m0 + wm*WM + fm*8 + (lane>>2),
-  // cols n0 + wn*32 + fn*8 + 2*(lane&3) + {0,1}.
-  double acc[FM][FN][2];
-  const int crow = lane >> 2, ccol = 2 * (lane & 3);
+  // acc[fm][fn][i]: C row m0 + wm*32 + fm*16 + g + 8(i/2), col n0 + wn*32 + fn*8 + 2t + i%2.
+  double acc[2][4][4];
 #pragma unroll
-  for (int fm = 0; fm < FM; ++fm)
+  for (int fm = 0; fm < 2; ++fm)
 #pragma unroll
-    for (int fn = 0; fn < FN; ++fn)
+    for (int fn = 0; fn < 4; ++fn)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int i = m0 + wm * WM + fm * 8 + crow, j = n0 + wn * 32 + fn * 8 + ccol + h;
-        acc[fm][fn][h] = (job.acc && i < C.rows && j < C.cols) ? C.at(i, j) : 0.0;
+      for (int i = 0; i < 4; ++i) {
+        const int r = m0 + wm * 32 + fm * 16 + g + 8 * (i / 2), c = n0 + wn * 32 + fn * 8 + 2 * t + (i % 2);
+        acc[fm][fn][i] = (job.acc && r < C.rows && c < C.cols) ? C.at(r, c) : 0.0;
       }
   int singular = 0;
+  int buf = 0;
   for (int s = 0; s < job.nseg; ++s) {
     const GemmSeg sg = segs[job.seg0 + s];
     const int K = sg.A.cols;
     if (K == 0) continue;
-    const int K4 = (K + 3) & ~3;  // padded with exact no-op (+0, -0) steps
+    const int K16 = (K + 15) & ~15;  // padded with exact no-op (+0, -0) steps
     if (sg.gen) {
       __syncthreads();
-      if (threadIdx.x < BN) Bmask[threadIdx.x] = sg.g.nmask ? masked(sg.g, n0 + threadIdx.x) : 0;
+      if (threadIdx.x < BN) sm.Bmask[threadIdx.x] = sg.g.nmask ? masked(sg.g, n0 + threadIdx.x) : 0;
       __syncthreads();
     }
     const bool a_colmajor = sg.A.rs == 1;
     const bool b_colmajor = sg.B.rs == 1;
+    // Generated B: every thread owns one C column of the tile (nn = tid % BN,
+    // NT is a multiple of BN) and BE k-rows per chunk. The column's point is
+    // loaded once per segment; a chunk row's point is warp-uniform.
+    const int nnT = threadIdx.x % BN;
+    const int jT = n0 + nnT;
+    bool liveT = false;
+    double xT = 0.0, yT = 0.0, zT = 0.0, qT = 0.0;
+    if (sg.gen) {
+      liveT = jT < C.cols && !sm.Bmask[nnT];
+      if (liveT) {
+        const int64_t tp = sg.g.trans ? sg.g.rb + jT : sg.g.cb + jT;
+        xT = cloud.x[tp];
+        yT = cloud.y[tp];
+        zT = cloud.z[tp];
+        qT = cloud.q[tp];
+      }
+    }
     double ra[AE], rb[BE];
     auto fetch = [&](int k0) {
 #pragma unroll
@@ -92,82 +121,102 @@ __global__ void __launch_bounds__(2 * BM) gemm_kernel(const GemmJob* __restrict_
         const int i = m0 + mm, l = k0 + kk;
         ra[u] = (i < sg.A.rows && l < K) ? sg.A.at(i, l) : 0.0;
       }
+      if (sg.gen) {
 #pragma unroll
-      for (int u = 0; u < BE; ++u) {
-        const int e = threadIdx.x + u * NT;
-        int nn, kk;
-        if (sg.gen || !b_colmajor) { nn = e % BN; kk = e / BN; } else { kk = e % BK; nn = e / BK; }
-        const int l = k0 + kk, j = n0 + nn;
-        double v = -0.0;  // pad: exact no-op with a = +0
-        if (l < K && j < C.cols) {
-          double b;
-          if (!sg.gen) {
-            b = sg.B.at(l, j);
-          } else if (Bmask[nn]) {
-            b = 0.0;
-          } else {
-            b = sg.g.trans ? kernel_entry(kp, cloud, sg.g.rb + j, sg.g.cb + l, &singular)
-                           : kernel_entry(kp, cloud, sg.g.rb + l, sg.g.cb + j, &singular);
+        for (int u = 0; u < BE; ++u) {
+          const int l = k0 + threadIdx.x / BN + u * (NT / BN);
+          double v = -0.0;  // pad: exact no-op with a = +0
+          if (l < K && jT < C.cols) {
+            double b = 0.0;
+            if (liveT) {
+              const int64_t cp = sg.g.trans ? sg.g.cb + l : sg.g.rb + l;
+              const double xc = cloud.x[cp], yc = cloud.y[cp], zc = cloud.z[cp];
+              // K(i, j): i = rb + row, j = cb + col of the generated block.
+              b = sg.g.trans ? kernel_pair(kp, xT, yT, zT, xc, yc, zc, cloud.q[cp], &singular)
+                             : kernel_pair(kp, xc, yc, zc, xT, yT, zT, qT, &singular);
+            }
+            v = sg.alpha * b;  // the reference pre-multiplies B by alpha
           }
-          v = sg.alpha * b;  // the reference pre-multiplies B by alpha
+          rb[u] = v;
         }
-        rb[u] = v;
+      } else {
+#pragma unroll
+        for (int u = 0; u < BE; ++u) {
+          const int e = threadIdx.x + u * NT;
+          int nn, kk;
+          if (!b_colmajor) { nn = e % BN; kk = e / BN; } else { kk = e % BK; nn = e / BK; }
+          const int l = k0 + kk, j = n0 + nn;
+          rb[u] = (l < K && j < C.cols) ? sg.alpha * sg.B.at(l, j) : -0.0;
+        }
       }
     };
-    auto stash = [&]() {
+    auto stash = [&](int bb) {
 #pragma unroll
       for (int u = 0; u < AE; ++u) {
         const int e = threadIdx.x + u * NT;
         int mm, kk;
         if (a_colmajor) { mm = e % BM; kk = e / BM; } else { kk = e % BK; mm = e / BK; }
-        As[kk][mm] = ra[u];
+        sm.A[bb][kk][mm] = ra[u];
       }
 #pragma unroll
       for (int u = 0; u < BE; ++u) {
         const int e = threadIdx.x + u * NT;
         int nn, kk;
         if (sg.gen || !b_colmajor) { nn = e % BN; kk = e / BN; } else { kk = e % BK; nn = e / BK; }
-        Bs[kk][nn] = rb[u];
+        sm.B[bb][kk][nn] = rb[u];
       }
     };
-    __syncthreads();
     fetch(0);
-    stash();
+    __syncthreads();  // previous segment's last reads of this buffer are done
+    stash(buf);
     __syncthreads();
-    for (int k0 = 0; k0 < K4; k0 += BK) {
+    for (int k0 = 0; k0 < K16; k0 += BK) {
       // Register prefetch of the next chunk overlaps this chunk's MMAs.
-      const bool more = k0 + BK < K4;
+      const bool more = k0 + BK < K16;
       if (more) fetch(k0 + BK);
-      const int ksteps = min(BK, K4 - k0) / 4;
-      for (int ks = 0; ks < ksteps; ++ks) {
-        const int kr = ks * 4 + (lane & 3);
-        double af[FM], bf[FN];
+      double af[2][8];
 #pragma unroll
-        for (int fm = 0; fm < FM; ++fm) af[fm] = As[kr][wm * WM + fm * 8 + (lane >> 2)];
+      for (int fm = 0; fm < 2; ++fm)
 #pragma unroll
-        for (int fn = 0; fn < FN; ++fn) bf[fn] = Bs[kr][wn * 32 + fn * 8 + (lane >> 2)];
+        for (int i = 0; i < 8; ++i)
+          af[fm][i] = sm.A[buf][t + 4 * (i / 2)][wm * 32 + fm * 16 + g + 8 * (i % 2)];
 #pragma unroll
-        for (int fm = 0; fm < FM; ++fm)
+      for (int fn = 0; fn < 4; ++fn) {
+        double bf[4];
 #pragma unroll
-          for (int fn = 0; fn < FN; ++fn) dmma(acc[fm][fn][0], acc[fm][fn][1], af[fm], bf[fn]);
+        for (int i = 0; i < 4; ++i) bf[i] = sm.B[buf][t + 4 * i][wn * 32 + fn * 8 + g];
+#pragma unroll
+        for (int fm = 0; fm < 2; ++fm) dmma16(acc[fm][fn], af[fm], bf);
       }
       if (more) {
+        stash(buf ^ 1);
         __syncthreads();
-        stash();
-        __syncthreads();
+        buf ^= 1;
       }
     }
   }
   if (singular) raise_err(err, 1, tile.job, 0, tag);
 #pragma unroll
-  for (int fm = 0; fm < FM; ++fm)
+  for (int fm = 0; fm < 2; ++fm)
 #pragma unroll
-    for (int fn = 0; fn < FN; ++fn)
+    for (int fn = 0; fn < 4; ++fn)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int i = m0 + wm * WM + fm * 8 + crow, j = n0 + wn * 32 + fn * 8 + ccol + h;
-        if (i < C.rows && j < C.cols) C.at(i, j) = acc[fm][fn][h];
+      for (int i = 0; i < 4; ++i) {
+        const int r = m0 + wm * 32 + fm * 16 + g + 8 * (i / 2), c = n0 + wn * 32 + fn * 8 + 2 * t + (i % 2);
+        if (r < C.rows && c < C.cols) C.at(r, c) = acc[fm][fn][i];
       }
+}
+
+template <int BM>
+void launch_bm(const GemmJob* jobs, const GemmSeg* segs, const GemmTile* tiles, int ntiles,
+               KernelParams kp, Cloud cloud, ErrWord* err, int tag, cudaStream_t st) {
+  static bool attr = false;
+  const int smem = int(sizeof(Smem<BM>));
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_kernel<BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  gemm_kernel<BM><<<ntiles, 2 * BM, smem, st>>>(jobs, segs, tiles, kp, cloud, err, tag);
 }
 
 }  // namespace
@@ -178,9 +227,9 @@ void launch_gemm(const GemmJob* jobs, const GemmSeg* segs, const GemmTile* tiles
                  int bm, KernelParams kp, Cloud cloud, ErrWord* err, int tag, cudaStream_t st) {
   if (ntiles <= 0) return;
   if (bm == 128)
-    gemm_kernel<128><<<ntiles, 256, 0, st>>>(jobs, segs, tiles, kp, cloud, err, tag);
+    launch_bm<128>(jobs, segs, tiles, ntiles, kp, cloud, err, tag, st);
   else
-    gemm_kernel<64><<<ntiles, 128, 0, st>>>(jobs, segs, tiles, kp, cloud, err, tag);
+    launch_bm<64>(jobs, segs, tiles, ntiles, kp, cloud, err, tag, st);
 }
 
 }  // namespace h2g

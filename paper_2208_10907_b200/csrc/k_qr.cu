@@ -152,10 +152,6 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 }
 
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
 __device__ __forceinline__ void st_global16(double* p, double x, double y) {
   asm volatile("st.global.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(x), "d"(y));
 }
