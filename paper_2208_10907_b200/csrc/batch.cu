@@ -6,6 +6,8 @@
 
 #include "batch.hpp"
 
+#include <cstring>
+
 namespace h2g {
 
 void cuda_check(cudaError_t e, const char* what) {
@@ -55,7 +57,7 @@ void Ctx::prof_end(const char* name, cudaEvent_t a, double flops, double bytes) 
   cudaEvent_t e;
   cuda_check(cudaEventCreate(&e), "event");
   cuda_check(cudaEventRecord(e, stream), "event record");
-  prec.push_back({name, a, e, flops, bytes});
+  prec.push_back({name, a, e, flops, bytes, phase});
 }
 
 void Ctx::prof_resolve() {
@@ -68,13 +70,53 @@ void Ctx::prof_resolve() {
     g.flops += r.flops;
     g.bytes += r.bytes;
     g.launches++;
+    if (prof_gaps && last_end) {
+      float gms = 0;
+      cuda_check(cudaEventElapsedTime(&gms, last_end, r.a), "elapsed");
+      auto& gg = pagg["gap@" + r.phase];
+      gg.ms += gms;
+      gg.launches++;
+      if (gms > 2.0f)
+        fprintf(stderr, "TIMELINE gap %.1f ms after %s before %s@%s\n", gms, last_name.c_str(),
+                r.name.c_str(), r.phase.c_str());
+    }
     cudaEventDestroy(r.a);
-    cudaEventDestroy(r.b);
+    if (last_end) cudaEventDestroy(last_end);
+    last_end = r.b;
+    last_name = r.name;
   }
   prec.clear();
 }
 
+const void* Ctx::stage(const void* src, size_t bytes) {
+  if (!pin) {
+    pin_cap = size_t(64) << 20;
+    if (cudaMallocHost(&pin, pin_cap) != cudaSuccess) {
+      cudaGetLastError();
+      pin = nullptr;
+      pin_cap = 0;
+    }
+  }
+  const size_t need = (bytes + 255) & ~size_t(255);
+  if (!pin || need > pin_cap) return src;  // pageable fallback
+  if (pin_head + need > pin_cap) {
+    cuda_check(cudaStreamSynchronize(stream), "stage sync");
+    pin_head = 0;
+  }
+  char* d = pin + pin_head;
+  pin_head += need;
+  memcpy(d, src, bytes);
+  return d;
+}
+
+Ctx::~Ctx() {
+  // The owner may already have destroyed the stream; cudaFreeHost waits for
+  // the device itself.
+  if (pin) cudaFreeHost(pin);
+}
+
 void Ctx::sync() {
+  pin_head = 0;
   cuda_check(cudaStreamSynchronize(stream), "stream sync");
   check_err();
 }

@@ -35,6 +35,17 @@ struct Ctx {
     phase_flops[phase] += f;
   }
   Slab alloc(size_t bytes);
+  // Pinned staging arena for descriptor uploads: a copy from pageable memory
+  // larger than a few KB makes cudaMemcpyAsync wait for the stream, which
+  // serialises host preparation with the GPU. Regions are handed out
+  // linearly and recycled at every sync (all staged copies have run).
+  char* pin = nullptr;
+  size_t pin_cap = 0, pin_head = 0;
+  const void* stage(const void* src, size_t bytes);
+  Ctx() = default;
+  Ctx(const Ctx&) = delete;
+  Ctx& operator=(const Ctx&) = delete;
+  ~Ctx();
   void sync();            // stream sync + error word check
   void check_err();       // throws the reference's message for device errors
   std::vector<std::string> lu_names;  // current LU batch names (for errors)
@@ -48,10 +59,16 @@ struct Ctx {
     std::string name;
     cudaEvent_t a, b;
     double flops, bytes;
+    std::string phase;
   };
   bool prof = false;
   bool prof_detail = getenv("H2G_PROF_DETAIL") != nullptr;  // per-phase kernel names
   std::vector<ProfRec> prec;
+  // H2G_TIMELINE: also account the idle time between consecutive profiled
+  // kernels as "gap@<phase>" (host-side launch preparation, syncs).
+  bool prof_gaps = getenv("H2G_TIMELINE") != nullptr;
+  cudaEvent_t last_end = nullptr;
+  std::string last_name;
   std::map<std::string, ProfAgg> pagg;
   cudaEvent_t prof_begin();
   void prof_end(const char* name, cudaEvent_t a, double flops, double bytes);
@@ -80,8 +97,8 @@ template <class T>
 T* upload(Ctx& c, const std::vector<T>& v, Slab& keep) {
   if (v.empty()) return nullptr;
   keep = c.alloc(sizeof(T) * v.size());
-  cuda_check(cudaMemcpyAsync(keep.get(), v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice,
-                             c.stream),
+  cuda_check(cudaMemcpyAsync(keep.get(), c.stage(v.data(), sizeof(T) * v.size()),
+                             sizeof(T) * v.size(), cudaMemcpyHostToDevice, c.stream),
              "upload");
   return static_cast<T*>(keep.get());
 }

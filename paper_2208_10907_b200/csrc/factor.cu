@@ -110,6 +110,13 @@ Problem::~Problem() {
 
 // Pipeline::build (report.cpp:79-91): tree, classification, near field.
 void Problem::build(const double* d_xyz, const double* d_q, int64_t n, int64_t leaf) {
+  // A rebuild invalidates any previous factorization.
+  factored = false;
+  built = false;
+  U.clear();
+  V.clear();
+  levels.clear();
+  top = LuF{};
   double t0 = now_s();
   DevTimer dt(c.stream);
   build_tree_device(T, d_xyz, d_q, n, leaf, c.stream);
@@ -350,7 +357,7 @@ struct Driver {
   // of the chunk's row (and col) concats in place, then sink(k, Qrow, rrow,
   // Qcol, rcol) per box while the Q's are alive.
   void run_bases(std::vector<Members>& rows, std::vector<Members>* cols, const FillFn& fill,
-                 const SinkFn& sink) {
+                 const SinkFn& sink, const std::function<void()>& flush = {}) {
     const int64_t m = int64_t(rows.size());
     int64_t k0 = 0;
     while (k0 < m) {
@@ -390,8 +397,10 @@ struct Driver {
         const int rc = cols ? rank[nk + (k - k0)] : 0;
         sink(k, Q[k - k0].m, rank[k - k0], qc, rc);
       }
-      // Drain the sink's copies before the Q's and concats are released.
-      c.sync();
+      // One launch for the whole chunk's sink copies; the Q's and concats
+      // are released stream-ordered behind them (cudaFreeAsync).
+      if (flush) flush();
+      if (hp) c.sync();
       double ht4 = now_s();
       for (int64_t k = k0; k < k1; ++k) {
         rows[k].concat = DMat{};
@@ -404,6 +413,24 @@ struct Driver {
       }
       k0 = k1;
     }
+  }
+
+  // Off-diagonal fills of a level indexed by row and by column, each list in
+  // the FillSet's (map) order, so that "for every fill with key.first == i"
+  // walks the same entries in the same order without scanning the map.
+  struct FillIndex {
+    std::vector<std::vector<const DMat*>> by_row, by_col;
+  };
+  static FillIndex index_fills(const FillSet& fills, int64_t m) {
+    FillIndex x;
+    x.by_row.resize(m);
+    x.by_col.resize(m);
+    for (auto& [key, F] : fills) {
+      if (key.first == key.second) continue;
+      x.by_row[key.first].push_back(&F);
+      x.by_col[key.second].push_back(&F);
+    }
+    return x;
   }
 
   // Rank-equalised square bases (compression.cpp:224-229 / ulv.cpp:507-511):
@@ -433,17 +460,16 @@ struct Driver {
     const bool coupling = opt.absorb_coupling && opt.structure == 0 && sys.offdiag;
     // Row members: fills (i, j != i) | A(i, far j) | A(i, ancestor far J) [+ coupling].
     std::vector<Members> rows(m), cols(m);
+    const FillIndex FI = index_fills(fills, m);
     for (int64_t i = 0; i < m; ++i) {
       Members& R = rows[i];
       R.dim = sys.dims[i];
-      for (auto& [key, F] : fills)
-        if (key.first == i && key.second != i) R.add(F.cols());
+      for (const DMat* F : FI.by_row[i]) R.add(F->cols());
       for (int64_t t = 0; t < S.nfar(L, i); ++t) R.add(int(rs(L, S.far(L, i)[t])));
       for (auto [l2, J] : ancestor_far_partners(L, i)) R.add(int(rs(l2, J)));
       Members& C = cols[i];
       C.dim = sys.dims[i];
-      for (auto& [key, F] : fills)
-        if (key.second == i && key.first != i) C.add(F.rows());
+      for (const DMat* F : FI.by_col[i]) C.add(F->rows());
       for (int64_t t = 0; t < S.nfar(L, i); ++t) C.add(int(rs(L, S.far(L, i)[t])));
       for (auto [l2, I] : ancestor_far_partners(L, i)) C.add(int(rs(l2, I)));
     }
@@ -451,11 +477,10 @@ struct Driver {
                               EvalBatch& eb) {
       for (int64_t i = k0; i < k1; ++i) {
         int off = 0;
-        for (auto& [key, F] : fills)
-          if (key.first == i && key.second != i) {
-            cb.copy(R[i].slice(off, F.cols()), F.m);
-            off += F.cols();
-          }
+        for (const DMat* F : FI.by_row[i]) {
+          cb.copy(R[i].slice(off, F->cols()), F->m);
+          off += F->cols();
+        }
         for (int64_t t = 0; t < S.nfar(L, i); ++t) {
           const int64_t j = S.far(L, i)[t];
           eb.add(R[i].slice(off, int(rs(L, j))), rb(L, i), rb(L, j));
@@ -474,6 +499,7 @@ struct Driver {
       // Provisional row bases (compression.cpp:203-211), kept as Qs_p.
       std::vector<Members> prow = rows;
       std::vector<DMat> provQs(m);
+      CopyBatch provcopies;
       run_bases(prow, nullptr,
                 [&](int64_t k0, int64_t k1) {
                   CopyBatch cb;
@@ -485,9 +511,11 @@ struct Driver {
                 [&](int64_t p, const Mat& q, int r, const Mat&, int) {
                   provR[p] = r;
                   provQs[p] = alloc_mat(c, sys.dims[p], r);
-                  CopyBatch cb;
-                  if (r > 0) cb.copy(provQs[p].m, q.sub(0, 0, sys.dims[p], r));
-                  cb.run(c);
+                  if (r > 0) provcopies.copy(provQs[p].m, q.sub(0, 0, sys.dims[p], r));
+                },
+                [&]() {
+                  provcopies.run(c);
+                  provcopies.jobs.clear();
                 });
       // X_p = A_pp^-1 Qs_p; coupling member A_ip X_p for p in near(i).
       SolveBatch sb;
@@ -517,11 +545,10 @@ struct Driver {
                 for (int64_t j = k0; j < k1; ++j) {
                   Members& C = cols[j];
                   int off = 0;
-                  for (auto& [key, F] : fills)
-                    if (key.second == j && key.first != j) {
-                      cb.copy(C.slice(off, F.rows()).t(), F.m);
-                      off += F.rows();
-                    }
+                  for (const DMat* F : FI.by_col[j]) {
+                    cb.copy(C.slice(off, F->rows()).t(), F->m);
+                    off += F->rows();
+                  }
                   for (int64_t t = 0; t < S.nfar(L, j); ++t) {
                     const int64_t i = S.far(L, j)[t];
                     eb.add(C.slice(off, int(rs(L, i))).t(), rb(L, i), rb(L, j));
@@ -538,6 +565,8 @@ struct Driver {
               },
               [&](int64_t k, const Mat& qu, int ru, const Mat& qv, int rv) {
                 square_sink(P.U[L], P.V[L], sqcopies)(k, qu, ru, qv, rv);
+              },
+              [&]() {
                 sqcopies.run(c);
                 sqcopies.jobs.clear();
               });
@@ -812,13 +841,12 @@ struct Driver {
     const int lvl = sys.lvl;
     const int64_t m = sys.m;
     std::vector<Members> rows(m), cols(m);
+    const FillIndex FI = index_fills(fills, m);
     for (int64_t k = 0; k < m; ++k) {
       rows[k].dim = cols[k].dim = sys.dims[k];
-      for (auto& [key, F] : fills)
-        if (key.first == k && key.second != k) rows[k].add(F.cols());
+      for (const DMat* F : FI.by_row[k]) rows[k].add(F->cols());
       for (auto& [tk, piece] : merged[k]) rows[k].add(piece.cols());
-      for (auto& [key, F] : fills)
-        if (key.second == k && key.first != k) cols[k].add(F.rows());
+      for (const DMat* F : FI.by_col[k]) cols[k].add(F->rows());
       for (int64_t t = 0; t < S.nfar(lvl, k); ++t) cols[k].add(sys.dims[S.far(lvl, k)[t]]);
       for (auto [l2, I] : ancestor_far_partners(lvl, k)) cols[k].add(int(rs(l2, I)));
     }
@@ -832,21 +860,19 @@ struct Driver {
                 GemmBatch gb;
                 for (int64_t k = k0; k < k1; ++k) {
                   int off = 0;
-                  for (auto& [key, F] : fills)
-                    if (key.first == k && key.second != k) {
-                      cb.copy(rows[k].slice(off, F.cols()), F.m);
-                      off += F.cols();
-                    }
+                  for (const DMat* F : FI.by_row[k]) {
+                    cb.copy(rows[k].slice(off, F->cols()), F->m);
+                    off += F->cols();
+                  }
                   for (auto& [tk, piece] : merged[k]) {
                     cb.copy(rows[k].slice(off, piece.cols()), piece.m);
                     off += piece.cols();
                   }
                   off = 0;
-                  for (auto& [key, F] : fills)
-                    if (key.second == k && key.first != k) {
-                      cb.copy(cols[k].slice(off, F.rows()).t(), F.m);
-                      off += F.rows();
-                    }
+                  for (const DMat* F : FI.by_col[k]) {
+                    cb.copy(cols[k].slice(off, F->rows()).t(), F->m);
+                    off += F->rows();
+                  }
                   for (int64_t t = 0; t < S.nfar(lvl, k); ++t) {
                     const int64_t i = S.far(lvl, k)[t];
                     const Mat piece = merged[i].at({lvl, k}).m;
@@ -870,6 +896,8 @@ struct Driver {
               },
               [&](int64_t k, const Mat& qu, int ru, const Mat& qv, int rv) {
                 square_sink(P.U[lvl], P.V[lvl], sqcopies)(k, qu, ru, qv, rv);
+              },
+              [&]() {
                 sqcopies.run(c);
                 sqcopies.jobs.clear();
               });

@@ -10,6 +10,18 @@ for n, leaf, geom in [(int(a), int(b), c) for a, b, c in (x.split(':') for x in 
     p = h2.Problem()
     p.set_kernel('yukawa', 1.0, 1.0, 1e-3)
     p.set_options(tol=float(__import__('os').environ.get('TOL', '1e-6')), cap=100)
+    warm = int(__import__('os').environ.get('WARM', '0'))
+    try:
+        for _ in range(warm):  # grow the device memory pool before the measured run
+            pw = h2.Problem()
+            pw.set_kernel('yukawa', 1.0, 1.0, 1e-3)
+            pw.set_options(tol=float(__import__('os').environ.get('TOL', '1e-6')), cap=100)
+            pw.build(xyz, q, leaf)
+            pw.factor()
+            pw.close()
+    except h2.H2GError as e:
+        print(n, leaf, geom, 'factor error:', e, flush=True)
+        continue
     p.set_profile(True)
     t = time.time(); p.build(xyz, q, leaf); tb = time.time() - t
     t = time.time()
