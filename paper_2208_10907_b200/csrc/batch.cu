@@ -113,6 +113,26 @@ Ctx::~Ctx() {
   // The owner may already have destroyed the stream; cudaFreeHost waits for
   // the device itself.
   if (pin) cudaFreeHost(pin);
+  for (auto s : sides) cudaStreamDestroy(s);
+  for (auto e : evs) cudaEventDestroy(e);
+}
+
+cudaStream_t Ctx::side_stream(int i) {
+  while (int(sides.size()) <= i) {
+    cudaStream_t s = nullptr;
+    cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "side stream");
+    sides.push_back(s);
+  }
+  return sides[i];
+}
+
+cudaEvent_t Ctx::event(int i) {
+  while (int(evs.size()) <= i) {
+    cudaEvent_t e = nullptr;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    evs.push_back(e);
+  }
+  return evs[i];
 }
 
 void Ctx::sync() {
@@ -533,6 +553,31 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
       fl += 2.0 * it.m * double(it.n);  // column norms
     }
     c.add_flops(fl);
+    // Launch plan: one cluster size for the batch (qr_cluster_size), the
+    // largest bases first so later waves hold the short ones. (Giving spare
+    // CTAs of a single wave to the largest bases, as concurrent launches of
+    // mixed cluster sizes, was measured slower: mixed clusters pack worse.)
+    std::vector<int> G(jobs.size(), 1);
+    {
+      const char* ecl = getenv("H2G_QR_CLUSTER");
+      auto work = [&](const QrJob& j) { return double(j.m) * j.n; };
+      std::fill(G.begin(), G.end(),
+                ecl ? std::max(1, std::min(8, atoi(ecl)))
+                    : qr_cluster_size(int(jobs.size()), min_n, max_m, max_nmem));
+      std::vector<size_t> ord(jobs.size());
+      for (size_t q = 0; q < ord.size(); ++q) ord[q] = q;
+      std::stable_sort(ord.begin(), ord.end(), [&](size_t x, size_t y) {
+        return G[x] != G[y] ? G[x] > G[y] : work(jobs[x]) > work(jobs[y]);
+      });
+      std::vector<QrJob> js(jobs.size());
+      std::vector<int> gs(jobs.size());
+      for (size_t q = 0; q < ord.size(); ++q) {
+        js[q] = jobs[ord[q]];
+        gs[q] = G[ord[q]];
+      }
+      jobs.swap(js);
+      G.swap(gs);
+    }
     Slab kdbg;
     double* ddbg = nullptr;
     if (getenv("H2G_QR_DEBUG")) {
@@ -544,21 +589,52 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
     Slab kj;
     auto* dj = upload(c, jobs, kj);
     auto ev = c.prof_begin();
-    const int cl = getenv("H2G_QR_CLUSTER") ? atoi(getenv("H2G_QR_CLUSTER"))
-                                            : qr_cluster_size(int(jobs.size()), min_n, max_m, max_nmem);
+    cudaEvent_t dbg_a = nullptr, dbg_b = nullptr;
+    if (ddbg) {
+      cudaEventCreate(&dbg_a);
+      cudaEventCreate(&dbg_b);
+      cudaEventRecord(dbg_a, c.stream);
+    }
+    const int cl = G.empty() ? 1 : G[0];
     launch_qr(dj, int(jobs.size()), max_m, max_nmem, cl, c.stream);
     if (ddbg) {
+      cudaEventRecord(dbg_b, c.stream);
+      cudaEventSynchronize(dbg_b);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, dbg_a, dbg_b);
+      cudaEventDestroy(dbg_a);
+      cudaEventDestroy(dbg_b);
+      int gh[10] = {0};
+      for (int g : G) ++gh[g];
+      fprintf(stderr, "QRDBG launch %.1f ms, clusters by size:", ms);
+      for (int g = 1; g <= 8; ++g)
+        if (gh[g]) fprintf(stderr, " %dx%d", gh[g], g);
+      fprintf(stderr, "\n");
       std::vector<double> h(16 * jobs.size());
       cudaMemcpyAsync(h.data(), ddbg, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c.stream);
       cudaStreamSynchronize(c.stream);
-      double a[12] = {0};
+      double a[14] = {0};
       for (size_t q = 0; q < jobs.size(); ++q)
-        for (int u = 0; u < 12; ++u) a[u] += h[16 * q + u];
+        for (int u = 0; u < 14; ++u) a[u] += h[16 * q + u];
       fprintf(stderr, "QRDBG jobs=%zu avg: piv %.3g refl %.3g tile %.3g mem %.3g rank %.1f n %.0f formq %.3g (cycles)\n",
               jobs.size(), a[0] / jobs.size(), a[1] / jobs.size(), a[2] / jobs.size(), a[3] / jobs.size(),
               a[4] / jobs.size(), a[5] / jobs.size(), a[6] / jobs.size());
-      fprintf(stderr, "QRDBG   warp0 per tile: wait %.0f chain %.0f store %.0f tiles %.0f\n",
-              a[8] / a[11], a[9] / a[11], a[10] / a[11], a[11] / jobs.size());
+      {
+        double mx = 0, sum = 0, wmx = 0, wsum = 0;
+        size_t qm = 0;
+        for (size_t q = 0; q < jobs.size(); ++q) {
+          const double tot = h[16 * q] + h[16 * q + 1] + h[16 * q + 2] + h[16 * q + 3] + h[16 * q + 6];
+          sum += tot;
+          if (tot > mx) { mx = tot; qm = q; }
+          const double w = double(jobs[q].m) * jobs[q].n;
+          wsum += w;
+          wmx = std::max(wmx, w);
+        }
+        fprintf(stderr, "QRDBG   G=%d job cycles max %.3g mean %.3g (max job m=%d n=%d rank %.0f); m*n max/mean %.2f\n",
+                cl, mx, sum / jobs.size(), jobs[qm].m, jobs[qm].n, h[16 * qm + 4], wmx / (wsum / jobs.size()));
+      }
+      fprintf(stderr, "QRDBG   warp0 per tile: wait %.0f chain %.0f store %.0f tiles %.0f; lane0 norm recomputes %.4f of chains\n",
+              a[8] / a[11], a[9] / a[11], a[10] / a[11], a[11] / jobs.size(), a[12] / (a[13] > 0 ? a[13] : 1));
     }
     c.prof_end("qr", ev, 0.0, 0.0);
     qr_recs.push_back({c.prof ? c.prec.size() - 1 : size_t(-1), t0, t1});

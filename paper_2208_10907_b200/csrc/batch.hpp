@@ -46,6 +46,12 @@ struct Ctx {
   Ctx(const Ctx&) = delete;
   Ctx& operator=(const Ctx&) = delete;
   ~Ctx();
+  // Side streams (fork/join from `stream` with the pooled events) for
+  // independent launches that should run concurrently.
+  std::vector<cudaStream_t> sides;
+  std::vector<cudaEvent_t> evs;
+  cudaStream_t side_stream(int i);
+  cudaEvent_t event(int i);
   void sync();            // stream sync + error word check
   void check_err();       // throws the reference's message for device errors
   std::vector<std::string> lu_names;  // current LU batch names (for errors)

@@ -21,6 +21,7 @@ void cuda_check(cudaError_t e, const char* what);  // batch.cu
 namespace {
 
 constexpr int NT = 128;
+constexpr int NBUF = 3;  // max column tiles in flight per warp in the sweep
 
 // The reference's reductions as GCC -O3 -mavx2 -mfma compiles them
 // (linalg.cpp; disassembly of oracle/_ref, verified bit-exact on random
@@ -152,9 +153,6 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 }
 
 
-__device__ __forceinline__ void st_global16(double* p, double x, double y) {
-  asm volatile("st.global.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(x), "d"(y));
-}
 
 // red_h (above) over a shared-memory column against v, streamed as 16-byte
 // pairs: element t is col[off + t] * vb[off + t], t < tc, with col and vb
@@ -244,6 +242,23 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+// Shared -> global bulk copy (TMA engine) in this thread's bulk async-group.
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+// All but the newest N bulk groups of this thread have finished reading shared memory.
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+// Every bulk group of this thread complete; its global writes ordered before
+// this thread's later generic accesses (and the cluster barrier's release).
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;\nfence.proxy.async.global;\n" ::: "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -347,14 +362,14 @@ struct ClSlots {
 //
 // Dynamic shared memory: [ v (m) | member masses (nmem) | D (2 kmax ints) | column tiles ].
 __global__ void __launch_bounds__(NT, 1) qr_kernel(const QrJob* __restrict__ jobs, int tile_doubles,
-                                                   int nmem_cap, int m_cap) {
+                                                   int nmem_cap, int m_cap, int nbuf) {
   extern __shared__ __align__(16) double dsm[];
   __shared__ double redd[32];
   __shared__ int redi[32];
   __shared__ double sh_tau;
   __shared__ int sh_nd;
   __shared__ ClSlots slot;
-  __shared__ __align__(8) uint64_t wbar[NT / 32];
+  __shared__ __align__(8) uint64_t wbar[NBUF * (NT / 32)];
   cg::cluster_group cluster = cg::this_cluster();
   const int G = int(cluster.num_blocks());
   const int cr = int(cluster.block_rank());
@@ -377,10 +392,10 @@ __global__ void __launch_bounds__(NT, 1) qr_kernel(const QrJob* __restrict__ job
   if (job.cap > 0 && job.cap < kmax) kmax = job.cap;
   const bool lead = cr == 0;
   const int nloc = own.below(n);
-  if (tid < NT / 32) mbar_init(&wbar[tid], 1);
+  if (tid < NBUF * (NT / 32)) mbar_init(&wbar[tid], 1);
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncthreads();
-  unsigned wpar = 0;  // phase parity of this warp's barrier
+  unsigned wpar = 0;  // bit b: phase parity of this warp's buffer-b barrier
 
   // R = A (skipped when factoring in place): own columns.
   if (!(job.A.p == W && job.A.rs == 1 && job.A.cs == ldw)) {
@@ -452,7 +467,7 @@ __global__ void __launch_bounds__(NT, 1) qr_kernel(const QrJob* __restrict__ job
   int rank = 0;
   int nd = 0;  // length of the displaced-position list D
   long long t_piv = 0, t_refl = 0, t_tile = 0, t_mem = 0, t0c;
-  long long t_w = 0, t_c = 0, t_s = 0, n_t = 0;
+  long long t_w = 0, t_c = 0, t_s = 0, n_t = 0, n_rc = 0, n_ch = 0;
   for (int k = 0; k < kmax; ++k) {
     t0c = clock64();
     // Pivot: cluster-wide max of the remaining norms (each CTA's max was
@@ -581,10 +596,12 @@ __global__ void __launch_bounds__(NT, 1) qr_kernel(const QrJob* __restrict__ job
       const int np = (m - k0 + 1) >> 1;  // pairs per segment
       const int P = (np & 1) ? 2 * np : 2 * np + 2;
       const int per_warp = (tile_doubles / NW) & ~1;
-      const int cw = max(1, min(32, per_warp / P));
+      // NBUF column tiles per warp: tile t's chain runs while tiles t+1 and
+      // t+2 load and tile t-1's bulk stores drain.
+      const int cw = max(1, min(32, per_warp / (nbuf * P)));
       double* Tw = T + warp * per_warp;
-      // Store pairs start at k1 = (k + 1) rounded down to even: row k (R's
-      // final row k, never read again) may be rewritten with its own value.
+      // Store pairs start at k1 = (k + 1) rounded down to even: row k is
+      // R's final row k (rkj), stored with its updated value.
       const int k1 = (k + 1) & ~1;
       const int nps = (m - k1 + 1) >> 1;
       const double* vb = vsh + k0;
@@ -595,65 +612,70 @@ __global__ void __launch_bounds__(NT, 1) qr_kernel(const QrJob* __restrict__ job
         vr[u] = p < nps ? *reinterpret_cast<const double2*>(vsh + k1 + 2 * p) : make_double2(0.0, 0.0);
       }
       const int l0 = own.below(k + 1);
+      const int stride = NW * cw;
+      const int a0 = l0 + warp * cw;
+      const int ntile = a0 < nloc ? (nloc - a0 + stride - 1) / stride : 0;
       // Tile loads: one bulk copy per column (lane c issues column c) on the
-      // warp's mbarrier; lane 0 arms it with the tile's byte count first.
+      // buffer's mbarrier; lane 0 arms it with the tile's byte count first.
+      // Lane c also issues column c's bulk store, so the slot a lane reloads
+      // is only ever read by its own earlier store (wait_group.read).
       const unsigned colbytes = unsigned(16 * np);
-      auto load_tile = [&](int abase, int cnt) {
-        if (lane == 0) mbar_expect_tx(&wbar[warp], colbytes * unsigned(cnt));
+      auto load_tile = [&](int t) {
+        const int b = t % nbuf, abase = a0 + t * stride, cnt = min(cw, nloc - abase);
+        if (lane == 0) mbar_expect_tx(&wbar[warp * NBUF + b], colbytes * unsigned(cnt));
         __syncwarp();
         if (lane < cnt) {
           fence_proxy_async();
-          bulk_load(Tw + lane * P, W + int64_t(own.l2g(abase + lane)) * ldw + k0, colbytes, &wbar[warp]);
+          bulk_load(Tw + (b * cw + lane) * P, W + int64_t(own.l2g(abase + lane)) * ldw + k0, colbytes,
+                    &wbar[warp * NBUF + b]);
         }
       };
-      int a = l0 + warp * cw;
-      if (a < nloc) load_tile(a, min(cw, nloc - a));
-      for (; a < nloc; a += NW * cw) {
+      // Tiles loaded ahead: nbuf - 1 (the buffer reloaded at the end of
+      // iteration t held tile t - 1), or 1 with a single buffer (tile t's own).
+      const int ahead = nbuf == 1 ? 1 : nbuf - 1;
+      for (int t = 0; t < ahead && t < ntile; ++t) load_tile(t);
+      for (int t = 0; t < ntile; ++t) {
+        const int b = t % nbuf, a = a0 + t * stride;
         const int tw = min(cw, nloc - a);
+        double* Tb = Tw + b * cw * P;
         long long c0 = clock64();
-        mbar_wait(&wbar[warp], wpar);
-        wpar ^= 1u;
+        mbar_wait(&wbar[warp * NBUF + b], (wpar >> b) & 1u);
+        wpar ^= 1u << b;
         long long c1 = clock64();
         double sc = 0.0;
         int jl = 0;
+        bool need_rc = false;
         if (lane < tw) {
           jl = own.l2g(a + lane);
           const double cn2j = S.cn2[jl], cn2oj = S.cn2o[jl];  // in flight during the chain
-          const double* col = Tw + lane * P;
+          const double* col = Tb + lane * P;
           if (tau != 0.0) sc = -(tau * dot_h_pairs(col, vb, off, rows));
           // GCC computes rkj*rkj once (rounded) for the norm and member downdates.
           const double rkj = tau != 0.0 ? fma(sc, vsh[k], col[off]) : col[off];
           const double sq = rkj * rkj;
-          double upd = cn2j - sq;
-          if (upd < 1e-8 * cn2oj)
-            upd = red_p2(
-                [&](int r, double& x, double& y) {
-                  x = y = tau != 0.0 ? fma(sc, vsh[k + r], col[off + r]) : col[off + r];
-                },
-                1, rows - 1);
-          const double nc = fmax(0.0, upd);
-          S.cn2[jl] = nc;
+          const double upd = cn2j - sq;
+          ++n_ch;
           S.sq[jl] = sq;
-          lmax = fmax(lmax, nc);
+          // Cancellation: the norm is recomputed from the updated column
+          // (linalg.cpp:300-311) after the update, overlapping the stores.
+          need_rc = upd < 1e-8 * cn2oj;
+          if (!need_rc) {
+            const double nc = fmax(0.0, upd);
+            S.cn2[jl] = nc;
+            lmax = fmax(lmax, nc);
+          }
         }
         __syncwarp();
         long long c2 = clock64();
-        const int an = a + NW * cw;
-        const int twn = an < nloc ? min(cw, nloc - an) : 0;
-        // Update + store, two columns per pass: the stores carry no memory
-        // clobber, so the next column's shared loads issue ahead of them.
-        // The slots are refilled only after every lane's reads (syncwarp).
+        // Update in place in shared memory, warp-wide (two columns per pass),
+        // then one bulk store per column straight from the slot.
         if (tau != 0.0) {
           for (int c = 0; c < tw; c += 2) {
             const bool two = c + 1 < tw;
             const double s_0 = __shfl_sync(0xffffffffu, sc, c);
-            const int j_0 = __shfl_sync(0xffffffffu, jl, c);
             const double s_1 = __shfl_sync(0xffffffffu, sc, two ? c + 1 : c);
-            const int j_1 = __shfl_sync(0xffffffffu, jl, two ? c + 1 : c);
-            const double* col0 = Tw + c * P + (k1 - k0);
-            const double* col1 = col0 + P;
-            double* dst0 = W + int64_t(j_0) * ldw + k1;
-            double* dst1 = W + int64_t(j_1) * ldw + k1;
+            double* col0 = Tb + c * P + (k1 - k0);
+            double* col1 = col0 + P;
             if (nps <= 128) {
               double2 x0[4], x1[4];
 #pragma unroll
@@ -667,29 +689,52 @@ __global__ void __launch_bounds__(NT, 1) qr_kernel(const QrJob* __restrict__ job
               for (int u = 0; u < 4; ++u) {
                 const int p = lane + 32 * u;
                 if (p < nps) {
-                  st_global16(dst0 + 2 * p, fma(s_0, vr[u].x, x0[u].x), fma(s_0, vr[u].y, x0[u].y));
+                  *reinterpret_cast<double2*>(col0 + 2 * p) =
+                      make_double2(fma(s_0, vr[u].x, x0[u].x), fma(s_0, vr[u].y, x0[u].y));
                   if (two)
-                    st_global16(dst1 + 2 * p, fma(s_1, vr[u].x, x1[u].x), fma(s_1, vr[u].y, x1[u].y));
+                    *reinterpret_cast<double2*>(col1 + 2 * p) =
+                        make_double2(fma(s_1, vr[u].x, x1[u].x), fma(s_1, vr[u].y, x1[u].y));
                 }
               }
             } else {
               for (int p = lane; p < nps; p += 32) {
                 const double2 v = *reinterpret_cast<const double2*>(vsh + k1 + 2 * p);
                 const double2 x = *reinterpret_cast<const double2*>(col0 + 2 * p);
-                st_global16(dst0 + 2 * p, fma(s_0, v.x, x.x), fma(s_0, v.y, x.y));
+                *reinterpret_cast<double2*>(col0 + 2 * p) = make_double2(fma(s_0, v.x, x.x), fma(s_0, v.y, x.y));
                 if (two) {
                   const double2 y = *reinterpret_cast<const double2*>(col1 + 2 * p);
-                  st_global16(dst1 + 2 * p, fma(s_1, v.x, y.x), fma(s_1, v.y, y.y));
+                  *reinterpret_cast<double2*>(col1 + 2 * p) = make_double2(fma(s_1, v.x, y.x), fma(s_1, v.y, y.y));
                 }
               }
             }
           }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane < tw) bulk_store(W + int64_t(jl) * ldw + k1, Tb + lane * P + (k1 - k0), unsigned(16 * nps));
+          bulk_commit();
         }
+        // Deferred norm recomputes: rows k+1.. of the updated column, read
+        // from the slot while the bulk stores drain it (both only read).
+        if (need_rc) {
+          ++n_rc;
+          const double* col = Tb + lane * P;
+          const double nc = fmax(0.0, red_p2([&](int r, double& x, double& y) { x = y = col[off + r]; }, 1, rows - 1));
+          S.cn2[jl] = nc;
+          lmax = fmax(lmax, nc);
+        }
+        // Tile t-1's buffer is reloaded next: its stores must have read it.
+        if (nbuf == 1)
+          bulk_wait_read<0>();
+        else
+          bulk_wait_read<1>();
         __syncwarp();
-        if (twn > 0) load_tile(an, twn);
+        if (t + ahead < ntile) load_tile(t + ahead);
         long long c3 = clock64();
         t_w += c1 - c0; t_c += c2 - c1; t_s += c3 - c2; ++n_t;
       }
+      // Every store complete (and visible) before the cluster barrier: the
+      // next step's swap and reflector read these columns from other CTAs.
+      bulk_wait_all();
     }
     {
       const double mx = block_max(lmax, redd);
@@ -759,6 +804,7 @@ __global__ void __launch_bounds__(NT, 1) qr_kernel(const QrJob* __restrict__ job
     job.dbg[0] = double(t_piv); job.dbg[1] = double(t_refl); job.dbg[2] = double(t_tile);
     job.dbg[3] = double(t_mem); job.dbg[4] = double(rank); job.dbg[5] = double(n);
     job.dbg[8] = double(t_w); job.dbg[9] = double(t_c); job.dbg[10] = double(t_s); job.dbg[11] = double(n_t);
+    job.dbg[12] = double(n_rc); job.dbg[13] = double(n_ch);
   }
   long long tq = clock64();
 
@@ -814,8 +860,8 @@ size_t qr_smem_bytes(int max_m, int max_nmem, size_t* tile_doubles) {
   }();
   const size_t fixed = qr_fixed_doubles(max_m, max_nmem);
   size_t tile = budget / sizeof(double) > fixed + 1024 ? budget / sizeof(double) - fixed : 1024;
-  // Every warp needs at least one column slot (pitch <= max_m + 4).
-  const size_t min_tile = size_t(NT / 32) * size_t(max_m + 4);
+  // Every warp needs at least one column slot per buffer (pitch <= max_m + 4).
+  const size_t min_tile = size_t(NT / 32) * NBUF * size_t(max_m + 4);
   if (tile < min_tile) tile = min_tile;
   if (tile_doubles) *tile_doubles = tile;
   return (fixed + tile) * sizeof(double);
@@ -862,36 +908,50 @@ void launch_qr(const QrJob* jobs, int njobs, int max_m, int max_nmem, int cluste
   const size_t smem = qr_smem_bytes(max_m, max_nmem, &tile);
   cudaLaunchAttribute at[1];
   cudaLaunchConfig_t cfg = qr_config(njobs, cluster, smem, st, at);
-  cudaLaunchKernelEx(&cfg, qr_kernel, jobs, int(tile), max_nmem, max_m);
+  static const int nbuf = [] {
+    const char* e = getenv("H2G_QR_NBUF");
+    return e ? std::max(1, std::min(NBUF, atoi(e))) : 1;
+  }();
+  cudaLaunchKernelEx(&cfg, qr_kernel, jobs, int(tile), max_nmem, max_m, nbuf);
+}
+
+// Clusters of g CTAs that can be co-resident (occupancy API, GPC packing
+// included), cached per (g, shared-memory size).
+int qr_fit(int g, int max_m, int max_nmem) {
+  qr_attr();
+  const size_t smem = qr_smem_bytes(max_m, max_nmem, nullptr);
+  static int cache_key[9] = {0};
+  static int cache_val[9] = {0};
+  if (g < 1 || g > 8) return 0;
+  if (cache_key[g] == int(smem)) return cache_val[g];
+  int fit = 0;
+  cudaLaunchAttribute at[1];
+  cudaLaunchConfig_t cfg = qr_config(g, g, smem, nullptr, at);
+  if (cudaOccupancyMaxActiveClusters(&fit, qr_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    fit = 0;
+  }
+  cache_key[g] = int(smem);
+  cache_val[g] = fit;
+  return fit;
+}
+
+int qr_max_cluster(int n) {
+  int g = 1;
+  while (g < 8 && n >= 2 * CB * (g + 1)) ++g;
+  return g;
 }
 
 int qr_cluster_size(int njobs, int min_n, int max_m, int max_nmem) {
   // A basis is a ~100-step sequential sweep, so the batch runs in waves of
   // co-resident clusters. Pick the cluster size g (CTAs per basis) that
   // minimises waves / g, using the occupancy API for how many clusters of
-  // size g fit at once (GPC packing included); every CTA must own at least
-  // two column blocks. Ties go to the smaller cluster.
-  qr_attr();
-  const size_t smem = qr_smem_bytes(max_m, max_nmem, nullptr);
-  static int cache_key[9] = {0};
-  static int cache_val[9] = {0};
+  // size g fit at once; every CTA must own at least two column blocks. Ties
+  // go to the smaller cluster.
   int best = 1;
   double best_cost = 1e30;
-  for (int g = 1; g <= 8; ++g) {
-    if (g > 1 && min_n < 2 * CB * g) break;
-    int fit = 0;
-    if (cache_key[g] == int(smem)) {
-      fit = cache_val[g];
-    } else {
-      cudaLaunchAttribute at[1];
-      cudaLaunchConfig_t cfg = qr_config(g, g, smem, nullptr, at);
-      if (cudaOccupancyMaxActiveClusters(&fit, qr_kernel, &cfg) != cudaSuccess) {
-        cudaGetLastError();
-        fit = 0;
-      }
-      cache_key[g] = int(smem);
-      cache_val[g] = fit;
-    }
+  for (int g = 1; g <= qr_max_cluster(min_n); ++g) {
+    const int fit = qr_fit(g, max_m, max_nmem);
     if (fit <= 0) continue;
     const int waves = (njobs + fit - 1) / fit;
     const double cost = double(waves) / g * (1.0 + 0.02 * (g - 1));

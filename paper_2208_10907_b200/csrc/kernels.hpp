@@ -161,6 +161,9 @@ void launch_qr(const QrJob* jobs, int njobs, int max_m, int max_nmem, int cluste
                cudaStream_t st);
 // CTAs per basis (thread-block cluster size) for a batch of njobs bases.
 int qr_cluster_size(int njobs, int min_n, int max_m, int max_nmem);
+// Co-resident clusters of g CTAs; largest cluster a basis of n columns uses.
+int qr_fit(int g, int max_m, int max_nmem);
+int qr_max_cluster(int n);
 size_t qr_scratch_doubles(int m, int n, int nmem);
 
 }  // namespace h2g
