@@ -103,6 +103,24 @@ int h2g_kernel_stats(h2g_problem* p, int idx, char* name, int name_len, double* 
  * (replaces matvec_dense_oracle, solve.cpp:234-239, without its N guard). */
 int h2g_matvec(h2g_problem* p, int64_t nrhs, const double* x, double* y);
 
+/* ---- multi-GPU level partition (one process per GPU) ----
+ * The reference has no multi-process path (its MPI plan is offline only,
+ * partition_plan_json, report.cpp:245-296); these follow that plan: rank r of
+ * P owns the contiguous box range [m r / P, m (r+1) / P) of every level with
+ * m >= P boxes, coarser levels are replicated. The partitioned stages (basis
+ * construction: member concats + pivoted QR) run only on owned boxes and
+ * all-gather their outputs, so every rank ends with the single-GPU factors,
+ * bit for bit. Set the communicator before h2g_factor. */
+int h2g_nccl_unique_id(void* id128); /* ncclGetUniqueId, 128 bytes (rank 0; broadcast it) */
+int h2g_set_comm_nccl(h2g_problem* p, int nranks, int rank, const void* id128);
+/* Host-mediated exchange (tests, or a host transport): called with a host
+ * buffer holding this rank's bytes [offs[rank], offs[rank+1]); must fill in
+ * the other ranks' segments (an all-gather-v); returns 0 on success. */
+typedef int (*h2g_host_allgather_fn)(void* user, void* host_buf, const int64_t* byte_offs, int nranks);
+int h2g_set_comm_host(h2g_problem* p, int nranks, int rank, h2g_host_allgather_fn fn, void* user);
+/* Box range [lo, hi) of an m-box level owned by rank (host logic, no GPU). */
+int h2g_partition_range(int64_t m, int nranks, int rank, int64_t* lo, int64_t* hi);
+
 /* ---- single-primitive entry points (kernel parity tests) ---- */
 /* lu_factor (linalg.cpp:352-388) on one n x n column-major block. */
 int h2g_lu_factor(int64_t n, const double* a, double tol, double* lu, int64_t* perm);

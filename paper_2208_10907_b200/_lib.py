@@ -37,7 +37,11 @@ EXPORTS = [
     "h2g_max_fill_residual", "h2g_stats", "h2g_matvec", "h2g_lu_factor",
     "h2g_basis_from_members", "h2g_lu_solve", "h2g_gemm", "h2g_stats_dev", "h2g_set_profile",
     "h2g_reset_profile", "h2g_kernel_stats", "h2g_set_stream", "h2g_phase_seconds",
+    "h2g_nccl_unique_id", "h2g_set_comm_nccl", "h2g_set_comm_host", "h2g_partition_range",
 ]
+
+# h2g_host_allgather_fn (include/h2g.h)
+HostAllgatherFn = ctypes.CFUNCTYPE(ctypes.c_int, P, P, ctypes.POINTER(i64), ctypes.c_int)
 
 
 def lib():
@@ -90,12 +94,59 @@ def lib():
         L.h2g_set_profile.argtypes = [P, ctypes.c_int]
         L.h2g_reset_profile.argtypes = [P]
         L.h2g_kernel_stats.argtypes = [P, ctypes.c_int, ctypes.c_char_p, ctypes.c_int, P, P, P, P]
+        L.h2g_nccl_unique_id.argtypes = [P]
+        L.h2g_set_comm_nccl.argtypes = [P, ctypes.c_int, ctypes.c_int, P]
+        L.h2g_set_comm_host.argtypes = [P, ctypes.c_int, ctypes.c_int, HostAllgatherFn, P]
+        L.h2g_partition_range.argtypes = [i64, ctypes.c_int, ctypes.c_int, P, P]
         _lib = L
     return _lib
 
 
 def _p(a):
     return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def partition_range(m, nranks, rank):
+    """Boxes [lo, hi) of an m-box level owned by rank (h2g_partition_range)."""
+    lo, hi = i64(), i64()
+    _check(lib().h2g_partition_range(m, nranks, rank, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
+def nccl_unique_id():
+    """128-byte ncclUniqueId (create on rank 0, broadcast to the others)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().h2g_nccl_unique_id(buf))
+    return buf.raw
+
+
+def gloo_allgather(group=None):
+    """A host all-gather-v callback over a torch.distributed (gloo) group, for
+    h2g_set_comm_host: the segments are padded to the longest and gathered."""
+    import torch
+    import torch.distributed as dist
+
+    def fn(user, host_buf, offs, nranks):
+        try:
+            o = [offs[r] for r in range(nranks + 1)]
+            sizes = [o[r + 1] - o[r] for r in range(nranks)]
+            me = dist.get_rank(group)
+            buf = (ctypes.c_uint8 * o[nranks]).from_address(host_buf)
+            arr = np.ctypeslib.as_array(buf)
+            mx = max(max(sizes), 1)
+            mine = torch.zeros(mx, dtype=torch.uint8)
+            mine[:sizes[me]] = torch.from_numpy(arr[o[me]:o[me + 1]].copy())
+            got = [torch.empty(mx, dtype=torch.uint8) for _ in range(nranks)]
+            dist.all_gather(got, mine, group=group)
+            for r in range(nranks):
+                if r != me and sizes[r]:
+                    arr[o[r]:o[r + 1]] = got[r][:sizes[r]].numpy()
+            return 0
+        except Exception:  # reported as a failed exchange by the library
+            import traceback
+            traceback.print_exc()
+            return 1
+    return fn
 
 
 def _check(rc):
@@ -227,6 +278,15 @@ class Problem:
 
     def set_stream(self, stream_ptr):
         _check(self.L.h2g_set_stream(self.h, stream_ptr))
+
+    def set_comm_nccl(self, nranks, rank, unique_id):
+        """Partition the factorization over nranks GPUs (one process each)."""
+        _check(self.L.h2g_set_comm_nccl(self.h, nranks, rank, ctypes.c_char_p(unique_id)))
+
+    def set_comm_host(self, nranks, rank, fn):
+        """Partition with a host all-gather-v callback (e.g. gloo_allgather())."""
+        self._comm_cb = HostAllgatherFn(fn)  # kept alive with the problem
+        _check(self.L.h2g_set_comm_host(self.h, nranks, rank, self._comm_cb, None))
 
     def stats_dev(self):
         t = np.zeros(3)

@@ -256,6 +256,43 @@ int h2g_set_stream(h2g_problem* p, void* stream) {
   });
 }
 
+int h2g_nccl_unique_id(void* id128) {
+  return guarded([&] { h2g::nccl_unique_id(id128); });
+}
+
+int h2g_set_comm_nccl(h2g_problem* p, int nranks, int rank, const void* id128) {
+  return guarded([&] {
+    if (p->P.factored) throw std::logic_error("h2g_set_comm: call before factor");
+    p->P.comm = nranks > 1 ? h2g::make_nccl_comm(nranks, rank, id128) : nullptr;
+  });
+}
+
+int h2g_set_comm_host(h2g_problem* p, int nranks, int rank, h2g_host_allgather_fn fn, void* user) {
+  return guarded([&] {
+    if (p->P.factored) throw std::logic_error("h2g_set_comm: call before factor");
+    p->P.comm = nranks > 1 ? h2g::make_host_comm(nranks, rank, fn, user) : nullptr;
+  });
+}
+
+int h2g_partition_range(int64_t m, int nranks, int rank, int64_t* lo, int64_t* hi) {
+  return guarded([&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks || m < 0)
+      throw std::invalid_argument("h2g_partition_range: bad arguments");
+    struct Plain : h2g::Comm {
+      void allgatherv(void*, const std::vector<int64_t>&, cudaStream_t) override {}
+    } c;
+    c.rank = rank;
+    c.size = nranks;
+    if (c.partitioned(m)) {
+      *lo = c.lo(m);
+      *hi = c.hi(m);
+    } else {
+      *lo = 0;
+      *hi = m;
+    }
+  });
+}
+
 int h2g_stats_dev(h2g_problem* p, double* t3) {
   t3[0] = p->P.stats.t_build_dev;
   t3[1] = p->P.stats.t_factor_dev;

@@ -359,7 +359,75 @@ struct Driver {
   void run_bases(std::vector<Members>& rows, std::vector<Members>* cols, const FillFn& fill,
                  const SinkFn& sink, const std::function<void()>& flush = {}) {
     const int64_t m = int64_t(rows.size());
-    int64_t k0 = 0;
+    if (P.comm && P.comm->partitioned(m))
+      run_bases_partitioned(rows, cols, fill, sink, flush);
+    else
+      run_bases_range(rows, cols, fill, sink, flush, 0, m);
+  }
+
+  // Multi-GPU: this rank builds and factors the concats of its own box range
+  // only; the Q's (and ranks) land in one box-ordered slab, so each owner's
+  // boxes are one contiguous segment, all-gathered in place; then every rank
+  // runs the sink for every box exactly as the single-GPU path does.
+  void run_bases_partitioned(std::vector<Members>& rows, std::vector<Members>* cols,
+                             const FillFn& fill, const SinkFn& sink,
+                             const std::function<void()>& flush) {
+    Comm& cm = *P.comm;
+    const int64_t m = int64_t(rows.size());
+    const int nq = cols ? 2 : 1;
+    std::vector<int64_t> qoff(m + 1, 0);
+    for (int64_t k = 0; k < m; ++k) qoff[k + 1] = qoff[k] + int64_t(nq) * rows[k].dim * rows[k].dim;
+    Slab qslab = c.alloc(sizeof(double) * size_t(std::max<int64_t>(qoff[m], 1)));
+    Slab rslab = c.alloc(sizeof(int) * size_t(nq * m));
+    double* qa = static_cast<double*>(qslab.get());
+    int* ra = static_cast<int*>(rslab.get());
+    auto qview = [&](int64_t k, int side) {
+      const int d = rows[k].dim;
+      return Mat{qa + qoff[k] + int64_t(side) * d * d, d, d, std::max(d, 1), 1};  // row-major like QrBatch
+    };
+    std::vector<int> rk(size_t(nq * m), 0);
+    CopyBatch qcopies;
+    run_bases_range(rows, cols, fill,
+                    [&](int64_t k, const Mat& qu, int ru, const Mat& qv, int rv) {
+                      if (rows[k].dim > 0) qcopies.copy(qview(k, 0), qu);
+                      rk[size_t(nq * k)] = ru;
+                      if (cols) {
+                        if (rows[k].dim > 0) qcopies.copy(qview(k, 1), qv);
+                        rk[size_t(nq * k + 1)] = rv;
+                      }
+                    },
+                    [&]() {
+                      qcopies.run(c);
+                      qcopies.jobs.clear();
+                    },
+                    cm.lo(m), cm.hi(m));
+    cuda_check(cudaMemcpyAsync(ra, c.stage(rk.data(), sizeof(int) * rk.size()), sizeof(int) * rk.size(),
+                               cudaMemcpyHostToDevice, c.stream),
+               "ranks h2d");
+    std::vector<int64_t> qb(cm.size + 1), rb(cm.size + 1);
+    for (int r = 0; r <= cm.size; ++r) {
+      const int64_t k = r == cm.size ? m : cm.lo(m, r);
+      qb[r] = int64_t(sizeof(double)) * qoff[k];
+      rb[r] = int64_t(sizeof(int)) * nq * k;
+    }
+    {
+      PhaseTimer pt(c, P.stats, "exchange");
+      cm.allgatherv(qa, qb, c.stream);
+      cm.allgatherv(ra, rb, c.stream);
+    }
+    cuda_check(cudaMemcpyAsync(rk.data(), ra, sizeof(int) * rk.size(), cudaMemcpyDeviceToHost, c.stream),
+               "ranks d2h");
+    c.sync();
+    for (int64_t k = 0; k < m; ++k)
+      sink(k, qview(k, 0), rk[size_t(nq * k)], cols ? qview(k, 1) : Mat{}, cols ? rk[size_t(nq * k + 1)] : 0);
+    if (flush) flush();
+  }
+
+  // Boxes [kb, ke): chunked concat fill -> in-place QR -> sink.
+  void run_bases_range(std::vector<Members>& rows, std::vector<Members>* cols, const FillFn& fill,
+                       const SinkFn& sink, const std::function<void()>& flush, int64_t kb, int64_t ke) {
+    const int64_t m = ke;
+    int64_t k0 = kb;
     while (k0 < m) {
       size_t bytes = 0;
       int64_t k1 = k0;

@@ -3,11 +3,13 @@
 // (ClusterTree, BlockStructure, HMatrix, SharedBasisSet, ULVFactors).
 #pragma once
 #include <map>
+#include <memory>
 #include <string>
 #include <utility>
 #include <vector>
 
 #include "batch.hpp"
+#include "comm.hpp"
 #include "tree.hpp"
 
 namespace h2g {
@@ -87,6 +89,10 @@ class Problem {
   std::vector<double> max_fill_resid;
   bool built = false, factored = false;
   bool auto_budget_ = true;
+  // Multi-GPU level partition (null: single GPU). The partitioned stages
+  // compute only this rank's box range and all-gather their outputs, so
+  // every rank ends with the single-GPU factors bit for bit.
+  std::unique_ptr<Comm> comm;
 
   Problem();
   ~Problem();
