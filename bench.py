@@ -15,9 +15,12 @@ and one right-hand-side solve. value = points / second of a step, timed with
 CUDA events on the stream every kernel of the step is launched on.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-Under torchrun each rank factorizes its own replica (seed 42 + rank; weak
-scaling, no data-path collective); the timed region is bracketed by a
-barrier + synchronize, and the max over ranks is reported.
+Under torchrun (N > 1) the N ranks factorize ONE problem together with the
+multi-GPU level partition (Morton-contiguous box ranges per rank, the
+partitioned basis stage all-gathers its outputs over NCCL; strong scaling,
+value = N_points / max-over-ranks time); --replicas instead gives each rank
+its own problem (seed 42 + rank, weak scaling, no collective). The timed
+region is bracketed by a barrier + synchronize.
 """
 import argparse
 import json
@@ -171,10 +174,17 @@ def run_b200_arm(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n = args.n or WORKLOAD["n"]
     leaf = WORKLOAD["leaf"]
-    xyz, q = make_points(n, 42 + rank)
+    partitioned = world > 1 and not args.replicas
+    comm = None
+    if partitioned:
+        uid = [h2.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(uid, src=0)
+        comm = h2.Comm.nccl(world, rank, uid[0])
+    seed = 42 if partitioned else 42 + rank
+    xyz, q = make_points(n, seed)
     d_xyz = torch.from_numpy(np.ascontiguousarray(xyz)).cuda()
     d_q = torch.from_numpy(np.ascontiguousarray(q)).cuda()
-    b = np.random.default_rng(7 + rank).uniform(-1.0, 1.0, n)
+    b = np.random.default_rng(7 if partitioned else 7 + rank).uniform(-1.0, 1.0, n)
     d_b = torch.from_numpy(b).cuda()
     d_x = torch.empty_like(d_b)
     stream = torch.cuda.Stream()
@@ -184,6 +194,8 @@ def run_b200_arm(args):
         p.set_stream(stream.cuda_stream)
         p.set_kernel("yukawa", WORKLOAD["alpha_m"], WORKLOAD["scale"], WORKLOAD["reg"])
         p.set_options(tol=WORKLOAD["tol"], cap=WORKLOAD["cap"], eta=WORKLOAD["eta"])
+        if comm is not None:
+            p.set_comm(comm)
         return p
 
     def step(p):
@@ -235,7 +247,8 @@ def run_b200_arm(args):
         tt = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t_max = float(tt.item())
-    value = n * world * args.steps / t_max
+    points = n if partitioned else n * world
+    value = points * args.steps / t_max
 
     # residual of the last solve through the matrix-free direct sum
     x = d_x.cpu().numpy()
@@ -253,6 +266,8 @@ def run_b200_arm(args):
         pe = h2.Problem()
         pe.set_kernel("yukawa", WORKLOAD["alpha_m"], WORKLOAD["scale"], WORKLOAD["reg"])
         pe.set_options(tol=WORKLOAD["tol"], cap=WORKLOAD["cap"], eta=WORKLOAD["eta"])
+        if comm is not None:
+            pe.set_comm(comm)
         pe.build(xyz, q, leaf)
         pe.factor()
         xe = pe.solve(b)
@@ -302,14 +317,16 @@ def run_b200_arm(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded Fibonacci-lattice sphere, seed 42+rank)",
-            "config": dict(WORKLOAD, n=n, parallelism=f"replica x{world}",
+            "scaling": "strong" if partitioned else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Fibonacci-lattice sphere, seed 42" + ("" if partitioned else "+rank") + ")",
+            "config": dict(WORKLOAD, n=n,
+                           parallelism=(f"box-partitioned x{world} (NCCL all-gather of bases)" if partitioned
+                                        else f"replica x{world}"),
                            l2="inputs larger than L2 (near-field arena and member panels are GBs)"),
             "phase_s_per_step": {k: v / args.steps for k, v in t_phase.items()},
             "factor_points_per_s": n / (sum(t_factor) / len(t_factor)),
             "solve_rel_residual": resid,
-            "e2e": {"value": n * world / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(8 * (4 * n + n)),
+            "e2e": {"value": points / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(8 * (4 * n + n)),
                     "d2h_bytes_per_step": int(8 * n)},
             "gpu_launches": launches,
             "roofline": roofline,
@@ -332,6 +349,8 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override N (testing only)")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: one independent problem per rank instead of one partitioned problem")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)

@@ -111,13 +111,19 @@ int h2g_matvec(h2g_problem* p, int64_t nrhs, const double* x, double* y);
  * construction: member concats + pivoted QR) run only on owned boxes and
  * all-gather their outputs, so every rank ends with the single-GPU factors,
  * bit for bit. Set the communicator before h2g_factor. */
+typedef struct h2g_comm h2g_comm;
 int h2g_nccl_unique_id(void* id128); /* ncclGetUniqueId, 128 bytes (rank 0; broadcast it) */
-int h2g_set_comm_nccl(h2g_problem* p, int nranks, int rank, const void* id128);
-/* Host-mediated exchange (tests, or a host transport): called with a host
- * buffer holding this rank's bytes [offs[rank], offs[rank+1]); must fill in
- * the other ranks' segments (an all-gather-v); returns 0 on success. */
+/* NCCL communicator over the node's GPUs (ncclCommInitRank; collective). */
+int h2g_comm_nccl(int nranks, int rank, const void* id128, h2g_comm** out);
+/* Host-mediated exchange (tests, or a host transport): fn is called with a
+ * host buffer holding this rank's bytes [offs[rank], offs[rank+1]) and must
+ * fill in the other ranks' segments (an all-gather-v); returns 0 on success. */
 typedef int (*h2g_host_allgather_fn)(void* user, void* host_buf, const int64_t* byte_offs, int nranks);
-int h2g_set_comm_host(h2g_problem* p, int nranks, int rank, h2g_host_allgather_fn fn, void* user);
+int h2g_comm_host(int nranks, int rank, h2g_host_allgather_fn fn, void* user, h2g_comm** out);
+void h2g_comm_destroy(h2g_comm* c); /* problems using it keep it alive */
+/* Partition this problem's factorization over the communicator's ranks
+ * (NULL: single GPU). Call before h2g_factor. */
+int h2g_set_comm(h2g_problem* p, h2g_comm* c);
 /* Box range [lo, hi) of an m-box level owned by rank (host logic, no GPU). */
 int h2g_partition_range(int64_t m, int nranks, int rank, int64_t* lo, int64_t* hi);
 

@@ -6,8 +6,9 @@ implemented by the in-tree sm_100a library libh2g.so. There is no CPU
 fallback: importing works anywhere, but every compute call raises if the
 library or a CUDA device is missing.
 """
-from ._lib import H2GError, Problem, lib, lib_path  # noqa: F401
+from ._lib import (Comm, H2GError, Problem, gloo_allgather, lib, lib_path,  # noqa: F401
+                   nccl_unique_id, partition_range)
 from .pipeline import RunConfig, Pipeline, make_cloud, run_pipeline  # noqa: F401
 
 __all__ = ["H2GError", "Problem", "RunConfig", "Pipeline", "make_cloud", "run_pipeline", "lib",
-           "lib_path"]
+           "lib_path", "Comm", "nccl_unique_id", "partition_range", "gloo_allgather"]

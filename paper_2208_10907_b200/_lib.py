@@ -37,7 +37,8 @@ EXPORTS = [
     "h2g_max_fill_residual", "h2g_stats", "h2g_matvec", "h2g_lu_factor",
     "h2g_basis_from_members", "h2g_lu_solve", "h2g_gemm", "h2g_stats_dev", "h2g_set_profile",
     "h2g_reset_profile", "h2g_kernel_stats", "h2g_set_stream", "h2g_phase_seconds",
-    "h2g_nccl_unique_id", "h2g_set_comm_nccl", "h2g_set_comm_host", "h2g_partition_range",
+    "h2g_nccl_unique_id", "h2g_comm_nccl", "h2g_comm_host", "h2g_comm_destroy", "h2g_set_comm",
+    "h2g_partition_range",
 ]
 
 # h2g_host_allgather_fn (include/h2g.h)
@@ -95,8 +96,10 @@ def lib():
         L.h2g_reset_profile.argtypes = [P]
         L.h2g_kernel_stats.argtypes = [P, ctypes.c_int, ctypes.c_char_p, ctypes.c_int, P, P, P, P]
         L.h2g_nccl_unique_id.argtypes = [P]
-        L.h2g_set_comm_nccl.argtypes = [P, ctypes.c_int, ctypes.c_int, P]
-        L.h2g_set_comm_host.argtypes = [P, ctypes.c_int, ctypes.c_int, HostAllgatherFn, P]
+        L.h2g_comm_nccl.argtypes = [ctypes.c_int, ctypes.c_int, P, ctypes.POINTER(P)]
+        L.h2g_comm_host.argtypes = [ctypes.c_int, ctypes.c_int, HostAllgatherFn, P, ctypes.POINTER(P)]
+        L.h2g_comm_destroy.argtypes = [P]
+        L.h2g_set_comm.argtypes = [P, P]
         L.h2g_partition_range.argtypes = [i64, ctypes.c_int, ctypes.c_int, P, P]
         _lib = L
     return _lib
@@ -118,6 +121,38 @@ def nccl_unique_id():
     buf = ctypes.create_string_buffer(128)
     _check(lib().h2g_nccl_unique_id(buf))
     return buf.raw
+
+
+class Comm:
+    """h2g_comm: the multi-GPU level partition's communicator (one per rank,
+    shared by any number of problems)."""
+
+    def __init__(self, h, cb=None):
+        self.h, self._cb = h, cb
+
+    @classmethod
+    def nccl(cls, nranks, rank, unique_id):
+        h = P()
+        _check(lib().h2g_comm_nccl(nranks, rank, ctypes.c_char_p(unique_id), ctypes.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def host(cls, nranks, rank, fn):
+        cb = HostAllgatherFn(fn)
+        h = P()
+        _check(lib().h2g_comm_host(nranks, rank, cb, None, ctypes.byref(h)))
+        return cls(h, cb)
+
+    def close(self):
+        if self.h:
+            lib().h2g_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def gloo_allgather(group=None):
@@ -279,14 +314,10 @@ class Problem:
     def set_stream(self, stream_ptr):
         _check(self.L.h2g_set_stream(self.h, stream_ptr))
 
-    def set_comm_nccl(self, nranks, rank, unique_id):
-        """Partition the factorization over nranks GPUs (one process each)."""
-        _check(self.L.h2g_set_comm_nccl(self.h, nranks, rank, ctypes.c_char_p(unique_id)))
-
-    def set_comm_host(self, nranks, rank, fn):
-        """Partition with a host all-gather-v callback (e.g. gloo_allgather())."""
-        self._comm_cb = HostAllgatherFn(fn)  # kept alive with the problem
-        _check(self.L.h2g_set_comm_host(self.h, nranks, rank, self._comm_cb, None))
+    def set_comm(self, comm):
+        """Partition the factorization over comm's ranks (None: single GPU)."""
+        self._comm = comm  # the callback (if any) stays alive with the problem
+        _check(self.L.h2g_set_comm(self.h, comm.h if comm is not None else None))
 
     def stats_dev(self):
         t = np.zeros(3)

@@ -13,6 +13,10 @@ struct h2g_problem {
   h2g::Problem P;
 };
 
+struct h2g_comm {
+  std::shared_ptr<h2g::Comm> c;
+};
+
 namespace {
 
 thread_local std::string g_err;
@@ -260,17 +264,20 @@ int h2g_nccl_unique_id(void* id128) {
   return guarded([&] { h2g::nccl_unique_id(id128); });
 }
 
-int h2g_set_comm_nccl(h2g_problem* p, int nranks, int rank, const void* id128) {
-  return guarded([&] {
-    if (p->P.factored) throw std::logic_error("h2g_set_comm: call before factor");
-    p->P.comm = nranks > 1 ? h2g::make_nccl_comm(nranks, rank, id128) : nullptr;
-  });
+int h2g_comm_nccl(int nranks, int rank, const void* id128, h2g_comm** out) {
+  return guarded([&] { *out = new h2g_comm{h2g::make_nccl_comm(nranks, rank, id128)}; });
 }
 
-int h2g_set_comm_host(h2g_problem* p, int nranks, int rank, h2g_host_allgather_fn fn, void* user) {
+int h2g_comm_host(int nranks, int rank, h2g_host_allgather_fn fn, void* user, h2g_comm** out) {
+  return guarded([&] { *out = new h2g_comm{h2g::make_host_comm(nranks, rank, fn, user)}; });
+}
+
+void h2g_comm_destroy(h2g_comm* c) { delete c; }
+
+int h2g_set_comm(h2g_problem* p, h2g_comm* c) {
   return guarded([&] {
     if (p->P.factored) throw std::logic_error("h2g_set_comm: call before factor");
-    p->P.comm = nranks > 1 ? h2g::make_host_comm(nranks, rank, fn, user) : nullptr;
+    p->P.comm = (c && c->c->size > 1) ? c->c : nullptr;
   });
 }
 

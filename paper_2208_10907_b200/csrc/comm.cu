@@ -114,7 +114,7 @@ void nccl_unique_id(void* out128) {
   std::memcpy(out128, &id, sizeof(id));
 }
 
-std::unique_ptr<Comm> make_nccl_comm(int nranks, int rank, const void* unique_id) {
+std::shared_ptr<Comm> make_nccl_comm(int nranks, int rank, const void* unique_id) {
   check_ranks(nranks, rank);
   auto c = std::make_unique<NcclComm>();
   c->rank = rank;
@@ -125,7 +125,7 @@ std::unique_ptr<Comm> make_nccl_comm(int nranks, int rank, const void* unique_id
   return c;
 }
 
-std::unique_ptr<Comm> make_host_comm(int nranks, int rank, HostAllgatherFn fn, void* user) {
+std::shared_ptr<Comm> make_host_comm(int nranks, int rank, HostAllgatherFn fn, void* user) {
   check_ranks(nranks, rank);
   if (!fn) throw std::invalid_argument("h2g: null all-gather callback");
   auto c = std::make_unique<HostComm>();

@@ -32,12 +32,12 @@ struct Comm {
 // without NCCL; the all-gather-v is a group of in-place broadcasts, one per
 // owner, over NVLink/NVSwitch).
 void nccl_unique_id(void* out128);
-std::unique_ptr<Comm> make_nccl_comm(int nranks, int rank, const void* unique_id);
+std::shared_ptr<Comm> make_nccl_comm(int nranks, int rank, const void* unique_id);
 
 // Host-mediated exchange through a caller callback (e.g. a gloo process group
 // in tests): the owned segment is staged to pinned host memory, the callback
 // all-gathers the host buffer, the result is copied back.
 typedef int (*HostAllgatherFn)(void* user, void* host_buf, const int64_t* byte_offs, int nranks);
-std::unique_ptr<Comm> make_host_comm(int nranks, int rank, HostAllgatherFn fn, void* user);
+std::shared_ptr<Comm> make_host_comm(int nranks, int rank, HostAllgatherFn fn, void* user);
 
 }  // namespace h2g

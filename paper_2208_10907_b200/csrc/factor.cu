@@ -423,6 +423,34 @@ struct Driver {
     if (flush) flush();
   }
 
+  // Multi-GPU: the box range this rank computes in a partitioned stage of an
+  // m-box level ([0, m) when single-GPU or the level is replicated).
+  std::pair<int64_t, int64_t> own_range(int64_t m) const {
+    if (P.comm && P.comm->partitioned(m)) return {P.comm->lo(m), P.comm->hi(m)};
+    return {0, m};
+  }
+
+  // All-gather matrices allocated by one alloc_mats call in non-decreasing
+  // box order (box[t] = box of mats[t]): every owner's matrices are one
+  // contiguous byte range of the slab.
+  void exchange_mats(const std::vector<DMat>& mats, const std::vector<int64_t>& box, int64_t m) {
+    if (!(P.comm && P.comm->partitioned(m)) || mats.empty()) return;
+    Comm& cm = *P.comm;
+    PhaseTimer pt(c, P.stats, "exchange");
+    char* base = reinterpret_cast<char*>(mats[0].m.p);
+    const DMat& last = mats.back();
+    const int64_t end = reinterpret_cast<char*>(last.m.p) - base +
+                        int64_t(sizeof(double)) * int64_t((size_t(last.m.rows) * last.m.cols + 3) & ~size_t(3));
+    std::vector<int64_t> offs(cm.size + 1, end);
+    size_t t = 0;
+    for (int r = 0; r < cm.size; ++r) {
+      const int64_t lo = cm.lo(m, r);
+      while (t < mats.size() && box[t] < lo) ++t;
+      if (t < mats.size()) offs[r] = reinterpret_cast<char*>(mats[t].m.p) - base;
+    }
+    cm.allgatherv(base, offs, c.stream);
+  }
+
   // Boxes [kb, ke): chunked concat fill -> in-place QR -> sink.
   void run_bases_range(std::vector<Members>& rows, std::vector<Members>* cols, const FillFn& fill,
                        const SinkFn& sink, const std::function<void()>& flush, int64_t kb, int64_t ke) {
@@ -650,10 +678,12 @@ struct Driver {
     pieces.assign(m, {});
     // q_cp = (A_pp^-T A_cp^T Us_c)^T for near p != c.
     std::map<std::pair<int64_t, int64_t>, DMat> qT;  // stored as B = dims_p x r_c (q = B^T)
+    // Multi-GPU: the pieces of this rank's boxes only, then all-gathered.
+    const auto [lo, hi] = own_range(m);
     if (sys.offdiag) {
       std::vector<std::pair<int64_t, int64_t>> keys;
       std::vector<std::pair<int, int>> shapes;
-      for (int64_t cc = 0; cc < m; ++cc) {
+      for (int64_t cc = lo; cc < hi; ++cc) {
         if (Ub[cc].rank == 0) continue;
         for (int64_t t = 0; t < S.nnear(L, cc); ++t) {
           const int64_t p = S.near(L, cc)[t];
@@ -686,6 +716,8 @@ struct Driver {
     GemmBatch gb;
     for (size_t t = 0; t < pkeys.size(); ++t) {
       const auto [cc, tk] = pkeys[t];
+      pieces[cc][tk] = mats[t];
+      if (cc < lo || cc >= hi) continue;
       const int64_t jb = rb(tk.first, tk.second), je = jb + rs(tk.first, tk.second);
       const int w = int(je - jb);
       gb.job(mats[t].m, false);
@@ -699,9 +731,13 @@ struct Driver {
           if (all_zero) continue;
           gb.seg_gen(qT[{cc, p}].m.t(), rb(L, p), jb, w, false, -1.0, mask);
         }
-      pieces[cc][tk] = mats[t];
     }
     gb.run(c);
+    {
+      std::vector<int64_t> box(pkeys.size());
+      for (size_t t = 0; t < pkeys.size(); ++t) box[t] = pkeys[t].first;
+      exchange_mats(mats, box, m);
+    }
     // Fill content: project, measure absorption, add into the target piece.
     observe_and_add_fills(L, fills, pieces, level_max, true);
   }
@@ -808,7 +844,10 @@ struct Driver {
       // g(P, tk) = A_PP^-1 (stack[P][tk] with P's near columns zeroed), shared across K.
       std::map<std::pair<int64_t, TargetKey>, DMat> g;
       std::vector<std::pair<int64_t, TargetKey>> need;
-      for (int64_t K = 0; K < m; ++K)
+      // Multi-GPU: corrected pieces of this rank's boxes only (all-gathered
+      // below); the g's they need may belong to neighbours (recomputed).
+      const auto [lo, hi] = own_range(m);
+      for (int64_t K = lo; K < hi; ++K)
         for (int64_t x = 0; x < S.nnear(lvl, K); ++x) {
           const int64_t Pp = S.near(lvl, K)[x];
           if (Pp == K) continue;
@@ -857,6 +896,8 @@ struct Driver {
       GemmBatch gb;
       for (size_t t = 0; t < keys.size(); ++t) {
         const auto [K, tk] = keys[t];
+        merged[K][tk] = cm[t];
+        if (K < lo || K >= hi) continue;
         cc.copy(cm[t].m, stack[K].at(tk).m);
         bool any = false;
         for (int64_t x = 0; x < S.nnear(lvl, K); ++x) {
@@ -868,10 +909,12 @@ struct Driver {
           any = true;
           gb.seg(block(sys, K, Pp), it->second.m, -1.0);
         }
-        merged[K][tk] = cm[t];
       }
       cc.run(c);
       gb.run(c);
+      std::vector<int64_t> box(keys.size());
+      for (size_t t = 0; t < keys.size(); ++t) box[t] = keys[t].first;
+      exchange_mats(cm, box, m);
     } else {
       merged = stack;
     }
@@ -1398,12 +1441,16 @@ struct Driver {
             }
           }
         auto mats = alloc_mats(c, shapes);
+        const auto [lo, hi] = own_range(sys.m);  // multi-GPU: own boxes, then all-gathered
+        std::vector<int64_t> box(keys.size());
         for (size_t t = 0; t < keys.size(); ++t) {
           const auto [k, tk] = keys[t];
-          gemm1(gb, mats[t].m, P.U[sys.lvl][k].Qs().t(), src[k].at(tk).m);
           next[k][tk] = mats[t];
+          box[t] = k;
+          if (k >= lo && k < hi) gemm1(gb, mats[t].m, P.U[sys.lvl][k].Qs().t(), src[k].at(tk).m);
         }
         gb.run(c);
+        exchange_mats(mats, box, sys.m);
         carried = std::move(next);
       }
       make_layer(sys.lvl);

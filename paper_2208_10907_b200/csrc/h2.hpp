@@ -92,7 +92,7 @@ class Problem {
   // Multi-GPU level partition (null: single GPU). The partitioned stages
   // compute only this rank's box range and all-gather their outputs, so
   // every rank ends with the single-GPU factors bit for bit.
-  std::unique_ptr<Comm> comm;
+  std::shared_ptr<Comm> comm;
 
   Problem();
   ~Problem();

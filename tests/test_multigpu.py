@@ -67,7 +67,7 @@ def _factor_case(case, comm=None):
     p.set_options(tol=tol, cap=cap)
     p.build(xyz, q, leaf)
     if comm is not None:
-        p.set_comm_host(*comm, g.gloo_allgather())
+        p.set_comm(g.Comm.host(*comm, g.gloo_allgather()))
     p.factor()
     x = _solve(p, n)
     bases = [p.basis(p.levels, k, side)[0] for k in range(1 << p.levels) for side in (0, 1)]
@@ -105,3 +105,26 @@ def test_partitioned_factor_is_bitwise_single_gpu(tmp_path, world, case):
         br = np.load(tmp_path / f"b{r}.npz")
         assert all(np.array_equal(br[f"arr_{i}"].view(np.int64), b.view(np.int64)) for i, b in enumerate(b1))
         assert np.load(tmp_path / f"r{r}.npy").tolist() == sum(r1, [])
+
+
+@pytest.mark.gpu
+def test_nccl_communicator_single_rank():
+    """libnccl.so.2 resolves at run time and a 1-rank communicator is a no-op
+    partition (the factors are the single-GPU ones)."""
+    uid = g.nccl_unique_id()
+    assert len(uid) == 128
+    comm = g.Comm.nccl(1, 0, uid)
+    x1, _, _ = _factor_case(CASES[0])
+    import paper_2208_10907_b200 as h2
+    from oracle import cpu
+    xyz, q = cpu.generate("cube", 4096, 42)
+    p = h2.Problem()
+    p.set_kernel("laplace", 0.0, 1.0, 1e-3)
+    p.set_options(tol=1e-8)
+    p.build(xyz, q, 128)
+    p.set_comm(comm)
+    p.factor()
+    x = _solve(p, 4096)
+    p.close()
+    comm.close()
+    assert np.array_equal(x.view(np.int64), x1.view(np.int64))
