@@ -1,0 +1,52 @@
+"""C++ façade (include/h2ulv_b200.hpp): the reference's Pipeline / build_cluster_tree /
+classify_blocks / solve API over the C ABI, exercised by tests/cpp/facade_demo.cpp
+(built by `make -C paper_2208_10907_b200`)."""
+import json
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+DEMO = os.path.join(ROOT, "paper_2208_10907_b200", "build", "facade_demo")
+
+
+def run_demo(*args):
+    if not os.path.exists(DEMO):
+        pytest.fail("facade_demo not built (make -C paper_2208_10907_b200)")
+    r = subprocess.run([DEMO, *map(str, args)], capture_output=True, text=True, timeout=600)
+    return r.returncode, [json.loads(line) for line in r.stdout.splitlines() if line.startswith("{")]
+
+
+def _has_gpu():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+@pytest.mark.skipif(_has_gpu(), reason="checks the no-device failure")
+def test_facade_errors_without_gpu():
+    """Config errors are invalid_argument with the reference's message; with no
+    device the path fails loudly (no CPU fallback)."""
+    rc, lines = run_demo()
+    assert lines[0] == {"invalid_argument": "config: need n >= 2 * leaf size"}
+    assert rc == 2 and "no CUDA device" in lines[1]["runtime_error"]
+
+
+@pytest.mark.gpu
+def test_facade_pipeline_matches_reference(golden):
+    """C1 oracle case through the C++ Pipeline: tree and x bit-identical to
+    the reference (golden), tree/lists identical between the entry points."""
+    gd, _ = golden
+    rec = gd["cases"]["c1_cube4096"]
+    rc, lines = run_demo(rec["n"], rec["leaf"])
+    assert rc == 0, lines
+    out = lines[1]
+    assert out["levels"] == rec["levels"]
+    assert out["perm_fnv"] == rec["perm_fnv"]
+    assert out["x_fnv"] == rec["x_fnv"]
+    assert out["same_tree"] and out["same_lists"]
+    assert out["rank_sum"] == sum(sum(v) for v in rec["ranks"].values())
+    assert abs(out["residual"] - rec["residual"]) <= 1e-12 * rec["residual"]
