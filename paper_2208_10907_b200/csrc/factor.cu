@@ -1400,6 +1400,16 @@ struct Driver {
       if (k.first != k.second) basis_fills[k] = F;
     build_leaf_bases(sys, basis_fills);
 
+    // H2G_HOST_PROF: host seconds per driver stage (enqueue + any syncs).
+    const bool hp = getenv("H2G_HOST_PROF") != nullptr;
+    double hpt = now_s();
+    auto mark = [&](const char* what) {
+      if (!hp) return;
+      const double t = now_s();
+      fprintf(stderr, "HOSTSTAGE level %d %-18s %.4f s\n", sys.lvl, what, t - hpt);
+      hpt = t;
+    };
+    mark("leaf_bases");
     while (true) {
       const bool is_leaf = sys.lvl == L;
       std::vector<PieceMap> pieces, stack, merged;
@@ -1407,20 +1417,26 @@ struct Driver {
       double* lm = &P.max_fill_resid.back();
       if (is_leaf) {
         build_leaf_pieces(sys, fills, pieces, lm);
+        mark("leaf_pieces");
       } else {
         fills = precompute_fillins(sys);
+        mark("fills");
         build_upper_pieces(sys, fills, stack, merged);
+        mark("upper_pieces");
         build_transfers(sys, fills, merged);
+        mark("transfers");
       }
       std::vector<DMat> diag_S;
       std::map<std::pair<int64_t, int64_t>, DMat> far_ss, dense_ss;
       assemble_level(sys, fills, pieces, merged, diag_S, far_ss, dense_ss, lm);
+      mark("assemble");
       LevelF lf;
       lf.level = sys.lvl;
       lf.dims = sys.dims;
       lf.ranks.resize(sys.m);
       for (int64_t k = 0; k < sys.m; ++k) lf.ranks[k] = P.U[sys.lvl][k].rank;
       eliminate_level(sys, diag_S, lf);
+      mark("eliminate");
       lf.use_z = sys.offdiag;
       // project_pieces (ulv.cpp:675-689)
       {
@@ -1453,9 +1469,11 @@ struct Driver {
         exchange_mats(mats, box, sys.m);
         carried = std::move(next);
       }
+      mark("project_pieces");
       make_layer(sys.lvl);
       big_owner = std::move(big_owner_next_);
       SysL next = merge(sys, diag_S, far_ss, dense_ss);
+      mark("layer+merge");
       lf.sys = std::move(sys);
       P.levels.push_back(std::move(lf));
       const int next_lvl = next.lvl;
