@@ -23,7 +23,7 @@ Slab Ctx::alloc(size_t bytes) {
   if (e != cudaSuccess) {
     cudaGetLastError();
     throw std::runtime_error("device memory exhausted allocating " + std::to_string(bytes) +
-                             " bytes: " + cudaGetErrorString(e));
+                             " bytes in phase " + phase + ": " + cudaGetErrorString(e));
   }
   cudaStream_t s = stream;
   return Slab(p, [s](void* q) { cudaFreeAsync(q, s); });
