@@ -329,9 +329,13 @@ void LuBatch::run(Ctx& c) {
   auto* dj = upload(c, jobs, k1);
   c.lu_names = names;
   double by = 0;
-  for (auto& j : jobs) by += 16.0 * j.A.rows * double(j.A.cols);
+  int max_n = 1;
+  for (auto& j : jobs) {
+    by += 16.0 * j.A.rows * double(j.A.cols);
+    max_n = std::max(max_n, j.A.rows);
+  }
   auto ev = c.prof_begin();
-  launch_lu(dj, int(jobs.size()), c.err, ++c.lu_tag, c.stream);
+  launch_lu(dj, int(jobs.size()), max_n, c.err, ++c.lu_tag, c.stream);
   c.prof_end("lu", ev, fl, by);
   c.launches++;
   cuda_check(cudaGetLastError(), "lu launch");

@@ -48,16 +48,19 @@ __device__ ValIdx block_argmax(ValIdx x, ValIdx* red) {
 __global__ void __launch_bounds__(NT) lu_kernel(const LuJob* __restrict__ jobs, ErrWord* err,
                                                 int tag) {
   __shared__ ValIdx red[32];
+  extern __shared__ double lcol[];  // scaled pivot column of the current step (n doubles)
   const LuJob job = jobs[blockIdx.x];
   const Mat M = job.A;
   const int n = M.rows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < n; i += NT) job.perm[i] = i;
   // amax = norm_max_abs(A)
   ValIdx am{0.0, 0};
-  for (int64_t e = threadIdx.x; e < int64_t(n) * n; e += NT) {
-    const double v = fabs(M.at(e % n, e / n));
-    if (v > am.v) am.v = v;
-  }
+  for (int j = warp; j < n; j += NT / 32)
+    for (int i = lane; i < n; i += 32) {
+      const double v = fabs(M.at(i, j));
+      if (v > am.v) am.v = v;
+    }
   const double amax = block_argmax(am, red).v;
   for (int k = 0; k < n; ++k) {
     ValIdx best{-1.0, 0x7fffffff};
@@ -82,12 +85,17 @@ __global__ void __launch_bounds__(NT) lu_kernel(const LuJob* __restrict__ jobs, 
       __syncthreads();
     }
     const double inv = 1.0 / M.at(k, k);
-    for (int i = k + 1 + threadIdx.x; i < n; i += NT) M.at(i, k) = M.at(i, k) * inv;
+    for (int i = k + 1 + threadIdx.x; i < n; i += NT) {
+      const double l = M.at(i, k) * inv;
+      M.at(i, k) = l;
+      lcol[i] = l;
+    }
     __syncthreads();
-    const int t = n - k - 1;
-    for (int64_t e = threadIdx.x; e < int64_t(t) * t; e += NT) {
-      const int i = k + 1 + int(e % t), j = k + 1 + int(e / t);
-      M.at(i, j) = fma(-M.at(i, k), M.at(k, j), M.at(i, j));
+    // Rank-1 update of the trailing block: a warp per column (u_kj loaded
+    // once), lanes down the rows (coalesced), l_ik from shared memory.
+    for (int j = k + 1 + warp; j < n; j += NT / 32) {
+      const double u = M.at(k, j);
+      for (int i = k + 1 + lane; i < n; i += 32) M.at(i, j) = fma(-lcol[i], u, M.at(i, j));
     }
     __syncthreads();
   }
@@ -294,8 +302,10 @@ void launch_gather_rows(const GatherJob* jobs, const int2* tiles, int ntiles, cu
   if (ntiles > 0) gather_rows_kernel<<<ntiles, 256, 0, st>>>(jobs, tiles);
 }
 
-void launch_lu(const LuJob* jobs, int njobs, ErrWord* err, int tag, cudaStream_t st) {
-  if (njobs > 0) lu_kernel<<<njobs, NT, 0, st>>>(jobs, err, tag);
+void launch_lu(const LuJob* jobs, int njobs, int max_n, ErrWord* err, int tag, cudaStream_t st) {
+  const size_t smem = sizeof(double) * size_t(max_n > 0 ? max_n : 1);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (njobs > 0) lu_kernel<<<njobs, NT, smem, st>>>(jobs, err, tag);
 }
 
 int solve_chunk_width(int m) {

@@ -99,7 +99,7 @@ struct LuJob {
   int64_t* perm;
   double tol;
 };
-void launch_lu(const LuJob* jobs, int njobs, ErrWord* err, int tag, cudaStream_t st);
+void launch_lu(const LuJob* jobs, int njobs, int max_n, ErrWord* err, int tag, cudaStream_t st);
 
 // LuFactors solve family (linalg.cpp:404-559), in place on X.
 enum SolveKind : int {
