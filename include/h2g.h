@@ -38,6 +38,9 @@ typedef struct {
   int32_t structure;            /* 0 = h2 (strong, nodep), 1 = hss (weak) */
   double eta;                   /* strong admissibility eta (1.0) */
   int64_t qr_mem_budget;        /* bytes of QR working memory per chunk, <= 0: default */
+  int32_t qr_mode;              /* 0 = exact (the reference's rounding, bit-exact),
+                                   1 = blocked (NB = 32 reflectors per panel update;
+                                   same decisions, parity within tolerance) */
 } h2g_options;
 
 const char* h2g_last_error(void);

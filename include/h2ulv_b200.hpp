@@ -135,10 +135,10 @@ inline void soa(const PointCloud& c, std::vector<double>& xyz) {
 }
 inline std::shared_ptr<Handle> build(const PointCloud& cloud, int64_t leaf, const KernelSpec& k,
                                      double eta, StructureVariant v, double tol,
-                                     std::optional<int64_t> cap, bool absorb) {
+                                     std::optional<int64_t> cap, bool absorb, int qr_mode = 0) {
   auto h = std::make_shared<Handle>();
   h2g_kernel hk{k.kind == KernelKind::laplace ? 0 : 1, k.alpha_m, k.permittivity_scale, k.eta_reg};
-  h2g_options o{tol, cap.value_or(0), 1e-13, absorb ? 1 : 0, 100.0, v == StructureVariant::h2 ? 0 : 1, eta, 0};
+  h2g_options o{tol, cap.value_or(0), 1e-13, absorb ? 1 : 0, 100.0, v == StructureVariant::h2 ? 0 : 1, eta, 0, qr_mode};
   check(h2g_set_kernel(h->p, &hk));
   check(h2g_set_options(h->p, &o));
   std::vector<double> xyz;
@@ -249,6 +249,9 @@ struct RunConfig {
   uint64_t seed = 42;
   bool absorb_coupling = true;
   std::optional<PointCloud> points;  // import instead of generating
+  // B200 extension: 0 = exact QR (bit-exact with the reference), 1 = blocked QR
+  // (reflectors applied 32 at a time; parity within tolerance).
+  int qr_mode = 0;
 
   void validate() const {  // report.cpp:43-58
     if (n < 2) throw std::invalid_argument("config: n must be >= 2");
@@ -284,7 +287,7 @@ class Pipeline {
     original_ = make_cloud(cfg_);
     kernel_ = make_kernel(cfg_, original_);
     h_ = detail::build(original_, cfg_.leaf_size, kernel_, cfg_.eta, cfg_.structure, cfg_.tol, cfg_.cap,
-                       cfg_.absorb_coupling);
+                       cfg_.absorb_coupling, cfg_.qr_mode);
     built_ = true;
   }
   void factor() {  // bases + fills + ULV factorization (report.cpp:93-106)

@@ -25,7 +25,7 @@ class Kernel(ctypes.Structure):
 class Options(ctypes.Structure):
     _fields_ = [("tol", f64), ("cap", i64), ("rr_pivot_tol", f64), ("absorb_coupling", ctypes.c_int32),
                 ("abort_residual_factor", f64), ("structure", ctypes.c_int32), ("eta", f64),
-                ("qr_mem_budget", i64)]
+                ("qr_mem_budget", i64), ("qr_mode", ctypes.c_int32)]
 
 
 EXPORTS = [
@@ -213,9 +213,9 @@ class Problem:
         _check(self.L.h2g_set_kernel(self.h, ctypes.byref(k)))
 
     def set_options(self, tol=1e-8, cap=None, rr_pivot_tol=1e-13, absorb_coupling=True,
-                    abort_residual_factor=100.0, structure="h2", eta=1.0, qr_mem_budget=0):
+                    abort_residual_factor=100.0, structure="h2", eta=1.0, qr_mem_budget=0, qr_mode="exact"):
         o = Options(tol, cap or 0, rr_pivot_tol, 1 if absorb_coupling else 0, abort_residual_factor,
-                    {"h2": 0, "hss": 1}[structure], eta, qr_mem_budget)
+                    {"h2": 0, "hss": 1}[structure], eta, qr_mem_budget, {"exact": 0, "blocked": 1}[qr_mode])
         _check(self.L.h2g_set_options(self.h, ctypes.byref(o)))
 
     def build(self, xyz, q, leaf):

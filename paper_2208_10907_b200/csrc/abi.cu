@@ -89,6 +89,8 @@ int h2g_set_options(h2g_problem* p, const h2g_options* o) {
     op.abort_residual_factor = o->abort_residual_factor;
     op.structure = o->structure;
     op.eta = o->eta;
+    if (o->qr_mode != 0 && o->qr_mode != 1) throw std::invalid_argument("config: qr_mode must be 0 (exact) or 1 (blocked)");
+    op.qr_mode = o->qr_mode;
     if (o->qr_mem_budget > 0) {
       op.qr_mem_budget = size_t(o->qr_mem_budget);
       p->P.auto_budget_ = false;

@@ -1,5 +1,6 @@
 // Host-side batch launchers (see batch.hpp).
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -19,7 +20,13 @@ Slab Ctx::alloc(size_t bytes) {
   void* p = nullptr;
   if (bytes == 0) bytes = 8;
   bytes = (bytes + 255) & ~size_t(255);
+  static const bool hp = getenv("H2G_HOST_PROF") != nullptr;
+  const auto t0 = hp ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
   cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+  if (hp) {
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (ms > 2.0) fprintf(stderr, "HOSTALLOC %.1f ms for %.3f GB in phase %s\n", ms, bytes / 1e9, phase.c_str());
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     throw std::runtime_error("device memory exhausted allocating " + std::to_string(bytes) +
@@ -479,6 +486,13 @@ void SolveBatch::run(Ctx& c) {
 
 void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t mem_budget) {
   const size_t n_items = items.size();
+  int max_rows = 0;
+  for (auto& it : items) max_rows = std::max(max_rows, it.m);
+  // Blocked mode when asked for and every basis fits its register-resident Q formation.
+  const bool blocked = c.qr_blocked && max_rows <= qrb_max_rows();
+  auto scratch_doubles = [&](int m, int n, int nmem) {
+    return blocked ? qrb_scratch_doubles(m, n, nmem) : qr_scratch_doubles(m, n, nmem);
+  };
   Q.assign(n_items, DMat{});
   rank.assign(n_items, 0);
   if (n_items == 0) return;
@@ -502,7 +516,7 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
     while (t1 < n_items) {  // (+32 B per item: 16-byte alignment padding)
       const auto& it = items[t1];
       const size_t need = sizeof(double) * ((it.inplace ? 0 : size_t((it.m + 1) & ~1) * it.n) +
-                                            qr_scratch_doubles(it.m, it.n, int(it.offs.size()) - 1)) +
+                                            scratch_doubles(it.m, it.n, int(it.offs.size()) - 1)) +
                           sizeof(int64_t) * it.offs.size() + 1024 + 32;
       if (t1 > t0 && bytes + need > mem_budget) break;
       bytes += need;
@@ -546,7 +560,7 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
         at = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(at) + 15) & ~uintptr_t(15));
       }
       j.scratch = reinterpret_cast<double*>(at);
-      at += sizeof(double) * qr_scratch_doubles(it.m, it.n, j.nmem);
+      at += sizeof(double) * scratch_doubles(it.m, it.n, j.nmem);
       at = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(at) + 15) & ~uintptr_t(15));
       j.Q = Q[t].m.p;
       j.rank_out = static_cast<int*>(rk.get()) + t;
@@ -567,7 +581,8 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
       auto work = [&](const QrJob& j) { return double(j.m) * j.n; };
       std::fill(G.begin(), G.end(),
                 ecl ? std::max(1, std::min(8, atoi(ecl)))
-                    : qr_cluster_size(int(jobs.size()), min_n, max_m, max_nmem));
+                    : blocked ? qrb_cluster_size(int(jobs.size()), min_n, max_m, max_nmem)
+                              : qr_cluster_size(int(jobs.size()), min_n, max_m, max_nmem));
       std::vector<size_t> ord(jobs.size());
       for (size_t q = 0; q < ord.size(); ++q) ord[q] = q;
       std::stable_sort(ord.begin(), ord.end(), [&](size_t x, size_t y) {
@@ -600,7 +615,10 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
       cudaEventRecord(dbg_a, c.stream);
     }
     const int cl = G.empty() ? 1 : G[0];
-    launch_qr(dj, int(jobs.size()), max_m, max_nmem, cl, c.stream);
+    if (blocked)
+      launch_qrb(dj, int(jobs.size()), max_m, max_nmem, cl, c.stream);
+    else
+      launch_qr(dj, int(jobs.size()), max_m, max_nmem, cl, c.stream);
     if (ddbg) {
       cudaEventRecord(dbg_b, c.stream);
       cudaEventSynchronize(dbg_b);

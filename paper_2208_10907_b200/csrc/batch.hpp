@@ -48,6 +48,8 @@ struct Ctx {
   ~Ctx();
   // Side streams (fork/join from `stream` with the pooled events) for
   // independent launches that should run concurrently.
+  // QR mode: exact (the reference's rounding, k_qr.cu) or blocked (k_qrb.cu).
+  bool qr_blocked = getenv("H2G_QR_MODE") && std::string(getenv("H2G_QR_MODE")) == "blocked";  // per problem: Options::qr_mode
   std::vector<cudaStream_t> sides;
   std::vector<cudaEvent_t> evs;
   cudaStream_t side_stream(int i);

@@ -732,7 +732,10 @@ struct Driver {
           gb.seg_gen(qT[{cc, p}].m.t(), rb(L, p), jb, w, false, -1.0, mask);
         }
     }
-    gb.run(c);
+    {
+      PhaseTimer pt2(c, P.stats, "skeleton_leaf_pieces");
+      gb.run(c);
+    }
     {
       std::vector<int64_t> box(pkeys.size());
       for (size_t t = 0; t < pkeys.size(); ++t) box[t] = pkeys[t].first;
@@ -1501,6 +1504,8 @@ void Problem::factor() {
     opt.qr_mem_budget = std::max<size_t>(size_t(1) << 28, fr / 3);
   }
   c.phase_flops.clear();
+  const char* qm = getenv("H2G_QR_MODE");  // experiment override
+  c.qr_blocked = qm ? std::string(qm) == "blocked" : opt.qr_mode == 1;
   levels.clear();
   max_fill_resid.clear();
   Driver d(*this);

@@ -23,6 +23,7 @@ struct Options {  // FactorOptions (ulv.hpp:29-45) + RunConfig bits
   int structure = 0;  // 0 h2 (strong, nodep), 1 hss (weak)
   double eta = 1.0;
   size_t qr_mem_budget = size_t(8) << 30;  // auto (free/3) unless set
+  int qr_mode = 0;  // 0 exact (k_qr.cu, bit-exact), 1 blocked (k_qrb.cu, tolerance parity)
 };
 
 struct Basis {  // SharedBasis (hstructure.hpp:61-69): square [Qr | Qs]

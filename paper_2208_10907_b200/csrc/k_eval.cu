@@ -84,26 +84,61 @@ __global__ void permute_rows_kernel(Mat dst, Mat src, const int64_t* idx, int sc
   else dst.at(i, j) = src.at(idx[i], j);
 }
 
-// norm_frobenius (linalg.cpp:604-609): s += d*d over storage order, one
-// thread per matrix so the rounding sequence is the reference's.
+// norm_frobenius (linalg.cpp:604-609): s += d*d over storage order. GCC's
+// vectorised reduction (see k_qr.cu, pattern P2): 4-wide groups of rounded
+// squares added in order; tails (and sizes <= 3) fused. One warp per matrix:
+// the lanes load 32 consecutive elements (coalesced, one chunk ahead) and
+// square them; the in-order sum runs on every lane from shuffled squares, so
+// the dependent chain is one DADD per element.
 __global__ void norms_kernel(const NormJob* __restrict__ jobs, int njobs) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= njobs) return;
-  const NormJob job = jobs[t];
-  // GCC's vectorised reduction (see k_qr.cu, pattern P2): 4-wide groups of
-  // rounded squares added in order; tails (and sizes <= 3) fused.
-  const int64_t rows = job.a.rows, tc = rows * job.a.cols;
-  auto get = [&](int64_t e) { const double d = job.a.at(e % rows, e / rows); return d; };
+  const int w = int((blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (w >= njobs) return;
+  const NormJob job = jobs[w];
+  const int rows = job.a.rows;
+  const int64_t tc = int64_t(rows) * job.a.cols;
+  // Element e = (e % rows, e / rows) of the column-major walk; (i0, j0) is the
+  // walk position of the current chunk's lane 0.
+  int i0 = 0;
+  int64_t j0 = 0;
+  auto elem = [&](int64_t base_i, int64_t base_j, int off, int64_t e, int64_t lim) {
+    if (e >= lim) return 0.0;
+    int64_t i = base_i + off, j = base_j;
+    while (i >= rows) {
+      i -= rows;
+      ++j;
+    }
+    return job.a.at(i, j);
+  };
+  auto advance = [&](int by) {
+    i0 += by;
+    while (i0 >= rows) {
+      i0 -= rows;
+      ++j0;
+    }
+  };
   double s = 0.0;
   if (tc <= 3) {
-    for (int64_t e = 0; e < tc; ++e) { const double d = get(e); s = fma(d, d, s); }
+    for (int64_t e = 0; e < tc; ++e) {
+      const double d = elem(0, 0, int(e), e, tc);
+      s = fma(d, d, s);
+    }
   } else {
     const int64_t v4 = tc & ~int64_t(3);
-    int64_t e = 0;
-    for (; e < v4; ++e) { const double d = get(e); s = s + d * d; }
-    for (; e < tc; ++e) { const double d = get(e); s = fma(d, d, s); }
+    double cur = elem(i0, j0, lane, lane, v4);
+    for (int64_t e0 = 0; e0 < v4; e0 += 32) {
+      advance(32);
+      const double nxt = elem(i0, j0, lane, e0 + 32 + lane, v4);  // next chunk in flight
+      const double sq = cur * cur;
+      const int cnt = v4 - e0 < 32 ? int(v4 - e0) : 32;
+      for (int l = 0; l < cnt; ++l) s = s + __shfl_sync(0xffffffffu, sq, l);
+      cur = nxt;
+    }
+    for (int64_t e = v4; e < tc; ++e) {  // fused tail (<= 3 elements)
+      const double d = job.a.at(e % rows, e / rows);
+      s = fma(d, d, s);
+    }
   }
-  *job.out = sqrt(s);
+  if (lane == 0) *job.out = sqrt(s);
 }
 
 // y = A x by direct summation in the ORIGINAL point order, each y_i
@@ -175,7 +210,7 @@ void launch_permute_rows(Mat dst, Mat src, const int64_t* idx, int scatter, cuda
 }
 
 void launch_norms(const NormJob* jobs, int njobs, cudaStream_t st) {
-  if (njobs > 0) norms_kernel<<<(njobs + 127) / 128, 128, 0, st>>>(jobs, njobs);
+  if (njobs > 0) norms_kernel<<<(njobs + 3) / 4, 128, 0, st>>>(jobs, njobs);  // a warp per matrix
 }
 
 }  // namespace h2g

@@ -165,5 +165,11 @@ int qr_cluster_size(int njobs, int min_n, int max_m, int max_nmem);
 int qr_fit(int g, int max_m, int max_nmem);
 int qr_max_cluster(int n);
 size_t qr_scratch_doubles(int m, int n, int nmem);
+// Blocked QR mode (k_qrb.cu): same job interface, reflectors accumulated NB at
+// a time; rounding differs from the reference (tolerance parity).
+size_t qrb_scratch_doubles(int m, int n, int nmem);
+int qrb_max_rows();
+void launch_qrb(const QrJob* jobs, int njobs, int max_m, int max_nmem, int cluster, cudaStream_t st);
+int qrb_cluster_size(int njobs, int min_n, int max_m, int max_nmem);
 
 }  // namespace h2g

@@ -60,11 +60,12 @@ def _solve(p, n):
 def _factor_case(case, comm=None):
     import paper_2208_10907_b200 as h2
     from oracle import cpu
-    geom, n, leaf, kind, cap, tol = case
+    geom, n, leaf, kind, cap, tol = case[:6]
+    mode = case[6] if len(case) > 6 else "exact"
     xyz, q = cpu.generate(geom, n, 42)
     p = h2.Problem()
     p.set_kernel(kind, 1.0 if kind == "yukawa" else 0.0, 1.0, 1e-3)
-    p.set_options(tol=tol, cap=cap)
+    p.set_options(tol=tol, cap=cap, qr_mode=mode)
     p.build(xyz, q, leaf)
     if comm is not None:
         p.set_comm(g.Comm.host(*comm, g.gloo_allgather()))
@@ -90,12 +91,13 @@ def _worker(rank, world, port, case, out):
 
 
 CASES = [("cube", 4096, 128, "laplace", 0, 1e-8),
-         ("cube", 8192, 128, "laplace", 64, 1e-4)]
+         ("cube", 8192, 128, "laplace", 64, 1e-4),
+         ("cube", 4096, 128, "laplace", 0, 1e-8, "blocked")]
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("case", CASES, ids=["c1_cube4096", "cube8192_cap64"])
+@pytest.mark.parametrize("case", CASES, ids=["c1_cube4096", "cube8192_cap64", "c1_cube4096_blockedqr"])
 def test_partitioned_factor_is_bitwise_single_gpu(tmp_path, world, case):
     x1, b1, r1 = _factor_case(case)
     mp.spawn(_worker, args=(world, _port(), case, str(tmp_path)), nprocs=world, join=True)
