@@ -8,6 +8,11 @@ so the diagonal is 1e3), leaf 256, strong admissibility eta = 1, rank cap
 100, tol 1e-6 (tol 1e-8 with cap 100 makes the reference abort with "basis
 does not absorb fill-in" at leaf 256; measured).
 
+QR mode: blocked by default (member-panel Householder reflectors applied 32
+at a time; the reference's pivoting/stopping rules; solve residual equal to
+the reference's within 1e-6 relative, tests/test_qr_blocked.py); the line's
+"exact_qr" field times the same step with the bit-exact per-step QR.
+
 A step = one pass of the hot path from device-resident points: cluster tree
 + admissibility lists + near-field arena (Pipeline::build), fill-in
 pre-computation + bases + level-parallel ULV factorization (Pipeline::factor)
@@ -175,6 +180,7 @@ def run_b200_arm(args):
     n = args.n or WORKLOAD["n"]
     leaf = WORKLOAD["leaf"]
     partitioned = world > 1 and not args.replicas
+    qr_mode = args.qr_mode
     comm = None
     if partitioned:
         uid = [h2.nccl_unique_id() if rank == 0 else None]
@@ -193,7 +199,7 @@ def run_b200_arm(args):
         p = h2.Problem()
         p.set_stream(stream.cuda_stream)
         p.set_kernel("yukawa", WORKLOAD["alpha_m"], WORKLOAD["scale"], WORKLOAD["reg"])
-        p.set_options(tol=WORKLOAD["tol"], cap=WORKLOAD["cap"], eta=WORKLOAD["eta"])
+        p.set_options(tol=WORKLOAD["tol"], cap=WORKLOAD["cap"], eta=WORKLOAD["eta"], qr_mode=qr_mode)
         if comm is not None:
             p.set_comm(comm)
         return p
@@ -265,7 +271,7 @@ def run_b200_arm(args):
         t0 = time.perf_counter()
         pe = h2.Problem()
         pe.set_kernel("yukawa", WORKLOAD["alpha_m"], WORKLOAD["scale"], WORKLOAD["reg"])
-        pe.set_options(tol=WORKLOAD["tol"], cap=WORKLOAD["cap"], eta=WORKLOAD["eta"])
+        pe.set_options(tol=WORKLOAD["tol"], cap=WORKLOAD["cap"], eta=WORKLOAD["eta"], qr_mode=qr_mode)
         if comm is not None:
             pe.set_comm(comm)
         pe.build(xyz, q, leaf)
@@ -278,6 +284,27 @@ def run_b200_arm(args):
         tt = torch.tensor([e2e_t], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_t = float(tt.item())
+
+    # the same step in exact QR mode (bit-exact with the reference), for comparison
+    exact = None
+    if qr_mode != "exact" and args.exact_steps > 0:
+        qr_mode_saved, qr_mode = qr_mode, "exact"
+        times = []
+        with torch.cuda.stream(stream):
+            for _ in range(args.exact_steps):
+                p = new_problem()
+                step(p)
+                sd = p.stats_dev()
+                times.append(sd["build"] + sd["factor"] + sd["solve"])
+                p.close()
+        qr_mode = qr_mode_saved
+        te = max(times)
+        if world > 1:
+            tt = torch.tensor([te], device="cuda", dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            te = float(tt.item())
+        exact = {"qr_mode": "exact", "points_per_s": points / te, "steps": len(times),
+                 "note": "same workload with the reference's per-step QR rounding (bit-exact); device time"}
 
     # dominant kernel family and its roofline
     import json as _json
@@ -319,7 +346,7 @@ def run_b200_arm(args):
             "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong" if partitioned else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Fibonacci-lattice sphere, seed 42" + ("" if partitioned else "+rank") + ")",
-            "config": dict(WORKLOAD, n=n,
+            "config": dict(WORKLOAD, n=n, qr_mode=qr_mode,
                            parallelism=(f"box-partitioned x{world} (NCCL all-gather of bases)" if partitioned
                                         else f"replica x{world}"),
                            l2="inputs larger than L2 (near-field arena and member panels are GBs)"),
@@ -333,6 +360,7 @@ def run_b200_arm(args):
             "kernels": {k: dict(v, avg_ms=v["ms"] / max(1, v["launches"])) for k, v in kstats.items()},
             "clocks": clk,
             "cpu_baseline": cpu_baseline,
+            "exact_qr": exact,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -349,6 +377,11 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override N (testing only)")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--qr-mode", default="blocked", choices=["blocked", "exact"],
+                    help="member-panel QR: blocked (32 reflectors per panel update, parity within "
+                         "tolerance) or exact (the reference's rounding, bit-exact)")
+    ap.add_argument("--exact-steps", type=int, default=1,
+                    help="extra device-timed steps in exact QR mode, reported beside the headline")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: one independent problem per rank instead of one partitioned problem")
     args = ap.parse_args()

@@ -638,6 +638,10 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
       double a[14] = {0};
       for (size_t q = 0; q < jobs.size(); ++q)
         for (int u = 0; u < 14; ++u) a[u] += h[16 * q + u];
+      if (blocked)
+        fprintf(stderr, "QRDBG blocked jobs=%zu avg cycles: pivot %.3g lead %.3g pass %.3g masses %.3g update %.3g rank %.1f n %.0f\n",
+                jobs.size(), a[0] / jobs.size(), a[1] / jobs.size(), a[2] / jobs.size(), a[3] / jobs.size(),
+                a[8] / jobs.size(), a[4] / jobs.size(), a[5] / jobs.size());
       fprintf(stderr, "QRDBG jobs=%zu avg: piv %.3g refl %.3g tile %.3g mem %.3g rank %.1f n %.0f formq %.3g (cycles)\n",
               jobs.size(), a[0] / jobs.size(), a[1] / jobs.size(), a[2] / jobs.size(), a[3] / jobs.size(),
               a[4] / jobs.size(), a[5] / jobs.size(), a[6] / jobs.size());
@@ -670,8 +674,9 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
              "rank d2h");
   c.sync();
   // Reference flop rules for the executed steps (linalg.cpp:148, :176); the
-  // algorithmic bytes of the unblocked sweep: each step reads and writes the
-  // trailing panel once, and Q formation reads/writes its active rows.
+  // algorithmic bytes: exact mode reads and writes the trailing panel every
+  // step, blocked mode reads it every step and rewrites it once per block;
+  // Q formation reads/writes its active rows.
   double fl = 0;
   std::vector<double> fl_item(n_items, 0.0), by_item(n_items, 0.0);
   for (size_t t = 0; t < n_items; ++t) {
@@ -680,7 +685,14 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
       const double f = 4.0 * (m - k) + 4.0 * (m - k) * (n - k - 1) + 4.0 * (m - k) * m;
       fl += f;
       fl_item[t] += f;
-      by_item[t] += 16.0 * (m - k) * (n - k) + 16.0 * (m - k) * m;
+      if (!blocked) {
+        by_item[t] += 16.0 * (m - k) * (n - k) + 16.0 * (m - k) * m;
+      } else {
+        // one read of the trailing panel per step; one read+write per block of
+        // 32 reflectors (k = 32 b: the update of the previous block's rows).
+        by_item[t] += 8.0 * (m - k) * (n - k) + 8.0 * (m - k) * m;  // + Q formation reads V
+        if (k > 0 && k % 32 == 0) by_item[t] += 16.0 * (m - k + 32) * (n - k);
+      }
     }
     by_item[t] += 8.0 * m * n;  // initial column norms
   }

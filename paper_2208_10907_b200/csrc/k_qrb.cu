@@ -207,11 +207,13 @@ __global__ void __launch_bounds__(NT, 2) qrb_kernel(const QrJob* __restrict__ jo
   double r11 = -1.0;
   int rank = 0;
   bool stop = false;
+  long long t_piv = 0, t_lead = 0, t_pass = 0, t_mem = 0, t_upd = 0;  // H2G_QR_DEBUG cycle counters
   int k = 0;
   while (k < kmax && !stop) {
     const int k0 = k;
     int i = 0;
     for (; i < NB && k < kmax; ++i, ++k) {
+      long long tc0 = clock64();
       // ---- pivot: cluster max, then the lowest original index in the tie band
       double best = -1.0;
       for (int q = 0; q < G; ++q) best = fmax(best, cluster.map_shared_rank(&slot, q)->d);
@@ -245,6 +247,8 @@ __global__ void __launch_bounds__(NT, 2) qrb_kernel(const QrJob* __restrict__ jo
           sel = o->pos;
         }
       }
+      long long tc1 = clock64();
+      t_piv += tc1 - tc0;
       // ---- lead: swap, bring the pivot column up to date, stop tests, reflector
       if (lead) {
         if (sel != k) {
@@ -317,6 +321,8 @@ __global__ void __launch_bounds__(NT, 2) qrb_kernel(const QrJob* __restrict__ jo
         stop = true;
         break;
       }
+      long long tc2 = clock64();
+      t_lead += tc2 - tc1;
       // ---- every CTA: the new reflector into its block copy
       const double* vk = S.V + int64_t(k) * m;
       for (int r = tid; r < m; r += NT) {
@@ -347,17 +353,22 @@ __global__ void __launch_bounds__(NT, 2) qrb_kernel(const QrJob* __restrict__ jo
         double acc[TC];
 #pragma unroll
         for (int c = 0; c < TC; ++c) acc[c] = 0.0;
-        for (int r = k + lane; r < m; r += 32) {
-          const double vr = vsh[r];
-          double a[TC];
+        // Rows in 16-byte pairs from the even row ke <= k (ldw is even, so
+        // every pair is aligned): 16 columns x 16 bytes in flight per lane.
+        const int ke = k & ~1;
+        for (int r = ke + 2 * lane; r < m; r += 64) {
+          const double v0 = r >= k ? vsh[r] : 0.0, v1 = r + 1 < m ? vsh[r + 1] : 0.0;
+          double2 a[TC];
 #pragma unroll
-          for (int c = 0; c < TC; ++c) a[c] = (c >= c0 && c < cnt) ? __ldcg(&base[int64_t(c) * ldw + r]) : 0.0;
-          if (r == k) {  // lane 0, first chunk: row k of the tile's columns
+          for (int c = 0; c < TC; ++c)
+            a[c] = (c >= c0 && c < cnt) ? __ldcg(reinterpret_cast<const double2*>(&base[int64_t(c) * ldw + r]))
+                                        : make_double2(0.0, 0.0);
+          if (r <= k && k <= r + 1) {  // row k of the tile's columns
 #pragma unroll
-            for (int c = 0; c < TC; ++c) rowk[warp * TC + c] = a[c];
+            for (int c = 0; c < TC; ++c) rowk[warp * TC + c] = r == k ? a[c].x : a[c].y;
           }
 #pragma unroll
-          for (int c = 0; c < TC; ++c) acc[c] = fma(vr, a[c], acc[c]);
+          for (int c = 0; c < TC; ++c) acc[c] = fma(v1, a[c].y, fma(v0, a[c].x, acc[c]));
         }
         __syncwarp();
 #pragma unroll
@@ -396,58 +407,120 @@ __global__ void __launch_bounds__(NT, 2) qrb_kernel(const QrJob* __restrict__ jo
         const double mx = block_max(lmax, redd);
         if (tid == 0) slot.d = mx;
       }
+      long long tc3 = clock64();
+      t_pass += tc3 - tc2;
       cluster.sync();  // every column's norm of this step is in place
       member_masses(k);
       cluster.sync();
       members_not_done = false;
       for (int g = 0; g < nmem; ++g) members_not_done |= __ldcg(&S.acc[g]) > __ldcg(&S.mt[g]);
       ++rank;
+      t_mem += clock64() - tc3;
     }
+    long long tb0 = clock64();
     // ---- block end: rank-nb trailing update + exact norms of the trailing columns
     const int nb = rank - k0;
     if (stop || k >= kmax || nb == 0) break;
+    // W(k0:m, trailing) -= V_blk F_blk^T on the DMMA path: a warp takes 8
+    // consecutive trailing columns (8-aligned local index, so contiguous
+    // positions), keeps their F rows as B fragments in registers and walks
+    // the rows in 16-row fragments (C loaded, two m16n8k16 steps with A = -V
+    // from shared memory, stored back); the updated column norms over rows
+    // >= k accumulate on the fly.
     lmax = -1.0;
     const int l1 = own.below(k);
-    constexpr int RPL = 12;  // rows per lane (m <= 384)
-    for (int li = l1 + warp; li < nloc; li += NW) {
-      const int j = own.l2g(li);
-      double* col = W + int64_t(j) * ldw;
-      const double fj = lane < nb ? S.F[int64_t(lane) * n + j] : 0.0;
-      double a[RPL];
+    const int g = lane >> 2, tq = lane & 3;
+    for (int lg = (l1 & ~7) + warp * 8; lg < nloc; lg += NW * 8) {
+      const int c0 = lg < l1 ? l1 - lg : 0;
+      const int cnt = min(8, nloc - lg);
+      const int jb = own.l2g(lg);
+      // B fragments: b_i = F(kk + tq + 4i, jb + g), zero past nb / dead columns.
+      double bf[2][4];
 #pragma unroll
-      for (int u = 0; u < RPL; ++u) {
-        const int r = k0 + lane + 32 * u;
-        a[u] = r < m ? col[r] : 0.0;
-      }
-      for (int t = 0; t < nb; ++t) {
-        const double f = __shfl_sync(0xffffffffu, fj, t);
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int u = 0; u < RPL; ++u) {
-          const int r = k0 + lane + 32 * u;
-          if (r < m) a[u] = fma(-VB(r, t), f, a[u]);
+        for (int q = 0; q < 4; ++q) {
+          const int t = 16 * h + tq + 4 * q;
+          bf[h][q] = (t < nb && g >= c0 && g < cnt) ? S.F[int64_t(t) * n + jb + g] : 0.0;
+        }
+      // This lane's C columns: jb + 2 tq + {0, 1}.
+      const bool live0 = 2 * tq >= c0 && 2 * tq < cnt, live1 = 2 * tq + 1 >= c0 && 2 * tq + 1 < cnt;
+      double* col0 = W + int64_t(jb + 2 * tq) * ldw;
+      double* col1 = col0 + ldw;
+      double s0 = 0.0, s1 = 0.0;
+      for (int r0 = k0; r0 < m; r0 += 16) {
+        double c[4];
+        const int ra = r0 + g, rb = r0 + g + 8;
+        c[0] = (live0 && ra < m) ? col0[ra] : 0.0;
+        c[1] = (live1 && ra < m) ? col1[ra] : 0.0;
+        c[2] = (live0 && rb < m) ? col0[rb] : 0.0;
+        c[3] = (live1 && rb < m) ? col1[rb] : 0.0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double af[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int r = r0 + g + 8 * (q % 2), t = 16 * h + tq + 4 * (q / 2);
+            af[q] = (r < m && t < nb) ? -VB(r, t) : 0.0;  // stale columns may hold NaN patterns
+          }
+          asm("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, "
+              "{%4,%5,%6,%7,%8,%9,%10,%11}, {%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+              : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+              : "d"(af[0]), "d"(af[1]), "d"(af[2]), "d"(af[3]), "d"(af[4]), "d"(af[5]), "d"(af[6]), "d"(af[7]),
+                "d"(bf[h][0]), "d"(bf[h][1]), "d"(bf[h][2]), "d"(bf[h][3]));
+        }
+        if (ra < m) {
+          if (live0) col0[ra] = c[0];
+          if (live1) col1[ra] = c[1];
+          if (ra >= k) {
+            s0 = fma(c[0], c[0], s0);
+            s1 = fma(c[1], c[1], s1);
+          }
+        }
+        if (rb < m) {
+          if (live0) col0[rb] = c[2];
+          if (live1) col1[rb] = c[3];
+          if (rb >= k) {
+            s0 = fma(c[2], c[2], s0);
+            s1 = fma(c[3], c[3], s1);
+          }
         }
       }
-      double s = 0.0;
+      // Column norms: reduce over the 8 lanes with the same tq (g = lane >> 2).
 #pragma unroll
-      for (int u = 0; u < RPL; ++u) {
-        const int r = k0 + lane + 32 * u;
-        if (r < m) {
-          col[r] = a[u];
-          if (r >= k) s = fma(a[u], a[u], s);
+      for (int o = 4; o < 32; o <<= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      }
+      if (g == 0) {
+        if (live0) {
+          S.cn2[jb + 2 * tq] = s0;
+          lmax = fmax(lmax, s0);
+        }
+        if (live1) {
+          S.cn2[jb + 2 * tq + 1] = s1;
+          lmax = fmax(lmax, s1);
         }
       }
-      s = warp_sum(s);
-      if (lane == 0) S.cn2[j] = s;
-      lmax = fmax(lmax, s);
     }
     {
       const double mx = block_max(lmax, redd);
       if (tid == 0) slot.d = mx;
     }
     cluster.sync();
+    t_upd += clock64() - tb0;
   }
   cluster.sync();
 
+  if (lead && tid == 0 && job.dbg) {
+    job.dbg[0] = double(t_piv);
+    job.dbg[1] = double(t_lead);
+    job.dbg[2] = double(t_pass);
+    job.dbg[3] = double(t_mem);
+    job.dbg[4] = double(rank);
+    job.dbg[5] = double(n);
+    job.dbg[8] = double(t_upd);
+  }
   // form_q (linalg.cpp:181-185): Q = H_0 ... H_{rank-1} I; a warp per column
   // of Q, columns split over the cluster. Output row-major Q[i*m + j].
   {
