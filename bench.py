@@ -317,7 +317,7 @@ def run_b200_arm(args):
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     dom = max(kstats.items(), key=lambda kv: kv[1]["ms"]) if kstats else ("none", {})
     name, st = dom
-    traffic = load_traffic().get(name)
+    traffic = load_traffic().get("qr_exact" if (name == "qr" and qr_mode == "exact") else name)
     avg_ms = st["ms"] / max(1, st["launches"]) if st else 0.0
     bytes_per_launch = st["bytes"] / max(1, st["launches"]) if st else 0.0
     achieved = bytes_per_launch / (avg_ms * 1e-3) / 1e9 if avg_ms else 0.0
