@@ -87,6 +87,8 @@ double h2g_max_fill_residual(h2g_problem* p);
  * [fill_precompute, basis, skeleton, factorize, assemble, solve] following the
  * reference ledger rules (flops.hpp); launches = kernels launched so far. */
 int h2g_stats(h2g_problem* p, double* t5, double* f6, int64_t* launches);
+/* Kernel-function entries evaluated so far (FlopCounter::kernel_evals, flops.hpp). */
+int64_t h2g_kernel_evals(h2g_problem* p);
 
 /* Launch everything on a caller-owned cudaStream_t (before h2g_build). */
 int h2g_set_stream(h2g_problem* p, void* stream);

@@ -38,7 +38,7 @@ EXPORTS = [
     "h2g_basis_from_members", "h2g_lu_solve", "h2g_gemm", "h2g_stats_dev", "h2g_set_profile",
     "h2g_reset_profile", "h2g_kernel_stats", "h2g_set_stream", "h2g_phase_seconds",
     "h2g_nccl_unique_id", "h2g_comm_nccl", "h2g_comm_host", "h2g_comm_destroy", "h2g_set_comm",
-    "h2g_partition_range",
+    "h2g_partition_range", "h2g_kernel_evals",
 ]
 
 # h2g_host_allgather_fn (include/h2g.h)
@@ -101,6 +101,8 @@ def lib():
         L.h2g_comm_destroy.argtypes = [P]
         L.h2g_set_comm.argtypes = [P, P]
         L.h2g_partition_range.argtypes = [i64, ctypes.c_int, ctypes.c_int, P, P]
+        L.h2g_kernel_evals.argtypes = [P]
+        L.h2g_kernel_evals.restype = i64
         _lib = L
     return _lib
 
@@ -365,6 +367,7 @@ class Problem:
         n = ctypes.c_int64(0)
         self.L.h2g_stats(self.h, _p(t), _p(f), ctypes.byref(n))
         return dict(t_tree=t[0], t_classify=t[1], t_near=t[2], t_factor=t[3], t_solve=t[4],
+                    kernel_evals=int(self.L.h2g_kernel_evals(self.h)),
                     flops_fills=f[0], flops_basis=f[1], flops_skeleton=f[2], flops_factorize=f[3],
                     flops_assemble=f[4], flops_solve=f[5], launches=n.value)
 

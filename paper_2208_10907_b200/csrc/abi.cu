@@ -234,6 +234,8 @@ int64_t h2g_basis(h2g_problem* p, int level, int64_t k, int side, double* sq) {
 
 double h2g_max_fill_residual(h2g_problem* p) { return p->P.stats.max_fill_residual; }
 
+int64_t h2g_kernel_evals(h2g_problem* p) { return int64_t(p->P.c.kernel_evals); }
+
 int h2g_stats(h2g_problem* p, double* t5, double* f6, int64_t* launches) {
   const auto& s = p->P.stats;
   t5[0] = s.t_tree;

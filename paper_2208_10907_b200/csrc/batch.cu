@@ -220,7 +220,10 @@ void GemmBatch::run(Ctx& c, int tag) {
     for (int s = 0; s < jobs[j].nseg; ++s) {
       const GemmSeg& sg = segs[jobs[j].seg0 + s];
       fl += 2.0 * C.rows * double(sg.A.cols) * C.cols;
-      if (sg.gen) fl += double(sg.A.cols) * C.cols * (c.kp.kind == 0 ? 9 : 11);
+      if (sg.gen) {
+        fl += double(sg.A.cols) * C.cols * (c.kp.kind == 0 ? 9 : 11);
+        c.kernel_evals += double(sg.A.cols) * C.cols;
+      }
     }
     const int tm = (C.rows + bm - 1) / bm, tn = (C.cols + 63) / 64;
     for (int a = 0; a < tm; ++a)
@@ -257,6 +260,7 @@ void EvalBatch::run(Ctx& c, int tag) {
   double evn_ = 0;
   for (auto& j : jobs) evn_ += double(j.out.rows) * j.out.cols;
   const double ev_flops_ = evn_ * (c.kp.kind == 0 ? 9 : 11);
+  c.kernel_evals += evn_;
   c.add_flops(ev_flops_);
   if (tj.empty()) return;
   Slab k1, k2, k3;

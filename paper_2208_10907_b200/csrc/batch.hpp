@@ -28,6 +28,7 @@ struct Ctx {
   // statistics
   int64_t launches = 0;
   double flops = 0;  // algorithmic (reference counting rules)
+  double kernel_evals = 0;  // kernel-function entries evaluated (FlopCounter::kernel_evals)
   std::map<std::string, double> phase_flops;
   std::string phase = "other";
   void add_flops(double f) {

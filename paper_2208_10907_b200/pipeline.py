@@ -210,32 +210,12 @@ class Pipeline:
         return self.prob.solve(b)
 
     def report(self):
-        """Subset of RunReport::to_json (h2ulv-report/1, report.cpp:182-237)."""
-        self.factor()
-        st = self.prob.stats()
-        rep = {
-            "schema": "h2ulv-report/1",
-            "impl": "b200",
-            "config": {k: v for k, v in self.cfg.__dict__.items() if k != "points"},
-            "phase_seconds": {"tree": st["t_tree"], "classify": st["t_classify"],
-                              "assemble": st["t_near"], "factor": st["t_factor"]},
-            "phase_flops": {"fill_precompute": st["flops_fills"], "basis": st["flops_basis"],
-                            "skeleton": st["flops_skeleton"], "factorize": st["flops_factorize"]},
-            "factorization_flops": st["flops_fills"] + st["flops_factorize"],
-            "levels": [{"level": int(l), "max_rank": int(r.max()), "mean_rank": float(r.mean())}
-                       for l, r in self.prob.factor_levels()],
-            "max_fill_residual_rel": self.prob.max_fill_residual(),
-            "dependency_edges": 0,
-            "solve_rel_error": -1.0,
-            "total_seconds": self.build_seconds + self.factor_seconds,
-        }
-        if self.cfg.oracle and self.cfg.n <= self.cfg.oracle_guard:
-            ones = np.ones(self.cfg.n)
-            b = self.prob.matvec(ones)
-            x = self.solve_rhs(b)
-            rep["solve_rel_error"] = float(np.linalg.norm(x - ones) / np.linalg.norm(ones))
-        return rep
+        """RunReport (h2ulv-report/1, report.cpp:113-237) as a dict; see report.py."""
+        from .report import report_of
+        return report_of(self)
 
 
 def run_pipeline(cfg):
-    return Pipeline(cfg).report()
+    """run_pipeline (report.cpp:239-243)."""
+    from .report import run_report
+    return run_report(cfg)
