@@ -358,6 +358,7 @@ int h2g_lu_factor(int64_t n, const double* a, double tol, double* lu, int64_t* p
     h2g::LuBatch lb;
     lb.add(f, tol, "block");
     lb.run(P.c);
+    P.c.sync();  // completes the batch and reports a singular pivot
     h2g::cuda_check(cudaMemcpy(lu, f.lu.m.p, sizeof(double) * n * n, cudaMemcpyDeviceToHost), "d2h");
     h2g::cuda_check(cudaMemcpy(perm, f.perm, sizeof(int64_t) * n, cudaMemcpyDeviceToHost), "d2h");
   });

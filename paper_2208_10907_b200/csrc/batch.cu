@@ -44,7 +44,10 @@ void Ctx::check_err() {
   if (h.code == 1)
     throw std::runtime_error("assemble_block: singular evaluation (r + eta_reg == 0)");
   if (h.code == 2) {
-    std::string what = (h.job >= 0 && h.job < int(lu_names.size())) ? lu_names[h.job] : "block";
+    std::string what = "block";
+    auto it = lu_names.find(h.tag);
+    if (it != lu_names.end() && h.job >= 0 && h.job < int(it->second.size())) what = it->second[h.job];
+    lu_names.clear();
     throw std::runtime_error("singular block in LU of " + what + " at step " +
                              std::to_string(h.step));
   }
@@ -146,6 +149,7 @@ void Ctx::sync() {
   pin_head = 0;
   cuda_check(cudaStreamSynchronize(stream), "stream sync");
   check_err();
+  lu_names.clear();  // every LU batch launched so far has completed without error
 }
 
 std::vector<DMat> alloc_mats(Ctx& c, const std::vector<std::pair<int, int>>& shapes) {
@@ -338,7 +342,7 @@ void LuBatch::run(Ctx& c) {
   c.add_flops(fl);
   Slab k1;
   auto* dj = upload(c, jobs, k1);
-  c.lu_names = names;
+  c.lu_names[c.lu_tag + 1] = names;
   double by = 0;
   int max_n = 1;
   for (auto& j : jobs) {
@@ -350,8 +354,8 @@ void LuBatch::run(Ctx& c) {
   c.prof_end("lu", ev, fl, by);
   c.launches++;
   cuda_check(cudaGetLastError(), "lu launch");
-  // LU errors must be attributed to this batch's names: check now.
-  c.sync();
+  // A singular pivot surfaces at the next sync (check_err maps its tag to
+  // this batch's names).
 }
 
 // Blocked left solve (forward/backward substitution with GEMM updates between

@@ -57,7 +57,10 @@ struct Ctx {
   cudaEvent_t event(int i);
   void sync();            // stream sync + error word check
   void check_err();       // throws the reference's message for device errors
-  std::vector<std::string> lu_names;  // current LU batch names (for errors)
+  // Names of the LU batches launched since the last sync, by tag: a singular
+  // pivot is reported (with the reference's message) at the next sync
+  // without making every LU batch a synchronisation point.
+  std::map<int, std::vector<std::string>> lu_names;
   int lu_tag = 0;
   // Per-kernel CUDA-event timing on the launching stream (bench roofline).
   struct ProfAgg {
