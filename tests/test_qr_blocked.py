@@ -63,3 +63,27 @@ def test_qr_mode_validation():
     with pytest.raises(KeyError):
         p.set_options(qr_mode="fast")
     p.close()
+
+
+def test_blocked_matches_exact_on_bench_family():
+    """The bench workload family (Fibonacci sphere, Yukawa, leaf 256, cap 100,
+    tol 1e-6) at N = 16,384: blocked and exact QR give the same solve
+    residual to 1e-6 relative and the same per-level rank sums."""
+    from paper_2208_10907_b200.pipeline import _fib_spheres
+    n = 16384
+    xyz, q = _fib_spheres(n, 1, 3.0, 42)
+    b = np.random.default_rng(7).uniform(-1, 1, n)
+    out = {}
+    for mode in ("exact", "blocked"):
+        p = h2.Problem()
+        p.set_kernel("yukawa", 1.0, 1.0, 1e-3)
+        p.set_options(tol=1e-6, cap=100, qr_mode=mode)
+        p.build(xyz, q, 256)
+        p.factor()
+        x = p.solve(b)
+        r = float(np.linalg.norm(p.matvec(x) - b) / np.linalg.norm(b))
+        out[mode] = (r, [int(rk.sum()) for _, rk in p.factor_levels()])
+        p.close()
+    (re, ke), (rb, kb) = out["exact"], out["blocked"]
+    assert abs(rb - re) <= 1e-6 * re, (rb, re)
+    assert all(abs(a - c) <= 0.01 * a for a, c in zip(ke, kb)), (ke, kb)
