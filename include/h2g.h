@@ -35,7 +35,7 @@ typedef struct {
   double rr_pivot_tol;          /* 1e-13 */
   int32_t absorb_coupling;      /* 1 */
   double abort_residual_factor; /* 100 */
-  int32_t structure;            /* 0 = h2 (strong, nodep), 1 = hss (weak) */
+  int32_t structure;            /* 0 = h2 (strong, nodep), 1 = hss (weak), 2 = blr2 (flat, weak) */
   double eta;                   /* strong admissibility eta (1.0) */
   int64_t qr_mem_budget;        /* bytes of QR working memory per chunk, <= 0: default */
   int32_t qr_mode;              /* 0 = exact (the reference's rounding, bit-exact),

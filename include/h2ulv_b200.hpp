@@ -99,7 +99,7 @@ inline PointCloud generate_line(int64_t n, uint64_t seed) {
 
 // ---- kernels / structure (kernels.hpp:11-39, geometry.hpp:60-67, hstructure.hpp:15)
 enum class KernelKind { laplace, yukawa };
-enum class StructureVariant { h2, hss };
+enum class StructureVariant { blr2, hss, h2 };  // hstructure.hpp:15
 enum class AdmissibilityKind { weak, strong };
 struct AdmissibilityRule {
   AdmissibilityKind kind = AdmissibilityKind::strong;
@@ -138,7 +138,7 @@ inline std::shared_ptr<Handle> build(const PointCloud& cloud, int64_t leaf, cons
                                      std::optional<int64_t> cap, bool absorb, int qr_mode = 0) {
   auto h = std::make_shared<Handle>();
   h2g_kernel hk{k.kind == KernelKind::laplace ? 0 : 1, k.alpha_m, k.permittivity_scale, k.eta_reg};
-  h2g_options o{tol, cap.value_or(0), 1e-13, absorb ? 1 : 0, 100.0, v == StructureVariant::h2 ? 0 : 1, eta, 0, qr_mode};
+  h2g_options o{tol, cap.value_or(0), 1e-13, absorb ? 1 : 0, 100.0, v == StructureVariant::h2 ? 0 : v == StructureVariant::hss ? 1 : 2, eta, 0, qr_mode};
   check(h2g_set_kernel(h->p, &hk));
   check(h2g_set_options(h->p, &o));
   std::vector<double> xyz;
@@ -228,7 +228,7 @@ inline BlockStructure read_lists(h2g_problem* p) {
 // makes of `cloud` (the tree is deterministic, so it is rebuilt on the GPU).
 inline BlockStructure classify_blocks(const PointCloud& cloud, int64_t leaf_size, const AdmissibilityRule& rule,
                                       StructureVariant v = StructureVariant::h2) {
-  if (rule.kind == AdmissibilityKind::weak) v = StructureVariant::hss;
+  if (rule.kind == AdmissibilityKind::weak && v == StructureVariant::h2) v = StructureVariant::hss;
   auto h = detail::build(cloud, leaf_size, KernelSpec{}, rule.eta, v, 1e-8, std::nullopt, true);
   return detail::read_lists(h->p);
 }

@@ -87,6 +87,7 @@ int h2g_set_options(h2g_problem* p, const h2g_options* o) {
     op.rr_pivot_tol = o->rr_pivot_tol;
     op.absorb_coupling = o->absorb_coupling != 0;
     op.abort_residual_factor = o->abort_residual_factor;
+    if (o->structure < 0 || o->structure > 2) throw std::invalid_argument("config: structure must be h2, hss or blr2");
     op.structure = o->structure;
     op.eta = o->eta;
     if (o->qr_mode != 0 && o->qr_mode != 1) throw std::invalid_argument("config: qr_mode must be 0 (exact) or 1 (blocked)");

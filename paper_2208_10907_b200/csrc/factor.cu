@@ -128,7 +128,36 @@ void Problem::build(const double* d_xyz, const double* d_q, int64_t n, int64_t l
              "be d2h");
   c.sync();
   double t1 = now_s();
-  classify_device(T, opt.eta, opt.structure == 1 ? 1 : 0, S, c.stream);
+  classify_device(T, opt.eta, opt.structure != 0 ? 1 : 0, S, c.stream);
+  if (opt.structure == 2) {
+    // BLR^2 (classify_blocks, hstructure.cpp:75-87): flat, every leaf pair
+    // classified at the leaf level with the weak rule -- the diagonal block is
+    // dense, every other leaf pair is far -- and no coarser levels.
+    const int L = T.levels;
+    for (int l = 1; l < L; ++l) {
+      const int64_t m = int64_t(1) << l;
+      S.level[l].near_ptr.assign(m + 1, 0);
+      S.level[l].far_ptr.assign(m + 1, 0);
+      S.level[l].near_idx.clear();
+      S.level[l].far_idx.clear();
+    }
+    const int64_t m = int64_t(1) << L;
+    auto& lv = S.level[L];
+    lv.near_ptr.resize(m + 1);
+    lv.far_ptr.resize(m + 1);
+    lv.near_idx.resize(m);
+    lv.far_idx.resize(m * (m - 1));
+    for (int64_t i = 0; i <= m; ++i) {
+      lv.near_ptr[i] = i;
+      lv.far_ptr[i] = i * (m - 1);
+    }
+    for (int64_t i = 0; i < m; ++i) {
+      lv.near_idx[i] = i;
+      int64_t t = i * (m - 1);
+      for (int64_t j = 0; j < m; ++j)
+        if (j != i) lv.far_idx[t++] = j;
+    }
+  }
   double t2 = now_s();
   c.cloud = Cloud{T.x, T.y, T.z, T.q, n};
   {
@@ -1337,6 +1366,43 @@ struct Driver {
     lb.run(c);
   }
 
+  // ---- finish_blr2 (ulv.cpp:762-781) ---------------------------------------------
+  // The flat variant's remaining skeleton grid is the top system itself:
+  // diagonal SS corners, far and dense skeleton couplings, one LU.
+  void finish_blr2(const SysL& sys, const std::vector<DMat>& diag_S,
+                   const std::map<std::pair<int64_t, int64_t>, DMat>& far_ss,
+                   const std::map<std::pair<int64_t, int64_t>, DMat>& dense_ss) {
+    PhaseTimer pt(c, P.stats, "factorize");
+    const int64_t m = sys.m;
+    const auto& Ub = P.U[sys.lvl];
+    P.cutoff_level = sys.lvl;
+    P.cutoff_dims.assign(m, 0);
+    std::vector<int64_t> off(m + 1, 0);
+    for (int64_t k = 0; k < m; ++k) {
+      P.cutoff_dims[k] = Ub[k].rank;
+      off[k + 1] = off[k] + Ub[k].rank;
+    }
+    P.top = alloc_lu(c, int(off[m]));
+    const Mat A = P.top.lu.m;
+    CopyBatch zb, cb;
+    zb.zero(A);
+    for (int64_t k = 0; k < m; ++k) {
+      const int r = Ub[k].rank;
+      if (r == 0) continue;
+      const int rd = diag_S[k].rows() - r;
+      cb.copy(A.sub(int(off[k]), int(off[k]), r, r), diag_S[k].m.sub(rd, rd, r, r));
+    }
+    for (const auto* ss : {&far_ss, &dense_ss})
+      for (auto& [key, SS] : *ss)
+        if (SS.rows() && SS.cols())
+          cb.copy(A.sub(int(off[key.first]), int(off[key.second]), SS.rows(), SS.cols()), SS.m);
+    zb.run(c);
+    cb.run(c);
+    LuBatch lb;
+    lb.add(P.top, 1e-15, "top system");
+    lb.run(c);
+  }
+
   // ---- lift_layer (compression.cpp:302-322) --------------------------------------
   void make_layer(int lvl) {
     const int64_t m = int64_t(1) << lvl;
@@ -1475,6 +1541,12 @@ struct Driver {
       mark("project_pieces");
       make_layer(sys.lvl);
       big_owner = std::move(big_owner_next_);
+      if (opt.structure == 2) {  // BLR^2: one level, then the flat top system
+        finish_blr2(sys, diag_S, far_ss, dense_ss);
+        lf.sys = std::move(sys);
+        P.levels.push_back(std::move(lf));
+        break;
+      }
       SysL next = merge(sys, diag_S, far_ss, dense_ss);
       mark("layer+merge");
       lf.sys = std::move(sys);
@@ -1656,8 +1728,16 @@ void Problem::solve(const double* d_b, double* d_x, int nrhs) {
   }
   std::vector<Mat> ys;
   {
+    // The downward pass splits parent segments into their children; a top
+    // system at the last factorized level itself (BLR^2) is regrouped by pairs.
+    std::vector<int> seg(cutoff_dims.begin(), cutoff_dims.end());
+    if (!levels.empty() && cutoff_level == levels.back().level) {
+      std::vector<int> pairs;
+      for (size_t k = 0; k + 1 < seg.size(); k += 2) pairs.push_back(seg[k] + seg[k + 1]);
+      seg = pairs;
+    }
     int at = 0;
-    for (int d : cutoff_dims) {
+    for (int d : seg) {
       ys.push_back(y.m.sub(at, 0, d, nrhs));
       at += d;
     }

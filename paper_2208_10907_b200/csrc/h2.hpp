@@ -20,7 +20,7 @@ struct Options {  // FactorOptions (ulv.hpp:29-45) + RunConfig bits
   double rr_pivot_tol = 1e-13;
   bool absorb_coupling = true;
   double abort_residual_factor = 100.0;
-  int structure = 0;  // 0 h2 (strong, nodep), 1 hss (weak)
+  int structure = 0;  // 0 h2 (strong, nodep), 1 hss (weak), 2 blr2 (flat, weak)
   double eta = 1.0;
   size_t qr_mem_budget = size_t(8) << 30;  // auto (free/3) unless set
   int qr_mode = 0;  // 0 exact (k_qr.cu, bit-exact), 1 blocked (k_qrb.cu, tolerance parity)

@@ -109,7 +109,7 @@ class RunConfig:
             raise ValueError("config: eta must be positive")
         if self.geometry not in ("cube", "line", "sphere", "uniform_sphere", "ellipsoids"):
             raise ValueError("config: unknown geometry " + self.geometry)
-        if self.structure not in ("h2", "hss"):
+        if self.structure not in ("h2", "hss", "blr2"):
             raise ValueError("config: unknown structure " + self.structure)
 
 

@@ -76,7 +76,7 @@ def _config_json(cfg):
     if cfg.geometry == "sphere":
         c["spheres"] = cfg.spheres
         c["spacing"] = cfg.spacing
-    c["admissibility"] = "weak" if cfg.structure == "hss" else "strong"
+    c["admissibility"] = "weak" if cfg.structure in ("hss", "blr2") else "strong"
     c["eta"] = cfg.eta
     c["structure"] = cfg.structure
     c["variant"] = "nodep"

@@ -222,3 +222,27 @@ def test_ragged_sizes_vs_live_reference(n, leaf):
     rr = np.linalg.norm(r.dense_matvec(xr) - b) / np.linalg.norm(b)
     rg = np.linalg.norm(p.matvec(xg) - b) / np.linalg.norm(b)
     assert abs(rr - rg) <= 0.05 * rr + 1e-12
+
+
+@pytest.mark.skipif(not has_ref(), reason="reference library oracle/_ref not built on this host")
+@pytest.mark.parametrize("n,leaf", [(1024, 128), (2048, 128)])
+def test_blr2_bitwise_vs_live_reference(n, leaf):
+    """BLR^2 (flat structure, finish_blr2 top system, ulv.cpp:762-781) through
+    the same kernels: ranks and the solution bit-identical to the reference."""
+    xyz, q = cpu.generate("cube", n, 42)
+    cfg = ref.make_config(leaf, reg=1e-3, scale=1.0, structure="blr2")
+    r = ref.RefRun(xyz, q, cfg).build().factor()
+    p = h2.Problem()
+    p.set_kernel("laplace", 0.0, 1.0, 1e-3)
+    p.set_options(tol=1e-8, structure="blr2")
+    p.build(xyz, q, leaf)
+    L = p.levels
+    assert p.lists(L, 0)[1].tolist() == list(range(1 << L))  # only the diagonal is dense
+    assert all(len(p.lists(l, 0)[1]) == 0 for l in range(1, L))
+    p.factor()
+    got = {int(l): rk.tolist() for l, rk in p.factor_levels()}
+    assert got == {int(l): list(map(int, rk)) for l, rk in r.factor_levels()}
+    b = ref.splitmix_signed(n, 7)
+    xr, xg = r.solve(b), p.solve(b)
+    assert np.array_equal(xg.view(np.int64), xr.view(np.int64))
+    assert np.linalg.norm(p.matvec(xg) - b) / np.linalg.norm(b) < 1e-6
