@@ -123,27 +123,8 @@ Ctx::~Ctx() {
   // The owner may already have destroyed the stream; cudaFreeHost waits for
   // the device itself.
   if (pin) cudaFreeHost(pin);
-  for (auto s : sides) cudaStreamDestroy(s);
-  for (auto e : evs) cudaEventDestroy(e);
 }
 
-cudaStream_t Ctx::side_stream(int i) {
-  while (int(sides.size()) <= i) {
-    cudaStream_t s = nullptr;
-    cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "side stream");
-    sides.push_back(s);
-  }
-  return sides[i];
-}
-
-cudaEvent_t Ctx::event(int i) {
-  while (int(evs.size()) <= i) {
-    cudaEvent_t e = nullptr;
-    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-    evs.push_back(e);
-  }
-  return evs[i];
-}
 
 void Ctx::sync() {
   pin_head = 0;

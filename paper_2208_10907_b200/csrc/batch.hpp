@@ -47,14 +47,6 @@ struct Ctx {
   Ctx(const Ctx&) = delete;
   Ctx& operator=(const Ctx&) = delete;
   ~Ctx();
-  // Side streams (fork/join from `stream` with the pooled events) for
-  // independent launches that should run concurrently.
-  // QR mode: exact (the reference's rounding, k_qr.cu) or blocked (k_qrb.cu).
-  bool qr_blocked = getenv("H2G_QR_MODE") && std::string(getenv("H2G_QR_MODE")) == "blocked";  // per problem: Options::qr_mode
-  std::vector<cudaStream_t> sides;
-  std::vector<cudaEvent_t> evs;
-  cudaStream_t side_stream(int i);
-  cudaEvent_t event(int i);
   void sync();            // stream sync + error word check
   void check_err();       // throws the reference's message for device errors
   // Names of the LU batches launched since the last sync, by tag: a singular
