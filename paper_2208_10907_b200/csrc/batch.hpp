@@ -47,6 +47,9 @@ struct Ctx {
   Ctx(const Ctx&) = delete;
   Ctx& operator=(const Ctx&) = delete;
   ~Ctx();
+  // QR mode: exact (the reference's rounding, k_qr.cu) or blocked (k_qrb.cu);
+  // set per factorization from Options::qr_mode (H2G_QR_MODE overrides).
+  bool qr_blocked = false;
   void sync();            // stream sync + error word check
   void check_err();       // throws the reference's message for device errors
   // Names of the LU batches launched since the last sync, by tag: a singular
