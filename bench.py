@@ -8,10 +8,11 @@ so the diagonal is 1e3), leaf 256, strong admissibility eta = 1, rank cap
 100, tol 1e-6 (tol 1e-8 with cap 100 makes the reference abort with "basis
 does not absorb fill-in" at leaf 256; measured).
 
-QR mode: blocked by default (member-panel Householder reflectors applied 32
-at a time; the reference's pivoting/stopping rules; solve residual equal to
-the reference's within 1e-6 relative, tests/test_qr_blocked.py); the line's
-"exact_qr" field times the same step with the bit-exact per-step QR.
+QR mode: compressed by default (each member of a box's basis panel replaced
+by a pivoted-Cholesky factor of its Gram matrix -- same range, same member
+masses -- then the blocked QR; the reference's pivoting/stopping rules on the
+compressed panel; parity within tolerance, tests/test_qr_blocked.py); the
+line's "exact_qr" field times the same step with the bit-exact per-step QR.
 
 A step = one pass of the hot path from device-resident points: cluster tree
 + admissibility lists + near-field arena (Pipeline::build), fill-in
@@ -46,6 +47,7 @@ WORKLOAD = dict(workload="c2_sphere_yukawa", n=65536, geometry="sphere(fibonacci
                 tol=1e-6, structure="h2/nodep")
 CPU_SAMPLE_N = 8192  # reference CPU sample: same workload family at N = 8192
 METRIC = "h2ulv_points_per_sec"
+FP64_DMMA_TFLOPS = 37.18  # profiles/r01_fp64_peak_probe.txt
 UNIT = "points/s"
 
 
@@ -317,16 +319,28 @@ def run_b200_arm(args):
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     dom = max(kstats.items(), key=lambda kv: kv[1]["ms"]) if kstats else ("none", {})
     name, st = dom
-    traffic = load_traffic().get("qr_exact" if (name == "qr" and qr_mode == "exact") else name)
+    traffic = load_traffic().get({"exact": "qr_exact", "blocked": "qr", "compressed": "qr_compressed"}[qr_mode]
+                                 if name == "qr" else name)
     avg_ms = st["ms"] / max(1, st["launches"]) if st else 0.0
     bytes_per_launch = st["bytes"] / max(1, st["launches"]) if st else 0.0
-    achieved = bytes_per_launch / (avg_ms * 1e-3) / 1e9 if avg_ms else 0.0
-    roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": hbm_peak,
-                "unit": "GB/s", "frac": achieved / hbm_peak if hbm_peak else None,
-                "traffic": traffic.get("bytes_per_launch") if traffic else None,
-                "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
-                "share_of_step": st["ms"] * 1e-3 / max(1e-12, t_phase["build"] + t_phase["factor"] + t_phase["solve"]) if st else None}
+    flops_per_launch = st["flops"] / max(1, st["launches"]) if st else 0.0
+    if name == "gemm":
+        # DMMA-bound: FP64 tensor peak from our own probe (MEASURED_PEAKS.json has no FP64 figure)
+        achieved = flops_per_launch / (avg_ms * 1e-3) / 1e12 if avg_ms else 0.0
+        roofline = {"bound": "tensor", "kernel": name, "achieved": achieved, "peak": FP64_DMMA_TFLOPS,
+                    "unit": "TFLOP/s", "frac": achieved / FP64_DMMA_TFLOPS,
+                    "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                    "algorithmic_flops_per_launch": flops_per_launch, "avg_launch_ms": avg_ms,
+                    "peak_source": "profiles/r01_fp64_peak_probe.txt (DMMA m16n8k16, measured on B200)",
+                    "share_of_step": st["ms"] * 1e-3 / max(1e-12, t_phase["build"] + t_phase["factor"] + t_phase["solve"]) if st else None}
+    else:
+        achieved = bytes_per_launch / (avg_ms * 1e-3) / 1e9 if avg_ms else 0.0
+        roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": hbm_peak,
+                    "unit": "GB/s", "frac": achieved / hbm_peak if hbm_peak else None,
+                    "traffic": traffic.get("bytes_per_launch") if traffic else None,
+                    "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_ms,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
+                    "share_of_step": st["ms"] * 1e-3 / max(1e-12, t_phase["build"] + t_phase["factor"] + t_phase["solve"]) if st else None}
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.skip_cpu:
@@ -377,9 +391,11 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override N (testing only)")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--skip-cpu", action="store_true")
-    ap.add_argument("--qr-mode", default="blocked", choices=["blocked", "exact"],
-                    help="member-panel QR: blocked (32 reflectors per panel update, parity within "
-                         "tolerance) or exact (the reference's rounding, bit-exact)")
+    ap.add_argument("--qr-mode", default="compressed", choices=["compressed", "blocked", "exact"],
+                    help="member-panel QR: compressed (members replaced by pivoted-Cholesky factors "
+                         "of their Gram matrices, then blocked QR), blocked (32 reflectors per panel "
+                         "update) -- both parity within tolerance -- or exact (the reference's "
+                         "rounding, bit-exact)")
     ap.add_argument("--exact-steps", type=int, default=1,
                     help="extra device-timed steps in exact QR mode, reported beside the headline")
     ap.add_argument("--replicas", action="store_true",

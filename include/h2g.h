@@ -40,7 +40,11 @@ typedef struct {
   int64_t qr_mem_budget;        /* bytes of QR working memory per chunk, <= 0: default */
   int32_t qr_mode;              /* 0 = exact (the reference's rounding, bit-exact),
                                    1 = blocked (NB = 32 reflectors per panel update;
-                                   same decisions, parity within tolerance) */
+                                   same decisions, parity within tolerance),
+                                   2 = compressed (each member of width >= 48 replaced by
+                                   a pivoted-Cholesky factor of its Gram matrix, then the
+                                   blocked QR; same stopping rule, tolerance parity,
+                                   meant for tol >= 1e-7) */
 } h2g_options;
 
 const char* h2g_last_error(void);

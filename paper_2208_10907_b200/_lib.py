@@ -217,7 +217,7 @@ class Problem:
     def set_options(self, tol=1e-8, cap=None, rr_pivot_tol=1e-13, absorb_coupling=True,
                     abort_residual_factor=100.0, structure="h2", eta=1.0, qr_mem_budget=0, qr_mode="exact"):
         o = Options(tol, cap or 0, rr_pivot_tol, 1 if absorb_coupling else 0, abort_residual_factor,
-                    {"h2": 0, "hss": 1, "blr2": 2}[structure], eta, qr_mem_budget, {"exact": 0, "blocked": 1}[qr_mode])
+                    {"h2": 0, "hss": 1, "blr2": 2}[structure], eta, qr_mem_budget, {"exact": 0, "blocked": 1, "compressed": 2}[qr_mode])
         _check(self.L.h2g_set_options(self.h, ctypes.byref(o)))
 
     def build(self, xyz, q, leaf):

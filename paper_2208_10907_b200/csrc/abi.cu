@@ -90,7 +90,8 @@ int h2g_set_options(h2g_problem* p, const h2g_options* o) {
     if (o->structure < 0 || o->structure > 2) throw std::invalid_argument("config: structure must be h2, hss or blr2");
     op.structure = o->structure;
     op.eta = o->eta;
-    if (o->qr_mode != 0 && o->qr_mode != 1) throw std::invalid_argument("config: qr_mode must be 0 (exact) or 1 (blocked)");
+    if (o->qr_mode < 0 || o->qr_mode > 2)
+      throw std::invalid_argument("config: qr_mode must be 0 (exact), 1 (blocked) or 2 (compressed)");
     op.qr_mode = o->qr_mode;
     if (o->qr_mem_budget > 0) {
       op.qr_mem_budget = size_t(o->qr_mem_budget);

@@ -233,7 +233,8 @@ void GemmBatch::run(Ctx& c, int tag) {
   }
   auto ev = c.prof_begin();
   launch_gemm(dj, ds, dt, int(tiles.size()), bm, c.kp, c.cloud, c.err, tag, c.stream);
-  c.prof_end(c.prof_detail ? ("gemm@" + c.phase).c_str() : "gemm", ev, fl, by);
+  const std::string nm = name ? name : "gemm";
+  c.prof_end(c.prof_detail ? (nm + "@" + c.phase).c_str() : nm.c_str(), ev, fl, by);
   c.launches++;
   cuda_check(cudaGetLastError(), "gemm launch");
 }
@@ -473,7 +474,136 @@ void SolveBatch::run(Ctx& c) {
   cuda_check(cudaGetLastError(), "solve launch");
 }
 
+// Compressed QR mode (qr_mode = 2): every member at least kPcholMinWidth wide
+// is replaced by the columns of a pivoted Cholesky factor of its Gram matrix
+// (k_pchol.cu), so the pivoted QR sees the same range and the same member
+// masses (up to a dropped trace <= eta) on a panel whose width is the sum of
+// the members' numerical ranks instead of O(N). G = M M^T runs as one batched
+// GEMM (DMMA) reading each member once.
+static constexpr int kPcholMinWidth = 48;
+
+static void compress_members(Ctx& c, std::vector<QrBatch::Item>& items, size_t mem_budget) {
+  struct Wide {
+    size_t item;
+    int mem, w, kmax;
+  };
+  std::vector<Wide> wide;
+  for (size_t t = 0; t < items.size(); ++t) {
+    const auto& it = items[t];
+    if (it.m == 0 || it.n == 0) continue;
+    for (size_t s = 0; s + 1 < it.offs.size(); ++s) {
+      const int w = int(it.offs[s + 1] - it.offs[s]);
+      if (w >= kPcholMinWidth) wide.push_back({t, int(s), w, std::min(it.m, w)});
+    }
+  }
+  if (wide.empty()) return;
+  std::vector<std::vector<DMat>> comp(items.size());  // per item, per member (wide only)
+  for (size_t t = 0; t < items.size(); ++t) comp[t].resize(items[t].offs.size() > 0 ? items[t].offs.size() - 1 : 0);
+  size_t g0 = 0;
+  while (g0 < wide.size()) {
+    size_t g1 = g0, bytes = 0;
+    while (g1 < wide.size()) {
+      const int m = items[wide[g1].item].m;
+      const size_t need = sizeof(double) * size_t(m) * (m + wide[g1].kmax) + 64;
+      if (g1 > g0 && bytes + need > mem_budget / 2) break;
+      bytes += need;
+      ++g1;
+    }
+    std::vector<std::pair<int, int>> shapes;
+    for (size_t g = g0; g < g1; ++g) {
+      const int m = items[wide[g].item].m;
+      shapes.push_back({m, m});
+      shapes.push_back({m, wide[g].kmax});
+    }
+    std::vector<DMat> gr = alloc_mats(c, shapes);
+    Slab kc = c.alloc(sizeof(int) * (g1 - g0));
+    int* dcount = static_cast<int*>(kc.get());
+    GemmBatch gb;
+    gb.name = "gram";
+    std::vector<PcholJob> pj;
+    int max_m = 1, max_k = 1;
+    for (size_t g = g0; g < g1; ++g) {
+      const auto& it = items[wide[g].item];
+      const Mat A = it.concat.m.sub(0, int(it.offs[wide[g].mem]), it.m, wide[g].w);
+      const DMat& G = gr[2 * (g - g0)];
+      const DMat& R = gr[2 * (g - g0) + 1];
+      gemm1(gb, G.m, A, A.t());
+      const double mt = it.tol * 0.5;  // member_tol (compression.hpp:67)
+      const double eta = std::max(64.0 * 2.220446049250313e-16, 0.01 * mt * mt);
+      pj.push_back({G.m.p, G.m.cs, R.m.p, R.m.cs, it.m, wide[g].kmax, eta, dcount + (g - g0)});
+      max_m = std::max(max_m, it.m);
+      max_k = std::max(max_k, wide[g].kmax);
+    }
+    gb.run(c);
+    Slab kj;
+    auto* dj = upload(c, pj, kj);
+    auto ev = c.prof_begin();
+    launch_pchol(dj, int(pj.size()), max_m, max_k, c.stream);
+    c.prof_end("pchol", ev, 0.0, 0.0);
+    c.launches++;
+    cuda_check(cudaGetLastError(), "pchol launch");
+    std::vector<int> cnt(g1 - g0);
+    cuda_check(cudaMemcpyAsync(cnt.data(), dcount, sizeof(int) * cnt.size(), cudaMemcpyDeviceToHost, c.stream),
+               "pchol counts");
+    c.sync();
+    double fl = 0;
+    std::vector<std::pair<int, int>> cs;
+    for (size_t g = g0; g < g1; ++g) {
+      const int m = items[wide[g].item].m, k = cnt[g - g0];
+      fl += double(m) * k * k;  // left-looking updates: m * k^2 / 2 FMAs
+      cs.push_back({m, std::max(k, 0)});
+    }
+    c.add_flops(fl);
+    std::vector<DMat> cm = alloc_mats(c, cs);
+    CopyBatch cb;
+    for (size_t g = g0; g < g1; ++g) {
+      const int k = cnt[g - g0];
+      if (k > 0) cb.copy(cm[g - g0].m, gr[2 * (g - g0) + 1].m.sub(0, 0, items[wide[g].item].m, k));
+      comp[wide[g].item][wide[g].mem] = cm[g - g0];
+    }
+    cb.run(c);
+    g0 = g1;
+  }
+  // Re-pack every item that had a wide member: narrow members verbatim,
+  // wide ones as their compressed columns; offsets follow.
+  CopyBatch cb;
+  std::vector<DMat> old;  // source concats stay alive until the copies are enqueued
+  std::vector<size_t> touched;
+  for (const auto& w : wide)
+    if (touched.empty() || touched.back() != w.item) touched.push_back(w.item);
+  for (size_t t : touched) {
+    auto& it = items[t];
+    std::vector<int64_t> offs{0};
+    for (size_t s = 0; s + 1 < it.offs.size(); ++s) {
+      const int w = int(it.offs[s + 1] - it.offs[s]);
+      const int nw = comp[t][s].owner ? comp[t][s].cols() : w;
+      offs.push_back(offs.back() + nw);
+    }
+    const int n2 = int(offs.back());
+    const int ld = std::max(2, (it.m + 1) & ~1);
+    DMat nc = alloc_mat(c, ld, std::max(n2, 1));
+    nc.m = Mat{nc.m.p, it.m, n2, 1, ld};
+    for (size_t s = 0; s + 1 < it.offs.size(); ++s) {
+      const int w2 = int(offs[s + 1] - offs[s]);
+      if (w2 == 0) continue;
+      const Mat dst = nc.m.sub(0, int(offs[s]), it.m, w2);
+      if (comp[t][s].owner)
+        cb.copy(dst, comp[t][s].m);
+      else
+        cb.copy(dst, it.concat.m.sub(0, int(it.offs[s]), it.m, w2));
+    }
+    old.push_back(std::move(it.concat));
+    it.concat = nc;
+    it.n = n2;
+    it.offs = std::move(offs);
+    it.inplace = true;
+  }
+  cb.run(c);
+  old.clear();  // stream-ordered frees behind the copies
+}
+
 void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t mem_budget) {
+  if (c.qr_compress) compress_members(c, items, mem_budget);
   const size_t n_items = items.size();
   int max_rows = 0;
   for (auto& it : items) max_rows = std::max(max_rows, it.m);

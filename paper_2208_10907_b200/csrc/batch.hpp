@@ -50,6 +50,9 @@ struct Ctx {
   // QR mode: exact (the reference's rounding, k_qr.cu) or blocked (k_qrb.cu);
   // set per factorization from Options::qr_mode (H2G_QR_MODE overrides).
   bool qr_blocked = false;
+  // Compressed QR mode (qr_mode = 2): members replaced by pivoted-Cholesky
+  // factors of their Gram matrices before the (blocked) QR (k_pchol.cu).
+  bool qr_compress = false;
   void sync();            // stream sync + error word check
   void check_err();       // throws the reference's message for device errors
   // Names of the LU batches launched since the last sync, by tag: a singular
@@ -116,6 +119,7 @@ struct GemmBatch {
   std::vector<GemmSeg> segs;
   std::vector<int2> masks;
   std::vector<int> seg_mask_off;  // per seg: offset into masks or -1
+  const char* name = nullptr;     // profiling name (default "gemm")
   // Begin a job; add segments with seg()/seg_gen() afterwards.
   void job(Mat C, bool acc) {
     GemmJob j;

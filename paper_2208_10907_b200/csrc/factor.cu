@@ -1577,7 +1577,9 @@ void Problem::factor() {
   }
   c.phase_flops.clear();
   const char* qm = getenv("H2G_QR_MODE");  // experiment override
-  c.qr_blocked = qm ? std::string(qm) == "blocked" : opt.qr_mode == 1;
+  const int qmode = qm ? (std::string(qm) == "compressed" ? 2 : std::string(qm) == "blocked" ? 1 : 0) : opt.qr_mode;
+  c.qr_blocked = qmode >= 1;
+  c.qr_compress = qmode == 2;
   levels.clear();
   max_fill_resid.clear();
   Driver d(*this);

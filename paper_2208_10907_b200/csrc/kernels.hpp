@@ -172,4 +172,18 @@ int qrb_max_rows();
 void launch_qrb(const QrJob* jobs, int njobs, int max_m, int max_nmem, int cluster, cudaStream_t st);
 int qrb_cluster_size(int njobs, int min_n, int max_m, int max_nmem);
 
+// ---- member compression (k_pchol.cu, qr_mode = 2) ------------------------------
+// Diagonally pivoted Cholesky of a member's Gram matrix G = M M^T: writes
+// count[0] <= kmax columns R with R R^T = G up to a dropped trace <= eta tr(G).
+struct PcholJob {
+  const double* G;  // m x m column-major
+  int64_t ldg;
+  double* R;        // m x kmax column-major
+  int64_t ldr;
+  int m, kmax;
+  double eta;
+  int* count;
+};
+void launch_pchol(const PcholJob* jobs, int njobs, int max_m, int max_k, cudaStream_t st);
+
 }  // namespace h2g
