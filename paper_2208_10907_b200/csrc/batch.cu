@@ -202,17 +202,24 @@ void GemmBatch::run(Ctx& c, int tag) {
   for (size_t j = 0; j < jobs.size(); ++j) {
     const Mat& C = jobs[j].C;
     if (C.rows <= 0 || C.cols <= 0) continue;
+    const int tm = (C.rows + bm - 1) / bm, tn = (C.cols + 63) / 64;
+    // Symmetric C: tiles entirely above the diagonal are skipped (and not counted).
+    auto above = [&](int a, int b) { return lower[j] && b * 64 >= (a + 1) * bm; };
+    int kept = 0;
+    for (int a = 0; a < tm; ++a)
+      for (int b = 0; b < tn; ++b) kept += above(a, b) ? 0 : 1;
+    const double frac = double(kept) / (tm * tn);
     for (int s = 0; s < jobs[j].nseg; ++s) {
       const GemmSeg& sg = segs[jobs[j].seg0 + s];
-      fl += 2.0 * C.rows * double(sg.A.cols) * C.cols;
+      fl += frac * 2.0 * C.rows * double(sg.A.cols) * C.cols;
       if (sg.gen) {
         fl += double(sg.A.cols) * C.cols * (c.kp.kind == 0 ? 9 : 11);
         c.kernel_evals += double(sg.A.cols) * C.cols;
       }
     }
-    const int tm = (C.rows + bm - 1) / bm, tn = (C.cols + 63) / 64;
     for (int a = 0; a < tm; ++a)
-      for (int b = 0; b < tn; ++b) tiles.push_back({int(j), a, b});
+      for (int b = 0; b < tn; ++b)
+        if (!above(a, b)) tiles.push_back({int(j), a, b});
   }
   c.add_flops(fl);
   if (tiles.empty()) return;
@@ -528,6 +535,7 @@ static void compress_members(Ctx& c, std::vector<QrBatch::Item>& items, size_t m
       const DMat& G = gr[2 * (g - g0)];
       const DMat& R = gr[2 * (g - g0) + 1];
       gemm1(gb, G.m, A, A.t());
+      gb.lower.back() = 1;  // pchol reads the lower triangle only
       const double mt = it.tol * 0.5;  // member_tol (compression.hpp:67)
       const double eta = std::max(64.0 * 2.220446049250313e-16, 0.01 * mt * mt);
       pj.push_back({G.m.p, G.m.cs, R.m.p, R.m.cs, it.m, wide[g].kmax, eta, dcount + (g - g0)});

@@ -120,6 +120,7 @@ struct GemmBatch {
   std::vector<int2> masks;
   std::vector<int> seg_mask_off;  // per seg: offset into masks or -1
   const char* name = nullptr;     // profiling name (default "gemm")
+  std::vector<char> lower;        // per job: only tiles touching the lower triangle (symmetric C)
   // Begin a job; add segments with seg()/seg_gen() afterwards.
   void job(Mat C, bool acc) {
     GemmJob j;
@@ -128,6 +129,7 @@ struct GemmBatch {
     j.nseg = 0;
     j.acc = acc ? 1 : 0;
     jobs.push_back(j);
+    lower.push_back(0);
   }
   void seg(Mat A, Mat B, double alpha = 1.0) {
     GemmSeg s;

@@ -10,8 +10,8 @@
 // O(N) wide; C_i from a diagonally pivoted Cholesky of G_i has at most
 // min(dim, w_i) columns (its numerical rank, usually far fewer).
 //
-// pchol_kernel: one CTA per member. G (dim x dim, column-major) is read, never
-// written; R (dim x kmax column-major) receives the columns in pick order:
+// pchol_kernel: one CTA per member. The lower triangle of G (dim x dim,
+// column-major) is read, never written; R (dim x kmax column-major) receives the columns in pick order:
 //   p_t = argmax of the unpicked remaining diagonal (lowest index on ties),
 //   R(:, t) = (G(:, p_t) - R(:, 0:t) R(p_t, 0:t)^T) / sqrt(d_{p_t}),
 //   d_j -= R(j, t)^2.
@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(NT) pchol_kernel(const PcholJob* __restrict__ 
       if (j == p) {
         r = piv;
       } else if (d[j] >= 0) {
-        double v = job.G[int64_t(p) * job.ldg + j];
+        // lower triangle only (the Gram GEMM skips tiles above the diagonal)
+        double v = j >= p ? job.G[int64_t(p) * job.ldg + j] : job.G[int64_t(j) * job.ldg + p];
         const double* Rj = job.R + j;
         for (int s = 0; s < t; ++s) v = fma(-Rj[int64_t(s) * job.ldr], rp[s], v);
         r = v * inv;
