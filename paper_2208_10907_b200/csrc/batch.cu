@@ -239,7 +239,8 @@ void GemmBatch::run(Ctx& c, int tag) {
     }
   }
   auto ev = c.prof_begin();
-  launch_gemm(dj, ds, dt, int(tiles.size()), bm, c.kp, c.cloud, c.err, tag, c.stream);
+  launch_gemm(dj, ds, dt, int(tiles.size()), bm, c.kp, c.cloud, c.err, tag, c.stream,
+              name && std::string(name) == "gram" ? 1 : 0);
   const std::string nm = name ? name : "gemm";
   c.prof_end(c.prof_detail ? (nm + "@" + c.phase).c_str() : nm.c_str(), ev, fl, by);
   c.launches++;

@@ -256,6 +256,9 @@ __device__ __forceinline__ void cp8(double* smem, const double* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(su32(smem)), "l"(gmem) : "memory");
 }
 
+// KIND only names the instantiation (0 = general, 1 = member Gram matrices)
+// so profiles can tell the launches apart.
+template <int KIND>
 __global__ void __launch_bounds__(NTW, 1) gemm_ws_kernel(const GemmJob* __restrict__ jobs,
                                                         const GemmSeg* __restrict__ segs,
                                                         const GemmTile* __restrict__ tiles,
@@ -453,17 +456,21 @@ void launch_bm(const GemmJob* jobs, const GemmSeg* segs, const GemmTile* tiles, 
 int gemm_tile_rows(int max_rows) { return max_rows > 64 ? 128 : 64; }
 
 void launch_gemm(const GemmJob* jobs, const GemmSeg* segs, const GemmTile* tiles, int ntiles,
-                 int bm, KernelParams kp, Cloud cloud, ErrWord* err, int tag, cudaStream_t st) {
+                 int bm, KernelParams kp, Cloud cloud, ErrWord* err, int tag, cudaStream_t st, int kind) {
   if (ntiles <= 0) return;
   static const bool use_ws = getenv("H2G_GEMM_CLASSIC") == nullptr;
   if (bm == 128 && use_ws) {
     static bool attr = false;
     const int smem = int(sizeof(ws::Smem));
     if (!attr) {
-      cudaFuncSetAttribute(ws::gemm_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(ws::gemm_ws_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(ws::gemm_ws_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       attr = true;
     }
-    ws::gemm_ws_kernel<<<ntiles, ws::NTW, smem, st>>>(jobs, segs, tiles, kp, cloud, err, tag);
+    if (kind == 1)
+      ws::gemm_ws_kernel<1><<<ntiles, ws::NTW, smem, st>>>(jobs, segs, tiles, kp, cloud, err, tag);
+    else
+      ws::gemm_ws_kernel<0><<<ntiles, ws::NTW, smem, st>>>(jobs, segs, tiles, kp, cloud, err, tag);
   } else if (bm == 128)
     launch_bm<128>(jobs, segs, tiles, ntiles, kp, cloud, err, tag, st);
   else

@@ -40,7 +40,8 @@ struct GemmTile {
 // tm indexes BM-row tiles; BM = gemm_tile_rows(max C rows in the batch).
 int gemm_tile_rows(int max_rows);
 void launch_gemm(const GemmJob* jobs, const GemmSeg* segs, const GemmTile* tiles, int ntiles,
-                 int bm, KernelParams kp, Cloud cloud, ErrWord* err, int tag, cudaStream_t st);
+                 int bm, KernelParams kp, Cloud cloud, ErrWord* err, int tag, cudaStream_t st,
+                 int kind = 0);
 
 // ---- batched kernel-block evaluation (k_eval.cu) ---------------------------
 // out(i, j) = K(x[rb + i], x[cb + j]) (assemble_block, kernels.cpp:242-268).

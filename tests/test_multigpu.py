@@ -92,12 +92,14 @@ def _worker(rank, world, port, case, out):
 
 CASES = [("cube", 4096, 128, "laplace", 0, 1e-8),
          ("cube", 8192, 128, "laplace", 64, 1e-4),
-         ("cube", 4096, 128, "laplace", 0, 1e-8, "blocked")]
+         ("cube", 4096, 128, "laplace", 0, 1e-8, "blocked"),
+         ("cube", 4096, 128, "laplace", 0, 1e-6, "compressed")]
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("case", CASES, ids=["c1_cube4096", "cube8192_cap64", "c1_cube4096_blockedqr"])
+@pytest.mark.parametrize("case", CASES, ids=["c1_cube4096", "cube8192_cap64", "c1_cube4096_blockedqr",
+                                         "cube4096_tol1e-6_compressedqr"])
 def test_partitioned_factor_is_bitwise_single_gpu(tmp_path, world, case):
     x1, b1, r1 = _factor_case(case)
     mp.spawn(_worker, args=(world, _port(), case, str(tmp_path)), nprocs=world, join=True)
