@@ -20,7 +20,10 @@ extern "C" {
 
 typedef struct h2g_problem h2g_problem;
 
-/* KernelSpec (kernels.hpp:15-23): kind 0 = Laplace, 1 = Yukawa. */
+/* KernelSpec (kernels.hpp:15-23): kind 0 = Laplace, 1 = Yukawa,
+ * 2 = Gaussian q_j (exp(-alpha_m r^2) + [r == 0] eta_reg) / permittivity_scale
+ * (BASELINE configs[2]: alpha_m = 1/0.1, eta_reg = 1e-2, scale 1; not in the
+ * reference, so its parity is by residual only). */
 typedef struct {
   int32_t kind;
   double alpha_m;

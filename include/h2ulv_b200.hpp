@@ -98,7 +98,7 @@ inline PointCloud generate_line(int64_t n, uint64_t seed) {
 }
 
 // ---- kernels / structure (kernels.hpp:11-39, geometry.hpp:60-67, hstructure.hpp:15)
-enum class KernelKind { laplace, yukawa };
+enum class KernelKind { laplace, yukawa, gaussian };
 enum class StructureVariant { blr2, hss, h2 };  // hstructure.hpp:15
 enum class AdmissibilityKind { weak, strong };
 struct AdmissibilityRule {
@@ -137,7 +137,7 @@ inline std::shared_ptr<Handle> build(const PointCloud& cloud, int64_t leaf, cons
                                      double eta, StructureVariant v, double tol,
                                      std::optional<int64_t> cap, bool absorb, int qr_mode = 0) {
   auto h = std::make_shared<Handle>();
-  h2g_kernel hk{k.kind == KernelKind::laplace ? 0 : 1, k.alpha_m, k.permittivity_scale, k.eta_reg};
+  h2g_kernel hk{k.kind == KernelKind::laplace ? 0 : k.kind == KernelKind::yukawa ? 1 : 2, k.alpha_m, k.permittivity_scale, k.eta_reg};
   h2g_options o{tol, cap.value_or(0), 1e-13, absorb ? 1 : 0, 100.0, v == StructureVariant::h2 ? 0 : v == StructureVariant::hss ? 1 : 2, eta, 0, qr_mode};
   check(h2g_set_kernel(h->p, &hk));
   check(h2g_set_options(h->p, &o));
@@ -273,7 +273,7 @@ inline PointCloud make_cloud(const RunConfig& cfg) {  // report.cpp:60-65
 inline KernelSpec make_kernel(const RunConfig& cfg, const PointCloud& cloud) {  // report.cpp:67-77
   KernelSpec k;
   k.kind = cfg.kernel;
-  k.alpha_m = cfg.kernel == KernelKind::yukawa ? cfg.alpha_m : 0.0;
+  k.alpha_m = cfg.kernel == KernelKind::laplace ? 0.0 : cfg.alpha_m;
   k.permittivity_scale = cfg.scale;
   k.eta_reg = cfg.reg ? *cfg.reg : 1e-3 * cloud.domain_diameter() / std::cbrt(double(cloud.size()));
   return k;

@@ -102,7 +102,7 @@ def assemble_block(xyz, q, rows, cols, kind="laplace", alpha_m=0.0, scale=4 * np
     xyz = np.ascontiguousarray(xyz, dtype=np.float64)
     q = np.ascontiguousarray(q, dtype=np.float64)
     out = np.zeros((rows[1] - rows[0], cols[1] - cols[0]), order="F")
-    rc = lib().or_assemble_block(0 if kind == "laplace" else 1, alpha_m, scale, reg, _p(xyz),
+    rc = lib().or_assemble_block({"laplace": 0, "yukawa": 1, "gaussian": 2}[kind], alpha_m, scale, reg, _p(xyz),
                                  _p(q), rows[0], rows[1], cols[0], cols[1], _p(out))
     if rc:
         raise RuntimeError("assemble_block: singular evaluation (r + eta_reg == 0)")

@@ -299,13 +299,20 @@ int or_classify(int levels, const double* geo, double eta, int weak, int64_t* ne
   return 0;
 }
 
-/* assemble_block (kernels.cpp:242-268): r = sqrt(fma(dz,dz,fma(dx,dx,dy*dy))). */
+/* assemble_block (kernels.cpp:242-268): r = sqrt(fma(dz,dz,fma(dx,dx,dy*dy))).
+ * kind 2 (Gaussian, BASELINE configs[2]) is NOT in the reference: q_j (exp(-alpha_m r^2)
+ * + [r^2 == 0] reg) / scale; parity unpinned (our definition, checked by residual). */
 int or_assemble_block(int kind, double alpha_m, double scale, double reg, const double* xyz,
                       const double* q, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
                       double* out) {
   const int64_t nr = r1 - r0;
   for (int64_t j = c0; j < c1; ++j)
     for (int64_t i = r0; i < r1; ++i) {
+      if (kind == 2) {
+        const double r2 = dist2(xyz + 3 * i, xyz + 3 * j);
+        out[(j - c0) * nr + (i - r0)] = q[j] * (exp(-alpha_m * r2) + (r2 == 0.0 ? reg : 0.0)) / scale;
+        continue;
+      }
       const double r = sqrt(dist2(xyz + 3 * i, xyz + 3 * j));
       const double denom = scale * (r + reg);
       if (denom == 0.0) return 1;

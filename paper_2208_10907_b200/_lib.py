@@ -211,7 +211,7 @@ class Problem:
         self.close()
 
     def set_kernel(self, kind="laplace", alpha_m=0.0, scale=4 * np.pi, reg=0.0):
-        k = Kernel(0 if kind == "laplace" else 1, alpha_m, scale, reg)
+        k = Kernel({"laplace": 0, "yukawa": 1, "gaussian": 2}[kind], alpha_m, scale, reg)
         _check(self.L.h2g_set_kernel(self.h, ctypes.byref(k)))
 
     def set_options(self, tol=1e-8, cap=None, rr_pivot_tol=1e-13, absorb_coupling=True,

@@ -69,6 +69,8 @@ void h2g_destroy(h2g_problem* p) { delete p; }
 int h2g_set_kernel(h2g_problem* p, const h2g_kernel* k) {
   return guarded([&] {
     h2g::KernelParams kp;
+    if (k->kind < 0 || k->kind > 2)
+      throw std::invalid_argument("kernel: kind must be 0 (laplace), 1 (yukawa) or 2 (gaussian)");
     kp.kind = k->kind;
     kp.alpha_m = k->alpha_m;
     kp.scale = k->permittivity_scale;

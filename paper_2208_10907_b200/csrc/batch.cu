@@ -213,7 +213,7 @@ void GemmBatch::run(Ctx& c, int tag) {
       const GemmSeg& sg = segs[jobs[j].seg0 + s];
       fl += frac * 2.0 * C.rows * double(sg.A.cols) * C.cols;
       if (sg.gen) {
-        fl += double(sg.A.cols) * C.cols * (c.kp.kind == 0 ? 9 : 11);
+        fl += double(sg.A.cols) * C.cols * kernel_entry_flops(c.kp.kind);
         c.kernel_evals += double(sg.A.cols) * C.cols;
       }
     }
@@ -253,7 +253,7 @@ void EvalBatch::run(Ctx& c, int tag) {
   tiles_of(jobs, tj, ti, &EvalJob::out);
   double evn_ = 0;
   for (auto& j : jobs) evn_ += double(j.out.rows) * j.out.cols;
-  const double ev_flops_ = evn_ * (c.kp.kind == 0 ? 9 : 11);
+  const double ev_flops_ = evn_ * kernel_entry_flops(c.kp.kind);
   c.kernel_evals += evn_;
   c.add_flops(ev_flops_);
   if (tj.empty()) return;

@@ -31,13 +31,19 @@ inline Mat colmajor(double* p, int rows, int cols, int64_t ld = -1) {
   return Mat{p, rows, cols, 1, ld < 0 ? rows : ld};
 }
 
-// Kernel function parameters (kernels.hpp:15-23): 0 = Laplace, 1 = Yukawa.
+// Kernel function parameters (kernels.hpp:15-23): 0 = Laplace, 1 = Yukawa,
+// 2 = Gaussian (BASELINE configs[2]; not in the reference): q_j (exp(-alpha_m r^2)
+// + [r == 0] reg) / scale, i.e. exp(-r^2/h) + sigma I with alpha_m = 1/h, reg = sigma.
 struct KernelParams {
   int kind = 0;
   double alpha_m = 0.0;
   double scale = 4.0 * 3.14159265358979323846;
   double reg = 0.0;
 };
+
+// Counted flops per kernel entry (kernels.cpp:266: 9 Laplace, 11 Yukawa; the
+// Gaussian is counted like Yukawa).
+inline double kernel_entry_flops(int kind) { return kind == 0 ? 9.0 : 11.0; }
 
 // Reordered cloud in SoA form on the device.
 struct Cloud {
@@ -51,18 +57,32 @@ struct Cloud {
 // kernel_eval / assemble_block entry (kernels.cpp:232-268): bitwise equal to
 // the reference for Laplace (r = sqrt(fma(dz,dz,fma(dx,dx,dy*dy))), IEEE
 // sqrt and division). Yukawa uses CUDA exp (<= 1 ulp from glibc).
-__device__ __forceinline__ double kernel_pair(const KernelParams& kp, double xi, double yi,
-                                              double zi, double xj, double yj, double zj,
-                                              double qj, int* singular) {
+template <int KIND>
+__device__ __forceinline__ double kernel_pair_k(const KernelParams& kp, double xi, double yi,
+                                                double zi, double xj, double yj, double zj,
+                                                double qj, int* singular) {
   const double dx = xi - xj, dy = yi - yj, dz = zi - zj;
+  if (KIND == 2) {
+    const double r2 = fma(dz, dz, fma(dx, dx, dy * dy));
+    const double v = exp(-kp.alpha_m * r2) + (r2 == 0.0 ? kp.reg : 0.0);
+    return qj * v / kp.scale;
+  }
   const double r = sqrt(fma(dz, dz, fma(dx, dx, dy * dy)));
   const double denom = kp.scale * (r + kp.reg);
   if (denom == 0.0) {
     *singular = 1;
     return 0.0;
   }
-  if (kp.kind == 0) return qj / denom;
+  if (KIND == 0) return qj / denom;
   return qj * exp(-kp.alpha_m * r) / denom;
+}
+
+__device__ __forceinline__ double kernel_pair(const KernelParams& kp, double xi, double yi,
+                                              double zi, double xj, double yj, double zj,
+                                              double qj, int* singular) {
+  if (kp.kind == 0) return kernel_pair_k<0>(kp, xi, yi, zi, xj, yj, zj, qj, singular);
+  if (kp.kind == 1) return kernel_pair_k<1>(kp, xi, yi, zi, xj, yj, zj, qj, singular);
+  return kernel_pair_k<2>(kp, xi, yi, zi, xj, yj, zj, qj, singular);
 }
 
 __device__ __forceinline__ double kernel_entry(const KernelParams& kp, const Cloud& c, int64_t i,

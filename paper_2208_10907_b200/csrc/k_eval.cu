@@ -167,11 +167,7 @@ __global__ void __launch_bounds__(256) matvec_kernel(KernelParams kp, Cloud c, c
       const int cnt = int(c.n - j0 < 256 ? c.n - j0 : 256);
       if (!live) continue;
       for (int t = 0; t < cnt; ++t) {
-        const double dx = xi - sx[t], dy = yi - sy[t], dz = zi - sz[t];
-        const double r = sqrt(fma(dz, dz, fma(dx, dx, dy * dy)));
-        const double denom = kp.scale * (r + kp.reg);
-        if (denom == 0.0) sing = 1;
-        const double a = kp.kind == 0 ? sq[t] / denom : sq[t] * exp(-kp.alpha_m * r) / denom;
+        const double a = kernel_pair(kp, xi, yi, zi, sx[t], sy[t], sz[t], sq[t], &sing);
         for (int q = 0; q < nr; ++q) acc[q] = fma(a, x[(r0 + q) * c.n + j0 + t], acc[q]);
       }
     }

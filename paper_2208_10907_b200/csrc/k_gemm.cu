@@ -19,6 +19,7 @@
 // used when the batch has tall C blocks so a kernel-generated B tile is
 // evaluated once per 128 rows.
 #include <cstdlib>
+#include <type_traits>
 
 #include "kernels.hpp"
 
@@ -255,6 +256,9 @@ __device__ __forceinline__ void mb_wait(unsigned long long* b, unsigned parity) 
 __device__ __forceinline__ void cp8(double* smem, const double* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(su32(smem)), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp16(double* smem, const double* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(su32(smem)), "l"(gmem) : "memory");
+}
 
 // KIND only names the instantiation (0 = general, 1 = member Gram matrices)
 // so profiles can tell the launches apart.
@@ -304,6 +308,24 @@ __global__ void __launch_bounds__(NTW, 1) gemm_ws_kernel(const GemmJob* __restri
       const bool gen = sg.gen;
       if (pt == 0) sm.alpha[st] = gen ? 1.0 : alpha;
       const bool a_colmajor = A.rs == 1;
+      // Column-major A with 16-byte aligned columns: row pairs by 16-byte
+      // cp.async (half the copy instructions).
+      const bool a_pairs = a_colmajor && (A.cs % 2 == 0) && ((reinterpret_cast<uintptr_t>(A.p) & 15) == 0);
+      if (a_pairs) {
+#pragma unroll 2
+        for (int u = 0; u < BM * BKW / (2 * NP); ++u) {
+          const int e = pt + u * NP;
+          const int mm = 2 * (e % (BM / 2)), kk = e / (BM / 2);
+          const int i = m0 + mm, l = pk + kk;
+          double* dst = &sm.A[st][kk][mm];
+          if (l < K && i + 1 < A.rows) {
+            cp16(dst, &A.at(i, l));
+          } else {
+            if (i < A.rows && l < K) cp8(dst, &A.at(i, l)); else dst[0] = 0.0;
+            dst[1] = 0.0;
+          }
+        }
+      } else
 #pragma unroll 2
       for (int u = 0; u < BM * BKW / NP; ++u) {
         const int e = pt + u * NP;
@@ -342,6 +364,41 @@ __global__ void __launch_bounds__(NTW, 1) gemm_ws_kernel(const GemmJob* __restri
           sm.P[st][pt / 4][comp] = v;
         }
         asm volatile("bar.sync 1, %0;\n" ::"n"(NP) : "memory");
+        if (pk + BKW <= K && jT < C.cols) {
+          // Full chunk: the BKW * BN / NP entries of this thread are
+          // independent chains (sqrt / div / exp); evaluated branch-free per
+          // kernel kind so they interleave.
+          constexpr int NE = BKW * BN / NP;
+          double vals[NE];
+          auto gen = [&](auto kind_tag) {
+            constexpr int KD = decltype(kind_tag)::value;
+            if (sg.g.trans) {
+#pragma unroll
+              for (int u = 0; u < NE; ++u) {
+                const double* q = sm.P[st][pt / BN + u * (NP / BN)];
+                vals[u] = kernel_pair_k<KD>(kp, xT, yT, zT, q[0], q[1], q[2], q[3], &singular);
+              }
+            } else {
+#pragma unroll
+              for (int u = 0; u < NE; ++u) {
+                const double* q = sm.P[st][pt / BN + u * (NP / BN)];
+                vals[u] = kernel_pair_k<KD>(kp, q[0], q[1], q[2], xT, yT, zT, qT, &singular);
+              }
+            }
+          };
+          if (!liveT) {
+#pragma unroll
+            for (int u = 0; u < NE; ++u) vals[u] = 0.0;
+          } else if (kp.kind == 0) {
+            gen(std::integral_constant<int, 0>{});
+          } else if (kp.kind == 1) {
+            gen(std::integral_constant<int, 1>{});
+          } else {
+            gen(std::integral_constant<int, 2>{});
+          }
+#pragma unroll
+          for (int u = 0; u < NE; ++u) sm.B[st][pt / BN + u * (NP / BN)][nnT] = alpha * vals[u];
+        } else
 #pragma unroll 2
         for (int u = 0; u < BKW * BN / NP; ++u) {
           const int kk = pt / BN + u * (NP / BN);
@@ -363,6 +420,25 @@ __global__ void __launch_bounds__(NTW, 1) gemm_ws_kernel(const GemmJob* __restri
         const Mat B = sg.B;
         const bool b_colmajor = B.rs == 1;
         const double pad = alpha < 0.0 ? 0.0 : -0.0;  // -0 after the consumer's alpha scaling
+        // Row-major B (columns contiguous, e.g. the Gram's A^T) with 16-byte
+        // aligned rows: column pairs by 16-byte cp.async.
+        const bool b_pairs = !b_colmajor && B.cs == 1 && (B.rs % 2 == 0) &&
+                             ((reinterpret_cast<uintptr_t>(B.p) & 15) == 0);
+        if (b_pairs) {
+#pragma unroll 4
+          for (int u = 0; u < BKW * BN / (2 * NP); ++u) {
+            const int e = pt + u * NP;
+            const int nn = 2 * (e % (BN / 2)), kk = e / (BN / 2);
+            const int l = pk + kk, j = n0 + nn;
+            double* dst = &sm.B[st][kk][nn];
+            if (l < K && j + 1 < C.cols) {
+              cp16(dst, &B.at(l, j));
+            } else {
+              if (l < K && j < C.cols) cp8(dst, &B.at(l, j)); else dst[0] = pad;
+              dst[1] = pad;
+            }
+          }
+        } else
 #pragma unroll 4
         for (int u = 0; u < BKW * BN / NP; ++u) {
           const int e = pt + u * NP;
