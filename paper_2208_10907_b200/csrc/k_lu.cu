@@ -45,7 +45,7 @@ __device__ ValIdx block_argmax(ValIdx x, ValIdx* red) {
   return r;
 }
 
-__global__ void __launch_bounds__(NT) lu_kernel(const LuJob* __restrict__ jobs, ErrWord* err,
+__global__ void __launch_bounds__(NT, 2) lu_kernel(const LuJob* __restrict__ jobs, ErrWord* err,
                                                 int tag) {
   __shared__ ValIdx red[32];
   extern __shared__ double lcol[];  // scaled pivot column of the current step (n doubles)
