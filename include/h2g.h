@@ -147,6 +147,11 @@ int h2g_lu_factor(int64_t n, const double* a, double tol, double* lu, int64_t* p
 int h2g_basis_from_members(int64_t dim, int64_t width, const double* concat, int64_t nmem,
                            const int64_t* offsets, double tol, int64_t cap, int64_t min_rank,
                            double* sq, int64_t* rank);
+/* The same through a chosen QR mode (h2g_options.qr_mode: 0 exact, 1 blocked,
+ * 2 compressed); h2g_basis_from_members is qr_mode 0. */
+int h2g_basis_from_members_mode(int64_t dim, int64_t width, const double* concat, int64_t nmem,
+                                const int64_t* offsets, double tol, int64_t cap, int64_t min_rank,
+                                int32_t qr_mode, double* sq, int64_t* rank);
 /* LuFactors solve family (linalg.cpp:404-559) with the given packed factors:
  * kind 0 solve, 1 lower, 2 upper, 3 transpose, 4 right, 5 upper_right. */
 int h2g_lu_solve(int64_t n, const double* lu, const int64_t* perm, int kind, int64_t rows,

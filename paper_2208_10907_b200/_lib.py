@@ -35,7 +35,7 @@ EXPORTS = [
     "h2g_list", "h2g_near_entries", "h2g_near_dense", "h2g_num_factor_levels",
     "h2g_factor_level", "h2g_cutoff", "h2g_top_n", "h2g_top", "h2g_basis",
     "h2g_max_fill_residual", "h2g_stats", "h2g_matvec", "h2g_lu_factor",
-    "h2g_basis_from_members", "h2g_lu_solve", "h2g_gemm", "h2g_stats_dev", "h2g_set_profile",
+    "h2g_basis_from_members", "h2g_basis_from_members_mode", "h2g_lu_solve", "h2g_gemm", "h2g_stats_dev", "h2g_set_profile",
     "h2g_reset_profile", "h2g_kernel_stats", "h2g_set_stream", "h2g_phase_seconds",
     "h2g_nccl_unique_id", "h2g_comm_nccl", "h2g_comm_host", "h2g_comm_destroy", "h2g_set_comm",
     "h2g_partition_range", "h2g_kernel_evals",
@@ -87,6 +87,7 @@ def lib():
         L.h2g_matvec.argtypes = [P, i64, P, P]
         L.h2g_lu_factor.argtypes = [i64, P, f64, P, P]
         L.h2g_basis_from_members.argtypes = [i64, i64, P, i64, P, f64, i64, i64, P, P]
+        L.h2g_basis_from_members_mode.argtypes = [i64, i64, P, i64, P, f64, i64, i64, ctypes.c_int32, P, P]
         L.h2g_lu_solve.argtypes = [i64, P, P, ctypes.c_int, i64, i64, P]
         L.h2g_gemm.argtypes = [i64, i64, i64, f64, P, ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P]
         L.h2g_stats_dev.argtypes = [P, P]
@@ -404,12 +405,14 @@ def gemm(a, b, alpha=1.0, transa=False, transb=False, c=None):
     return out
 
 
-def basis_from_members(concat, offsets, tol, cap=None, min_rank=0):
+def basis_from_members(concat, offsets, tol, cap=None, min_rank=0, qr_mode="exact"):
     concat = np.asfortranarray(concat, dtype=np.float64)
     dim = concat.shape[0]
     offsets = np.ascontiguousarray(offsets, dtype=np.int64)
     sq = np.zeros((dim, dim), order="F")
     rank = np.zeros(1, dtype=np.int64)
-    _check(lib().h2g_basis_from_members(dim, concat.shape[1], _p(concat), len(offsets) - 1,
-                                        _p(offsets), tol, cap or 0, min_rank, _p(sq), _p(rank)))
+    _check(lib().h2g_basis_from_members_mode(dim, concat.shape[1], _p(concat), len(offsets) - 1,
+                                             _p(offsets), tol, cap or 0, min_rank,
+                                             {"exact": 0, "blocked": 1, "compressed": 2}[qr_mode],
+                                             _p(sq), _p(rank)))
     return sq, int(rank[0])

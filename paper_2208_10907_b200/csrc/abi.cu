@@ -409,9 +409,19 @@ int h2g_gemm(int64_t m, int64_t n, int64_t k, double alpha, const double* a, int
 int h2g_basis_from_members(int64_t dim, int64_t width, const double* concat, int64_t nmem,
                            const int64_t* offsets, double tol, int64_t cap, int64_t min_rank,
                            double* sq, int64_t* rank) {
+  return h2g_basis_from_members_mode(dim, width, concat, nmem, offsets, tol, cap, min_rank, 0, sq, rank);
+}
+
+int h2g_basis_from_members_mode(int64_t dim, int64_t width, const double* concat, int64_t nmem,
+                                const int64_t* offsets, double tol, int64_t cap, int64_t min_rank,
+                                int32_t qr_mode, double* sq, int64_t* rank) {
   return guarded([&] {
     require_device();
+    if (qr_mode < 0 || qr_mode > 2)
+      throw std::invalid_argument("config: qr_mode must be 0 (exact), 1 (blocked) or 2 (compressed)");
     h2g::Problem P;
+    P.c.qr_blocked = qr_mode >= 1;
+    P.c.qr_compress = qr_mode == 2;
     auto Cm = h2g::alloc_mat(P.c, int(dim), int(width > 0 ? width : 1));
     if (width > 0)
       h2g::cuda_check(cudaMemcpy(Cm.m.p, concat, sizeof(double) * dim * width, cudaMemcpyHostToDevice), "h2d");

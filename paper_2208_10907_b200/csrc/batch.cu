@@ -238,6 +238,23 @@ void GemmBatch::run(Ctx& c, int tag) {
       by += 8.0 * sg.A.rows * double(sg.A.cols) + (sg.gen ? 0.0 : 8.0 * sg.B.rows * double(sg.B.cols));
     }
   }
+  static const bool shapes = getenv("H2G_GEMM_SHAPES") != nullptr;
+  if (shapes) {  // launch shape census (profiling aid)
+    double sr = 0, sc = 0, sk = 0, nseg = 0, ngen = 0;
+    for (auto& j : jobs) {
+      sr += j.C.rows;
+      sc += j.C.cols;
+      for (int q = 0; q < j.nseg; ++q) {
+        sk += segs[j.seg0 + q].A.cols;
+        ngen += segs[j.seg0 + q].gen;
+      }
+      nseg += j.nseg;
+    }
+    const double nj = double(jobs.size());
+    fprintf(stderr, "GEMMSHAPE %s@%s jobs %zu tiles %zu bm %d rows %.0f cols %.0f segs %.1f K/seg %.0f gen %.0f%% GF %.2f\n",
+            name ? name : "gemm", c.phase.c_str(), jobs.size(), tiles.size(), bm, sr / nj, sc / nj, nseg / nj,
+            sk / std::max(1.0, nseg), 100.0 * ngen / std::max(1.0, nseg), fl * 1e-9);
+  }
   auto ev = c.prof_begin();
   launch_gemm(dj, ds, dt, int(tiles.size()), bm, c.kp, c.cloud, c.err, tag, c.stream,
               name && std::string(name) == "gram" ? 1 : 0);
@@ -350,7 +367,55 @@ void LuBatch::run(Ctx& c) {
 
 // Blocked left solve (forward/backward substitution with GEMM updates between
 // 32-row diagonal blocks) for wide right-hand sides.
+static void run_trsm_chunks(Ctx& c, const std::vector<SolveJob>& bj);
+static void run_blocked_gemm(Ctx& c, const std::vector<SolveJob>& bj);
+
 static void run_blocked(Ctx& c, const std::vector<SolveJob>& bj) {
+  if (bj.empty()) return;
+  // Default: GEMM (DMMA) updates between 32-row diagonal blocks. H2G_TRSM_FUSED=1
+  // selects the single-launch shared-memory kernel (trsm_chunk_kernel): bitwise
+  // identical, measured no faster on the bench (332 ms vs ~330 ms for the GEMM path),
+  // kept for further work. It keeps a 32-column chunk of X in shared memory: m <= 800.
+  static const bool gemm_updates = getenv("H2G_TRSM_FUSED") == nullptr;
+  std::vector<SolveJob> big;
+  if (!gemm_updates) {
+    std::vector<SolveJob> small;
+    for (auto& s : bj) (s.lu.rows <= 800 ? small : big).push_back(s);
+    run_trsm_chunks(c, small);
+    if (big.empty()) return;
+  }
+  const std::vector<SolveJob>& rest = gemm_updates ? bj : big;
+  run_blocked_gemm(c, rest);
+}
+
+static void run_trsm_chunks(Ctx& c, const std::vector<SolveJob>& bj) {
+  if (bj.empty()) return;
+  {
+    std::vector<int2> tiles;
+    int max_m = 1;
+    double fl = 0, by = 0;
+    const int w = trsm_chunk_cols();
+    for (size_t t = 0; t < bj.size(); ++t) {
+      const SolveJob& s = bj[t];
+      for (int g = 0; g * w < s.X.cols; ++g) tiles.push_back(make_int2(int(t), g));
+      max_m = std::max(max_m, s.lu.rows);
+      const double mm = s.lu.rows;
+      fl += (s.kind == SOLVE_FULL ? 2.0 : 1.0) * mm * mm * s.X.cols;
+      by += 8.0 * mm * mm + 16.0 * s.X.rows * double(s.X.cols);
+    }
+    c.add_flops(fl);
+    Slab k1, k2;
+    auto* dj = upload(c, bj, k1);
+    auto* dt = upload(c, tiles, k2);
+    auto ev = c.prof_begin();
+    launch_trsm_chunk(dj, dt, int(tiles.size()), max_m, c.stream);
+    c.prof_end(c.prof_detail ? ("trsm@" + c.phase).c_str() : "trsm", ev, fl, by);
+    c.launches++;
+    cuda_check(cudaGetLastError(), "trsm chunk");
+  }
+}
+
+static void run_blocked_gemm(Ctx& c, const std::vector<SolveJob>& bj) {
   if (bj.empty()) return;
   constexpr int NB = 32;
   // X <- P X for the permuted kinds.

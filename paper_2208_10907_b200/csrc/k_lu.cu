@@ -2,6 +2,8 @@
 // family. One CTA per matrix (LU) or per RHS chunk (solves). Every element
 // sees the reference's exact rounding sequence (linalg.cpp:352-559), so the
 // packed factors and solutions are bitwise equal to the reference.
+#include <cstdio>
+
 #include "kernels.hpp"
 
 namespace h2g {
@@ -281,6 +283,156 @@ __global__ void __launch_bounds__(128) trsm_block_kernel(const TrsmBlockJob* __r
     if (i < nb) job.X.at(kb + i, c) = x[i];
 }
 
+
+// Fused blocked left solve for wide right-hand sides (SOLVE_FULL / LOWER /
+// UPPER): one CTA per (job, 32-column chunk of X); the chunk lives in shared
+// memory for the whole solve, so X is read and written once (the previous
+// path re-read the rows below / above every 32-row block from HBM through a
+// GEMM launch per block). Per 32-row diagonal block: warp 0 solves the block
+// with one lane per column (registers, the 32 x 32 factor block staged in
+// shared memory), then every warp updates 32-row groups of the remaining rows
+// with one lane per row, the row's factor segment in registers and the
+// block's solved values broadcast from shared memory. Each element sees the
+// reference's update sequence: forward fma(-L(i,k), x_k, x_i) for k ascending,
+// backward k descending then the division (linalg.cpp:404-542) — the same
+// sequence the GEMM-update path produced, so results are bitwise unchanged.
+constexpr int TRSM_NC = 32;
+
+__global__ void __launch_bounds__(256, 2) trsm_chunk_kernel(const SolveJob* __restrict__ jobs,
+                                                            const int2* __restrict__ tiles) {
+  extern __shared__ double xs[];  // [TRSM_NC][ldx]
+  __shared__ double blk[32 * 33];
+  const int2 t = tiles[blockIdx.x];
+  const SolveJob job = jobs[t.x];
+  const Mat L = job.lu;
+  const Mat X = job.X;
+  const int m = L.rows;
+  const int ldx = m | 1;  // odd stride: lane-per-column accesses are conflict-free
+  const int c0 = t.y * TRSM_NC;
+  const int nc = min(TRSM_NC, X.cols - c0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const bool perm_in = job.kind == SOLVE_FULL || job.kind == SOLVE_LOWER;
+  for (int e = threadIdx.x; e < m * TRSM_NC; e += blockDim.x) {
+    const int i = e % m, c = e / m;
+    xs[c * ldx + i] = c < nc ? X.at(perm_in ? job.perm[i] : i, c0 + c) : 0.0;
+  }
+  __syncthreads();
+  const int nblk = (m + 31) / 32;
+  if (job.kind != SOLVE_UPPER) {
+    for (int b = 0; b < nblk; ++b) {
+      const int kb = b * 32, nb = min(32, m - kb);
+      for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+        const int i = e % 32, kk = e / 32;
+        blk[kk * 33 + i] = (i < nb && kk < nb) ? L.at(kb + i, kb + kk) : 0.0;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        double* col = xs + lane * ldx + kb;
+        double x[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = i < nb ? col[i] : 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 32; ++kk) {
+          const double xk = x[kk];
+#pragma unroll
+          for (int i = kk + 1; i < 32; ++i)
+            if (i < nb) x[i] = fma(-blk[kk * 33 + i], xk, x[i]);  // rows/cols >= nb are zero-padded
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i < nb) col[i] = x[i];
+      }
+      __syncthreads();
+      // rows below the block: (32-row group, 8-column group) items round-robin
+      // over the warps; a lane owns a row and runs 8 independent column chains.
+      {
+        const int rbeg = kb + nb, ng = (m - rbeg + 31) / 32, ncg = (nc + 7) / 8;
+        for (int it = warp; it < ng * ncg; it += nw) {
+          const int i = rbeg + (it / ncg) * 32 + lane, cb = (it % ncg) * 8;
+          if (i < m) {
+            double l[32];
+#pragma unroll
+            for (int kk = 0; kk < 32; ++kk) l[kk] = kk < nb ? L.at(i, kb + kk) : 0.0;
+            double acc[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] = xs[(cb + q) * ldx + i];
+#pragma unroll
+            for (int kk = 0; kk < 32; ++kk) {
+              if (kk < nb) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) acc[q] = fma(-l[kk], xs[(cb + q) * ldx + kb + kk], acc[q]);
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (cb + q < nc) xs[(cb + q) * ldx + i] = acc[q];
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (job.kind != SOLVE_LOWER) {
+    for (int b = nblk - 1; b >= 0; --b) {
+      const int kb = b * 32, nb = min(32, m - kb);
+      for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+        const int i = e % 32, kk = e / 32;
+        blk[kk * 33 + i] = (i < nb && kk < nb) ? L.at(kb + i, kb + kk) : 0.0;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        double* col = xs + lane * ldx + kb;
+        double x[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = i < nb ? col[i] : 0.0;
+#pragma unroll
+        for (int kk = 31; kk >= 0; --kk) {
+          if (kk < nb) {
+            x[kk] = x[kk] / blk[kk * 33 + kk];
+            const double xk = x[kk];
+#pragma unroll
+            for (int i = 0; i < kk; ++i) x[i] = fma(-blk[kk * 33 + i], xk, x[i]);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i < nb) col[i] = x[i];
+      }
+      __syncthreads();
+      // rows above the block (k descending), same work split as the forward sweep
+      {
+        const int ng = (kb + 31) / 32, ncg = (nc + 7) / 8;
+        for (int it = warp; it < ng * ncg; it += nw) {
+          const int i = (it / ncg) * 32 + lane, cb = (it % ncg) * 8;
+          if (i < kb) {
+            double u[32];
+#pragma unroll
+            for (int kk = 0; kk < 32; ++kk) u[kk] = kk < nb ? L.at(i, kb + kk) : 0.0;
+            double acc[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] = xs[(cb + q) * ldx + i];
+#pragma unroll
+            for (int kk = 31; kk >= 0; --kk) {
+              if (kk < nb) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) acc[q] = fma(-u[kk], xs[(cb + q) * ldx + kb + kk], acc[q]);
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (cb + q < nc) xs[(cb + q) * ldx + i] = acc[q];
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int e = threadIdx.x; e < m * nc; e += blockDim.x) {
+    const int i = e % m, c = e / m;
+    X.at(i, c0 + c) = xs[c * ldx + i];
+  }
+}
+
 __global__ void gather_rows_kernel(const GatherJob* __restrict__ jobs, const int2* __restrict__ tiles) {
   const int2 t = tiles[blockIdx.x];
   const GatherJob job = jobs[t.x];
@@ -297,6 +449,24 @@ __global__ void gather_rows_kernel(const GatherJob* __restrict__ jobs, const int
 void launch_trsm_block(const TrsmBlockJob* jobs, const int2* tiles, int ntiles, cudaStream_t st) {
   if (ntiles > 0) trsm_block_kernel<<<ntiles, 128, 0, st>>>(jobs, tiles);
 }
+
+void launch_trsm_chunk(const SolveJob* jobs, const int2* tiles, int ntiles, int max_m, cudaStream_t st) {
+  if (ntiles <= 0) return;
+  const size_t smem = sizeof(double) * size_t(TRSM_NC) * size_t(max_m | 1);
+  static size_t attr = 0;
+  if (smem > attr) {  // static shared memory (blk) counts against the 48 KB default too
+    const cudaError_t e = cudaFuncSetAttribute(trsm_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess)
+      fprintf(stderr, "trsm_chunk: cudaFuncSetAttribute(%zu) failed: %s\n", smem, cudaGetErrorString(e));
+    attr = smem;
+  }
+  trsm_chunk_kernel<<<ntiles, 256, smem, st>>>(jobs, tiles);
+  const cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess)
+    fprintf(stderr, "trsm_chunk launch failed: %s (ntiles %d, max_m %d, smem %zu)\n", cudaGetErrorString(e), ntiles, max_m, smem);
+}
+
+int trsm_chunk_cols() { return TRSM_NC; }
 
 void launch_gather_rows(const GatherJob* jobs, const int2* tiles, int ntiles, cudaStream_t st) {
   if (ntiles > 0) gather_rows_kernel<<<ntiles, 256, 0, st>>>(jobs, tiles);

@@ -134,6 +134,10 @@ struct TrsmBlockJob {
   int lower;
 };
 void launch_trsm_block(const TrsmBlockJob* jobs, const int2* tiles, int ntiles, cudaStream_t st);
+// Fused blocked left solve (FULL / LOWER / UPPER): tiles = (job, chunk of
+// trsm_chunk_cols() RHS columns); the chunk stays in shared memory.
+void launch_trsm_chunk(const SolveJob* jobs, const int2* tiles, int ntiles, int max_m, cudaStream_t st);
+int trsm_chunk_cols();
 // dst(i, :) = src(perm[i], :); tiles = (job, 4096-element chunk).
 struct GatherJob {
   Mat dst, src;

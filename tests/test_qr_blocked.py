@@ -140,3 +140,33 @@ def test_compressed_matches_exact_on_bench_family():
     (re, ke), (rc, kc) = out["exact"], out["compressed"]
     assert abs(rc - re) <= 1e-4 * re, (rc, re)
     assert all(abs(c - a) <= 0.1 * a for a, c in zip(ke, kc)), (ke, kc)
+
+
+@pytest.mark.parametrize("tol", [1e-6, 1e-4])
+def test_compressed_basis_keeps_member_stopping_rule(tol):
+    """basis_from_members through the compressed mode: members wider than the
+    compression threshold (numerically low-rank kernel blocks and one
+    full-rank noise member) are replaced by pivoted-Cholesky factors of their
+    Gram matrices. The resulting basis must still satisfy the reference's
+    per-member rule ||(I - Qs Qs^T) M_i||_F <= member_tol ||M_i||_F
+    (member_tol = tol / 2, linalg.cpp:276-297), with a rank within 10 % of the
+    exact mode's and Q orthonormal."""
+    rng = np.random.default_rng(11)
+    dim = 200
+    src = rng.uniform(0, 1, (dim, 3))
+    members = []
+    for w, shift in ((3000, 2.5), (700, 1.5), (64, 4.0), (30, 3.0)):
+        tgt = rng.uniform(0, 1, (w, 3)) + np.array([shift, 0, 0])
+        d = np.sqrt(((src[:, None, :] - tgt[None, :, :]) ** 2).sum(-1))
+        members.append(1.0 / d)
+    members.append(1e-3 * rng.standard_normal((dim, 100)))
+    concat = np.hstack(members)
+    offs = np.cumsum([0] + [m.shape[1] for m in members])
+    sq_e, r_e = h2._lib.basis_from_members(concat, offs, tol)
+    sq_c, r_c = h2._lib.basis_from_members(concat, offs, tol, qr_mode="compressed")
+    assert np.allclose(sq_c.T @ sq_c, np.eye(dim), atol=1e-12)
+    qs = sq_c[:, dim - r_c:]
+    for mem in members:
+        left = mem - qs @ (qs.T @ mem)
+        assert np.linalg.norm(left) <= 0.5 * tol * np.linalg.norm(mem) * 1.01, (r_c, r_e)
+    assert abs(r_c - r_e) <= max(2, 0.1 * r_e), (r_c, r_e)
