@@ -503,8 +503,69 @@ static void run_blocked_gemm(Ctx& c, const std::vector<SolveJob>& bj) {
   for (int b = nblk - 1; b >= 0; --b) block_step(bwd, b, false);
 }
 
+// Tolerance-parity mode (qr_mode = 2): wide A^-1 X / A^-T X applications as
+// DMMA GEMMs with the explicit inverse. Each distinct factor's inverse is
+// formed once (exact blocked solve of the identity); X is then overwritten
+// with Inv X (or Inv^T X) through a temporary, in memory-bounded groups.
+static void run_inverse(Ctx& c, const std::vector<SolveJob>& ij, size_t budget) {
+  std::map<const double*, size_t> idx;
+  std::vector<SolveJob> inv;  // identity right-hand sides, solved in place
+  std::vector<int> ns;
+  for (auto& s : ij)
+    if (idx.emplace(s.lu.p, ns.size()).second) ns.push_back(s.lu.rows);
+  std::vector<std::pair<int, int>> shapes;
+  for (int n : ns) shapes.push_back({n, n});
+  std::vector<DMat> invm = alloc_mats(c, shapes);
+  {
+    CopyBatch id;
+    for (auto& im : invm) id.ident(im.m);
+    id.run(c);
+    std::vector<SolveJob> sj(ns.size());
+    for (auto& s : ij) {
+      const size_t k = idx[s.lu.p];
+      sj[k] = SolveJob{s.lu, s.perm, invm[k].m, SOLVE_FULL};
+    }
+    run_blocked(c, sj);
+  }
+  size_t t0 = 0;
+  while (t0 < ij.size()) {
+    size_t t1 = t0, bytes = 0;
+    std::vector<std::pair<int, int>> ts;
+    while (t1 < ij.size()) {
+      const size_t need = sizeof(double) * size_t(ij[t1].X.rows) * ij[t1].X.cols + 32;
+      if (t1 > t0 && bytes + need > budget) break;
+      bytes += need;
+      ts.push_back({ij[t1].X.rows, ij[t1].X.cols});
+      ++t1;
+    }
+    std::vector<DMat> tmp = alloc_mats(c, ts);
+    GemmBatch gb;
+    CopyBatch cb;
+    for (size_t t = t0; t < t1; ++t) {
+      const SolveJob& s = ij[t];
+      const Mat A = invm[idx[s.lu.p]].m;
+      gemm1(gb, tmp[t - t0].m, s.kind == SOLVE_TRANSPOSE ? A.t() : A, s.X);
+      cb.copy(s.X, tmp[t - t0].m);
+    }
+    gb.run(c);
+    cb.run(c);
+    t0 = t1;
+  }
+}
+
 void SolveBatch::run(Ctx& c) {
   if (jobs.empty()) return;
+  if (c.fast_solve) {
+    std::vector<SolveJob> ij, rest;
+    for (auto& s : jobs)
+      ((s.kind == SOLVE_FULL || s.kind == SOLVE_TRANSPOSE) && s.X.cols >= 48 && s.lu.rows >= 64 ? ij : rest)
+          .push_back(s);
+    if (!ij.empty()) {
+      run_inverse(c, ij, size_t(2) << 30);
+      jobs = rest;
+      if (jobs.empty()) return;
+    }
+  }
   {
     // Wide left solves go through the blocked path (GEMM updates).
     std::vector<SolveJob> blocked, rest;

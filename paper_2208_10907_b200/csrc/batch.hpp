@@ -53,6 +53,9 @@ struct Ctx {
   // Compressed QR mode (qr_mode = 2): members replaced by pivoted-Cholesky
   // factors of their Gram matrices before the (blocked) QR (k_pchol.cu).
   bool qr_compress = false;
+  // Same mode: wide A^-1 / A^-T applications as GEMMs with explicit inverses
+  // (tolerance parity; SolveBatch::run).
+  bool fast_solve = false;
   void sync();            // stream sync + error word check
   void check_err();       // throws the reference's message for device errors
   // Names of the LU batches launched since the last sync, by tag: a singular

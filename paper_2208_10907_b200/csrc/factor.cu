@@ -1580,6 +1580,7 @@ void Problem::factor() {
   const int qmode = qm ? (std::string(qm) == "compressed" ? 2 : std::string(qm) == "blocked" ? 1 : 0) : opt.qr_mode;
   c.qr_blocked = qmode >= 1;
   c.qr_compress = qmode == 2;
+  c.fast_solve = qmode == 2 && getenv("H2G_EXACT_SOLVES") == nullptr;
   levels.clear();
   max_fill_resid.clear();
   Driver d(*this);
