@@ -339,8 +339,61 @@ std::vector<double> NormBatch::run(Ctx& c) {
   return out;
 }
 
+static void run_blocked_lu(Ctx& c, const LuJob& j, const std::string& name) {
+  const int n = j.A.rows;
+  double fl = 0;
+  for (double k = 0; k < n; ++k) fl += (n - k - 1) + 2.0 * (n - k - 1) * (n - k - 1);
+  c.add_flops(fl);
+  c.lu_names[++c.lu_tag] = {name};
+  const int tag = c.lu_tag;
+  Slab am = c.alloc(sizeof(double));
+  double* amax = static_cast<double*>(am.get());
+  auto ev = c.prof_begin();
+  launch_lu_amax(j, amax, c.stream);
+  constexpr int NB = 32;
+  for (int kb = 0; kb < n; kb += NB) {
+    const int nb = std::min(NB, n - kb);
+    launch_lu_panel(j, kb, nb, amax, c.err, tag, c.stream);
+    launch_lu_rows(j, kb, nb, c.stream);
+    const int r = n - kb - nb;
+    if (r > 0) {
+      GemmBatch gb;
+      gb.job(j.A.sub(kb + nb, kb + nb, r, r), true);
+      gb.seg(j.A.sub(kb + nb, kb, r, nb), j.A.sub(kb, kb + nb, nb, r), -1.0);
+      const bool pr = c.prof;
+      c.prof = false;  // the trailing GEMMs are part of this "lu" record
+      gb.run(c, tag);
+      c.prof = pr;
+      c.add_flops(-2.0 * r * double(nb) * r);  // counted once above (reference LU rule)
+    }
+    c.launches += 2;
+  }
+  c.prof_end("lu", ev, fl, 16.0 * n * double(n));
+  cuda_check(cudaGetLastError(), "blocked lu");
+}
+
 void LuBatch::run(Ctx& c) {
   if (jobs.empty()) return;
+  // Large blocks (the top system) go through the blocked LU: one CTA would
+  // walk a ~1000-column factorization alone (100 ms at the bench size).
+  static const bool unblocked = getenv("H2G_LU_UNBLOCKED") != nullptr;
+  if (!unblocked) {
+    std::vector<LuJob> small;
+    std::vector<std::string> snames;
+    for (size_t t = 0; t < jobs.size(); ++t) {
+      if (jobs[t].A.rows >= 384) {
+        run_blocked_lu(c, jobs[t], names[t]);
+      } else {
+        small.push_back(jobs[t]);
+        snames.push_back(names[t]);
+      }
+    }
+    if (small.size() != jobs.size()) {
+      jobs.swap(small);
+      names.swap(snames);
+      if (jobs.empty()) return;
+    }
+  }
   double fl = 0;
   for (auto& j : jobs) {
     const double n = j.A.rows;

@@ -103,6 +103,107 @@ __global__ void __launch_bounds__(NT, 2) lu_kernel(const LuJob* __restrict__ job
   }
 }
 
+// ---- blocked LU for large blocks (the top system) ---------------------------
+// Right-looking, panels of LU_NB columns: (1) lu_panel_kernel factors columns
+// [kb, kb+nb) on one CTA (pivot search, full-row swap over all n columns,
+// reciprocal scaling, in-panel rank-1 updates), (2) lu_rows_kernel applies
+// the panel's unit-lower steps to the panel rows of the columns to the right
+// (one thread per column, k ascending), (3) a DMMA GEMM does the trailing
+// update A22 = fma(L21, -U12, A22) with k ascending. Every element receives
+// the reference's updates fma(-l_ik, u_kj, a_ij) in ascending k (linalg.cpp:
+// 352-388): a row swap only moves a row's values and its multipliers
+// together, so delaying the right-hand columns' updates to the GEMM does not
+// change any element's sequence. Results equal lu_kernel's bit for bit.
+__global__ void __launch_bounds__(1024) lu_panel_kernel(LuJob job, int kb, int nb,
+                                                        const double* __restrict__ amax_p, ErrWord* err,
+                                                        int tag) {
+  const double amax = *amax_p;
+  __shared__ ValIdx red[32];
+  extern __shared__ double lcol[];
+  const Mat M = job.A;
+  const int n = M.rows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+  for (int k = kb; k < kb + nb; ++k) {
+    ValIdx best{-1.0, 0x7fffffff};
+    for (int i = k + threadIdx.x; i < n; i += blockDim.x) best = better(best, ValIdx{fabs(M.at(i, k)), i});
+    best = block_argmax(best, red);
+    if (best.v <= job.tol * amax) {
+      if (threadIdx.x == 0) raise_err(err, 2, 0, k, tag);
+      return;
+    }
+    const int p = best.i;
+    if (p != k) {
+      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        const double t = M.at(k, j);
+        M.at(k, j) = M.at(p, j);
+        M.at(p, j) = t;
+      }
+      if (threadIdx.x == 0) {
+        const int64_t t = job.perm[k];
+        job.perm[k] = job.perm[p];
+        job.perm[p] = t;
+      }
+      __syncthreads();
+    }
+    const double inv = 1.0 / M.at(k, k);
+    for (int i = k + 1 + threadIdx.x; i < n; i += blockDim.x) {
+      const double l = M.at(i, k) * inv;
+      M.at(i, k) = l;
+      lcol[i] = l;
+    }
+    __syncthreads();
+    for (int j = k + 1 + warp; j < kb + nb; j += nwarp) {
+      const double u = M.at(k, j);
+      for (int i = k + 1 + lane; i < n; i += 32) M.at(i, j) = fma(-lcol[i], u, M.at(i, j));
+    }
+    __syncthreads();
+  }
+}
+
+// Panel rows [kb, kb+nb) of the columns j >= kb + nb: a_ij -= l_ik u_kj for
+// k ascending, i in (k, kb+nb). One thread per column, values in registers.
+__global__ void __launch_bounds__(128) lu_rows_kernel(LuJob job, int kb, int nb) {
+  __shared__ double lblk[32 * 33];
+  const Mat M = job.A;
+  const int n = M.rows;
+  for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
+    const int i = e % 32, kk = e / 32;
+    lblk[kk * 33 + i] = (i < nb && kk < nb) ? M.at(kb + i, kb + kk) : 0.0;
+  }
+  __syncthreads();
+  const int j = kb + nb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = i < nb ? M.at(kb + i, j) : 0.0;
+#pragma unroll
+  for (int kk = 0; kk < 32; ++kk) {
+    const double u = x[kk];
+#pragma unroll
+    for (int i = kk + 1; i < 32; ++i)
+      if (i < nb) x[i] = fma(-lblk[kk * 33 + i], u, x[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (i < nb) M.at(kb + i, j) = x[i];
+}
+
+__global__ void lu_amax_kernel(LuJob job, double* out) {
+  __shared__ ValIdx red[32];
+  const Mat M = job.A;
+  const int n = M.rows;
+  ValIdx am{0.0, 0};
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < n; j += blockDim.x / 32)
+    for (int i = lane; i < n; i += 32) {
+      const double v = fabs(M.at(i, j));
+      if (v > am.v) am.v = v;
+    }
+  am = block_argmax(am, red);
+  if (threadIdx.x == 0) *out = am.v;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) job.perm[i] = i;
+}
+
 // Dot products of the reference's solve_transpose_in_place (linalg.cpp:487-495)
 // as GCC -O3 -mavx2 -mfma vectorises them: products of each 4-wide group are
 // rounded and added in order (no FMA), a trailing pair likewise, and an odd
@@ -470,6 +571,26 @@ int trsm_chunk_cols() { return TRSM_NC; }
 
 void launch_gather_rows(const GatherJob* jobs, const int2* tiles, int ntiles, cudaStream_t st) {
   if (ntiles > 0) gather_rows_kernel<<<ntiles, 256, 0, st>>>(jobs, tiles);
+}
+
+void launch_lu_amax(const LuJob& job, double* out, cudaStream_t st) {
+  lu_amax_kernel<<<1, 1024, 0, st>>>(job, out);
+}
+
+void launch_lu_panel(const LuJob& job, int kb, int nb, const double* amax, ErrWord* err, int tag,
+                     cudaStream_t st) {
+  const size_t smem = sizeof(double) * size_t(job.A.rows);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(lu_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    attr = smem;
+  }
+  lu_panel_kernel<<<1, 1024, smem, st>>>(job, kb, nb, amax, err, tag);
+}
+
+void launch_lu_rows(const LuJob& job, int kb, int nb, cudaStream_t st) {
+  const int ncols = job.A.rows - kb - nb;
+  if (ncols > 0) lu_rows_kernel<<<(ncols + 127) / 128, 128, 0, st>>>(job, kb, nb);
 }
 
 void launch_lu(const LuJob* jobs, int njobs, int max_n, ErrWord* err, int tag, cudaStream_t st) {
