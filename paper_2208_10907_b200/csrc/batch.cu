@@ -790,6 +790,14 @@ static void compress_members(Ctx& c, std::vector<QrBatch::Item>& items, size_t m
   old.clear();  // stream-ordered frees behind the copies
 }
 
+static int median_n(const std::vector<QrJob>& js) {
+  std::vector<int> ns;
+  for (auto& j : js) ns.push_back(j.n);
+  if (ns.empty()) return 1;
+  std::nth_element(ns.begin(), ns.begin() + ns.size() / 2, ns.end());
+  return ns[ns.size() / 2];
+}
+
 void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t mem_budget) {
   if (c.qr_compress) compress_members(c, items, mem_budget);
   const size_t n_items = items.size();
@@ -888,7 +896,7 @@ void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t m
       auto work = [&](const QrJob& j) { return double(j.m) * j.n; };
       std::fill(G.begin(), G.end(),
                 ecl ? std::max(1, std::min(8, atoi(ecl)))
-                    : blocked ? qrb_cluster_size(int(jobs.size()), min_n, max_m, max_nmem)
+                    : blocked ? qrb_cluster_size(int(jobs.size()), median_n(jobs), max_m, max_nmem)
                               : qr_cluster_size(int(jobs.size()), min_n, max_m, max_nmem));
       std::vector<size_t> ord(jobs.size());
       for (size_t q = 0; q < ord.size(); ++q) ord[q] = q;

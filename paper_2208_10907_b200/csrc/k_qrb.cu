@@ -599,13 +599,18 @@ void launch_qrb(const QrJob* jobs, int njobs, int max_m, int max_nmem, int clust
   cuda_check(cudaLaunchKernelEx(&cfg, qrb_kernel, jobs, max_nmem, max_m), "qrb launch");
 }
 
-int qrb_cluster_size(int njobs, int min_n, int max_m, int max_nmem) {
+// Cluster size for a batch whose typical basis has n columns: a cluster of g
+// CTAs splits the panel's CB-column blocks, so its speed-up is at most the
+// number of blocks; waves / min(g, blocks) is minimised (small batches of
+// compressed panels take large clusters, large batches small ones).
+int qrb_cluster_size(int njobs, int typ_n, int max_m, int max_nmem) {
   const size_t smem = qrb_smem_bytes(max_m, max_nmem);
   cudaFuncSetAttribute(qrb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   int best = 1;
   double best_cost = 1e30;
+  const int nblk = std::max(1, (typ_n + CB - 1) / CB);
   for (int g = 1; g <= 8; ++g) {
-    if (g > 1 && min_n < 2 * CB * g) break;
+    if (g > 1 && g > nblk) break;
     int fit = 0;
     cudaLaunchAttribute at[1];
     cudaLaunchConfig_t cfg = qrb_config(g, g, smem, nullptr, at);
@@ -615,7 +620,7 @@ int qrb_cluster_size(int njobs, int min_n, int max_m, int max_nmem) {
     }
     if (fit <= 0) continue;
     const int waves = (njobs + fit - 1) / fit;
-    const double cost = double(waves) / g * (1.0 + 0.02 * (g - 1));
+    const double cost = double(waves) / std::min(g, nblk) * (1.0 + 0.02 * (g - 1));
     if (cost < best_cost) {
       best_cost = cost;
       best = g;
