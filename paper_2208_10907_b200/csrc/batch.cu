@@ -790,6 +790,11 @@ static void compress_members(Ctx& c, std::vector<QrBatch::Item>& items, size_t m
   old.clear();  // stream-ordered frees behind the copies
 }
 
+void QrBatch::compress(Ctx& c, size_t mem_budget) {
+  if (c.qr_compress && !compressed) compress_members(c, items, mem_budget);
+  compressed = true;
+}
+
 static int median_n(const std::vector<QrJob>& js) {
   std::vector<int> ns;
   for (auto& j : js) ns.push_back(j.n);
@@ -799,7 +804,7 @@ static int median_n(const std::vector<QrJob>& js) {
 }
 
 void QrBatch::run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t mem_budget) {
-  if (c.qr_compress) compress_members(c, items, mem_budget);
+  if (c.qr_compress && !compressed) compress_members(c, items, mem_budget);
   const size_t n_items = items.size();
   int max_rows = 0;
   for (auto& it : items) max_rows = std::max(max_rows, it.m);

@@ -253,6 +253,10 @@ struct QrBatch {
   // Runs all QRs (in memory-bounded chunks); returns Q (row-major m x m in a
   // DMat whose view is Q as an m x m matrix) and ranks.
   void run(Ctx& c, std::vector<DMat>& Q, std::vector<int>& rank, size_t mem_budget);
+  // Compressed mode only: replace the wide members of every item now (the
+  // items then own narrow panels; run() does not compress them again).
+  void compress(Ctx& c, size_t mem_budget);
+  bool compressed = false;
 };
 
 }  // namespace h2g

@@ -483,6 +483,10 @@ struct Driver {
   // Boxes [kb, ke): chunked concat fill -> in-place QR -> sink.
   void run_bases_range(std::vector<Members>& rows, std::vector<Members>* cols, const FillFn& fill,
                        const SinkFn& sink, const std::function<void()>& flush, int64_t kb, int64_t ke) {
+    if (c.qr_compress) {
+      run_bases_range_compressed(rows, cols, fill, sink, flush, kb, ke);
+      return;
+    }
     const int64_t m = ke;
     int64_t k0 = kb;
     while (k0 < m) {
@@ -538,6 +542,78 @@ struct Driver {
       }
       k0 = k1;
     }
+  }
+
+  // Compressed mode: the member panels are filled and compressed chunk by
+  // chunk (the wide panels never coexist beyond the memory budget), then one
+  // QR launch factors every compressed panel of the range and the sinks run.
+  void run_bases_range_compressed(std::vector<Members>& rows, std::vector<Members>* cols,
+                                  const FillFn& fill, const SinkFn& sink,
+                                  const std::function<void()>& flush, int64_t kb, int64_t ke) {
+    QrBatch all;
+    all.compressed = true;
+    int64_t k0 = kb;
+    while (k0 < ke) {
+      size_t bytes = 0;
+      int64_t k1 = k0;
+      while (k1 < ke) {
+        size_t need = rows[k1].bytes() + (cols ? (*cols)[k1].bytes() : 0);
+        need += need / 16 + 65536;
+        if (k1 > k0 && bytes + need > opt.qr_mem_budget) break;
+        bytes += need;
+        ++k1;
+      }
+      for (int64_t k = k0; k < k1; ++k) {
+        alloc_concat(rows[k]);
+        if (cols) alloc_concat((*cols)[k]);
+      }
+      fill(k0, k1);
+      QrBatch qb;
+      for (int64_t k = k0; k < k1; ++k) {
+        qb.add(rows[k].concat, rows[k].dim, rows[k].width, rows[k].offs, opt.tol, opt.cap, true);
+        rows[k].concat = DMat{};
+      }
+      if (cols)
+        for (int64_t k = k0; k < k1; ++k) {
+          qb.add((*cols)[k].concat, (*cols)[k].dim, (*cols)[k].width, (*cols)[k].offs, opt.tol, opt.cap, true);
+          (*cols)[k].concat = DMat{};
+        }
+      qb.compress(c, opt.qr_mem_budget);
+      for (auto& it : qb.items) all.items.push_back(std::move(it));
+      k0 = k1;
+    }
+    // all.items: per chunk, the chunk's rows then its cols; map back per box.
+    std::vector<size_t> at_row(size_t(ke - kb)), at_col(size_t(ke - kb));
+    {
+      size_t t = 0;
+      int64_t a = kb;
+      while (a < ke) {
+        // recover the chunk boundaries in the same way as above
+        size_t bytes = 0;
+        int64_t b = a;
+        while (b < ke) {
+          size_t need = rows[b].bytes() + (cols ? (*cols)[b].bytes() : 0);
+          need += need / 16 + 65536;
+          if (b > a && bytes + need > opt.qr_mem_budget) break;
+          bytes += need;
+          ++b;
+        }
+        for (int64_t k = a; k < b; ++k) at_row[size_t(k - kb)] = t++;
+        if (cols)
+          for (int64_t k = a; k < b; ++k) at_col[size_t(k - kb)] = t++;
+        a = b;
+      }
+    }
+    std::vector<DMat> Q;
+    std::vector<int> rank;
+    all.run(c, Q, rank, opt.qr_mem_budget);
+    for (int64_t k = kb; k < ke; ++k) {
+      const size_t r = at_row[size_t(k - kb)];
+      const Mat qc = cols ? Q[at_col[size_t(k - kb)]].m : Mat{};
+      const int rc = cols ? rank[at_col[size_t(k - kb)]] : 0;
+      sink(k, Q[r].m, rank[r], qc, rc);
+    }
+    if (flush) flush();
   }
 
   // Off-diagonal fills of a level indexed by row and by column, each list in
