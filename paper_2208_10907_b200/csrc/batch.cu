@@ -678,7 +678,7 @@ static void compress_members(Ctx& c, std::vector<QrBatch::Item>& items, size_t m
   for (size_t t = 0; t < items.size(); ++t) {
     const auto& it = items[t];
     if (it.m == 0 || it.n == 0) continue;
-    for (size_t s = 0; s + 1 < it.offs.size(); ++s) {
+    for (size_t s = size_t(it.fixed); s + 1 < it.offs.size(); ++s) {
       const int w = int(it.offs[s + 1] - it.offs[s]);
       if (w >= kPcholMinWidth) wide.push_back({t, int(s), w, std::min(it.m, w)});
     }

@@ -243,6 +243,7 @@ struct QrBatch {
     double tol;
     int cap;
     bool inplace;  // factor the concat itself (it is consumed)
+    int fixed = 0;  // compressed mode: members [0, fixed) are already compressed
   };
   std::vector<Item> items;
   int add(DMat concat, int m, int n, std::vector<int64_t> offs, double tol, int cap,

@@ -355,6 +355,7 @@ struct Driver {
     int width = 0;
     std::vector<int64_t> offs{0};
     DMat concat;
+    int fixed = 0;  // compressed mode: members [0, fixed) are already compressed
     Mat slice(int off, int w) const {
       const int ld = std::max(2, (dim + 1) & ~1);
       return Mat{concat.m.p + int64_t(off) * ld, dim, w, 1, ld};
@@ -571,6 +572,7 @@ struct Driver {
       QrBatch qb;
       for (int64_t k = k0; k < k1; ++k) {
         qb.add(rows[k].concat, rows[k].dim, rows[k].width, rows[k].offs, opt.tol, opt.cap, true);
+        qb.items.back().fixed = rows[k].fixed;
         rows[k].concat = DMat{};
       }
       if (cols)
@@ -579,6 +581,19 @@ struct Driver {
           (*cols)[k].concat = DMat{};
         }
       qb.compress(c, opt.qr_mem_budget);
+      if (save_rows_) {  // keep a copy of each compressed row panel (the QR consumes it)
+        CopyBatch cb;
+        for (int64_t k = k0; k < k1; ++k) {
+          const auto& it = qb.items[size_t(k - k0)];
+          saved_rows_[size_t(k)].offs = it.offs;
+          saved_rows_[size_t(k)].dim = it.m;
+          saved_rows_[size_t(k)].width = it.n;
+          saved_rows_[size_t(k)].concat = alloc_mat(c, ldc(it.m), std::max(it.n, 1));
+          saved_rows_[size_t(k)].concat.m = Mat{saved_rows_[size_t(k)].concat.m.p, it.m, it.n, 1, ldc(it.m)};
+          if (it.n > 0 && it.m > 0) cb.copy(saved_rows_[size_t(k)].concat.m, it.concat.m);
+        }
+        cb.run(c);
+      }
       for (auto& it : qb.items) all.items.push_back(std::move(it));
       k0 = k1;
     }
@@ -615,6 +630,11 @@ struct Driver {
     }
     if (flush) flush();
   }
+
+  // Compressed mode, leaf coupling: the provisional pass's compressed row
+  // panels, reused as the first members of the final row panels.
+  bool save_rows_ = false;
+  std::vector<Members> saved_rows_;
 
   // Off-diagonal fills of a level indexed by row and by column, each list in
   // the FillSet's (map) order, so that "for every fill with key.first == i"
@@ -696,11 +716,18 @@ struct Driver {
     std::vector<DMat> X(m);
     std::vector<int> provR(m, 0);
     std::vector<std::vector<std::pair<int64_t, int>>> couple_at(m);
+    bool reuse = false;
     if (coupling) {
       // Provisional row bases (compression.cpp:203-211), kept as Qs_p.
       std::vector<Members> prow = rows;
       std::vector<DMat> provQs(m);
       CopyBatch provcopies;
+      // Compressed mode: the provisional members' compressed panels are kept
+      // and become the first members of the final row panels (the final
+      // row members are the provisional ones plus the coupling products).
+      reuse = c.qr_compress;
+      save_rows_ = reuse;
+      if (reuse) saved_rows_.assign(size_t(m), Members{});
       run_bases(prow, nullptr,
                 [&](int64_t k0, int64_t k1) {
                   CopyBatch cb;
@@ -718,6 +745,20 @@ struct Driver {
                   provcopies.run(c);
                   provcopies.jobs.clear();
                 });
+      save_rows_ = false;
+      if (reuse) {
+        const auto [lo, hi] = own_range(m);
+        for (int64_t i = 0; i < m; ++i) {
+          Members R;
+          R.dim = sys.dims[i];
+          if (i >= lo && i < hi) {
+            R.offs = saved_rows_[size_t(i)].offs;
+            R.width = saved_rows_[size_t(i)].width;
+          }
+          R.fixed = int(R.offs.size()) - 1;
+          rows[i] = std::move(R);
+        }
+      }
       // X_p = A_pp^-1 Qs_p; coupling member A_ip X_p for p in near(i).
       SolveBatch sb;
       for (int64_t p = 0; p < m; ++p) {
@@ -738,7 +779,14 @@ struct Driver {
                 CopyBatch cb;
                 EvalBatch eb;
                 GemmBatch gb;
-                fill_base_rows(rows, k0, k1, cb, eb);
+                if (reuse) {
+                  for (int64_t i = k0; i < k1; ++i) {
+                    const Members& sv = saved_rows_[size_t(i)];
+                    if (sv.width > 0 && sv.dim > 0) cb.copy(rows[i].slice(0, sv.width), sv.concat.m);
+                  }
+                } else {
+                  fill_base_rows(rows, k0, k1, cb, eb);
+                }
                 for (int64_t i = k0; i < k1; ++i)
                   for (auto [p, off] : couple_at[i])
                     gemm1(gb, rows[i].slice(off, provR[p]), block(sys, i, p), X[p].m);
@@ -771,6 +819,7 @@ struct Driver {
                 sqcopies.run(c);
                 sqcopies.jobs.clear();
               });
+    saved_rows_.clear();
   }
 
   // ---- build_leaf_pieces (ulv.cpp:336-401) -----------------------------------
