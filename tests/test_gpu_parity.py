@@ -246,3 +246,27 @@ def test_blr2_bitwise_vs_live_reference(n, leaf):
     xr, xg = r.solve(b), p.solve(b)
     assert np.array_equal(xg.view(np.int64), xr.view(np.int64))
     assert np.linalg.norm(p.matvec(xg) - b) / np.linalg.norm(b) < 1e-6
+
+
+def test_fused_trsm_path_is_bitwise(golden):
+    """The opt-in single-launch blocked solve (H2G_TRSM_FUSED=1, k_lu.cu
+    trsm_chunk_kernel) gives the reference's solution bit for bit on the C1
+    case (the env switch is read once per process, hence the subprocess)."""
+    import os
+    import subprocess
+    import sys
+    rec = golden[0]["cases"]["c1_cube4096"]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_2208_10907_b200 as h2\n"
+        "from oracle import cpu, ref\n"
+        "xyz, q = cpu.generate('cube', 4096, 42)\n"
+        "p = h2.Problem(); p.set_kernel('laplace', 0.0, 1.0, 1e-3); p.set_options(tol=1e-8)\n"
+        "p.build(xyz, q, 128); p.factor(); x = p.solve(ref.splitmix_signed(4096, 7))\n"
+        "print(ref.fnv64(np.ascontiguousarray(x, dtype=np.float64).view(np.int64).ravel()))\n" % root)
+    env = dict(os.environ, H2G_TRSM_FUSED="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.strip().splitlines()[-1] == str(rec["x_fnv"])
