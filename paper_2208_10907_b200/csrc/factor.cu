@@ -858,6 +858,25 @@ struct Driver {
       gb.run(c);
       sb.run(c);
     }
+    // The generated-B GEMM's A operands, stored column-major with an even
+    // leading dimension (Us_c^T and q_cp; the views above are transposes):
+    // the producers then move A by 16-byte row pairs. Same values, same order.
+    std::map<int64_t, DMat> usT;
+    std::map<std::pair<int64_t, int64_t>, DMat> qcm;
+    {
+      CopyBatch cb;
+      auto colmajor_copy = [&](const Mat& src) {
+        const int ld = (src.rows + 1) & ~1;
+        DMat d = alloc_mat(c, ld, std::max(src.cols, 1));
+        d.m = Mat{d.m.p, src.rows, src.cols, 1, ld};
+        if (src.rows > 0 && src.cols > 0) cb.copy(d.m, src);
+        return d;
+      };
+      for (int64_t cc = lo; cc < hi; ++cc)
+        if (Ub[cc].rank > 0) usT[cc] = colmajor_copy(Ub[cc].Qs().t());
+      for (auto& [key, m] : qT) qcm[key] = colmajor_copy(m.m.t());
+      cb.run(c);
+    }
     // Pieces: Us_c^T A(c, J) - sum_p q_cp A(p, J)[masked], B generated in-kernel.
     std::vector<std::pair<int64_t, TargetKey>> pkeys;
     std::vector<std::pair<int, int>> shapes;
@@ -875,7 +894,7 @@ struct Driver {
       const int64_t jb = rb(tk.first, tk.second), je = jb + rs(tk.first, tk.second);
       const int w = int(je - jb);
       gb.job(mats[t].m, false);
-      gb.seg_gen(Ub[cc].Qs().t(), rb(L, cc), jb, w, false, 1.0);
+      gb.seg_gen(Ub[cc].rank > 0 ? usT.at(cc).m : Ub[cc].Qs().t(), rb(L, cc), jb, w, false, 1.0);
       if (Ub[cc].rank > 0 && sys.offdiag)
         for (int64_t x = 0; x < S.nnear(L, cc); ++x) {
           const int64_t p = S.near(L, cc)[x];
@@ -883,7 +902,7 @@ struct Driver {
           bool all_zero;
           auto mask = mask_for(L, p, jb, je, all_zero);
           if (all_zero) continue;
-          gb.seg_gen(qT[{cc, p}].m.t(), rb(L, p), jb, w, false, -1.0, mask);
+          gb.seg_gen(qcm.at({cc, p}).m, rb(L, p), jb, w, false, -1.0, mask);
         }
     }
     {
