@@ -822,6 +822,16 @@ struct Driver {
     saved_rows_.clear();
   }
 
+  // A column-major copy (even leading dimension) of a strided view, queued on
+  // cb: generated-B GEMM producers move such A operands by 16-byte pairs.
+  DMat colmajor_copy(CopyBatch& cb, const Mat& src) {
+    const int ld = (src.rows + 1) & ~1;
+    DMat d = alloc_mat(c, std::max(ld, 2), std::max(src.cols, 1));
+    d.m = Mat{d.m.p, src.rows, src.cols, 1, std::max(ld, 2)};
+    if (src.rows > 0 && src.cols > 0) cb.copy(d.m, src);
+    return d;
+  }
+
   // ---- build_leaf_pieces (ulv.cpp:336-401) -----------------------------------
   void build_leaf_pieces(SysL& sys, const FillSet& fills, std::vector<PieceMap>& pieces,
                          double* level_max) {
@@ -865,16 +875,9 @@ struct Driver {
     std::map<std::pair<int64_t, int64_t>, DMat> qcm;
     {
       CopyBatch cb;
-      auto colmajor_copy = [&](const Mat& src) {
-        const int ld = (src.rows + 1) & ~1;
-        DMat d = alloc_mat(c, ld, std::max(src.cols, 1));
-        d.m = Mat{d.m.p, src.rows, src.cols, 1, ld};
-        if (src.rows > 0 && src.cols > 0) cb.copy(d.m, src);
-        return d;
-      };
       for (int64_t cc = lo; cc < hi; ++cc)
-        if (Ub[cc].rank > 0) usT[cc] = colmajor_copy(Ub[cc].Qs().t());
-      for (auto& [key, m] : qT) qcm[key] = colmajor_copy(m.m.t());
+        if (Ub[cc].rank > 0) usT[cc] = colmajor_copy(cb, Ub[cc].Qs().t());
+      for (auto& [key, m] : qT) qcm[key] = colmajor_copy(cb, m.m.t());
       cb.run(c);
     }
     // Pieces: Us_c^T A(c, J) - sum_p q_cp A(p, J)[masked], B generated in-kernel.
@@ -1145,6 +1148,7 @@ struct Driver {
               [&](int64_t k0, int64_t k1) {
                 CopyBatch cb;
                 GemmBatch gb;
+                std::vector<DMat> keep;  // A operands alive until the GEMMs are queued
                 for (int64_t k = k0; k < k1; ++k) {
                   int off = 0;
                   for (const DMat* F : FI.by_row[k]) {
@@ -1166,15 +1170,22 @@ struct Driver {
                     cols_to_merged(gb, cols[k].slice(off, piece.rows).t(), {piece}, k);
                     off += piece.rows;
                   }
-                  for (auto [l2, I] : ancestor_far_partners(lvl, k)) {
+                  const auto anc = ancestor_far_partners(lvl, k);
+                  if (anc.empty()) continue;
+                  // Vbig_c^T column-major (even ld) for the generated GEMMs' A.
+                  const Mat v0 = Vbig[2 * k], v1 = Vbig[2 * k + 1];
+                  keep.push_back(colmajor_copy(cb, v0.t()));
+                  const Mat v0T = keep.back().m;
+                  keep.push_back(colmajor_copy(cb, v1.t()));
+                  const Mat v1T = keep.back().m;
+                  for (auto [l2, I] : anc) {
                     // (A(I, c0) Vbig_c0 | A(I, c1) Vbig_c1)^T, B generated in-kernel.
                     const int w = int(rs(l2, I));
                     const Mat dst = cols[k].slice(off, w);
-                    const Mat v0 = Vbig[2 * k], v1 = Vbig[2 * k + 1];
                     gb.job(dst.sub(0, 0, v0.cols, w), false);
-                    gb.seg_gen(v0.t(), rb(l2, I), rb(lvl + 1, 2 * k), w, true, 1.0);
+                    gb.seg_gen(v0T, rb(l2, I), rb(lvl + 1, 2 * k), w, true, 1.0);
                     gb.job(dst.sub(v0.cols, 0, v1.cols, w), false);
-                    gb.seg_gen(v1.t(), rb(l2, I), rb(lvl + 1, 2 * k + 1), w, true, 1.0);
+                    gb.seg_gen(v1T, rb(l2, I), rb(lvl + 1, 2 * k + 1), w, true, 1.0);
                     off += w;
                   }
                 }
