@@ -1050,18 +1050,46 @@ struct Driver {
         shapes.push_back({sys.dims[Pp], int(je - jb)});
       }
       auto mats = alloc_mats(c, shapes);
+      // Tolerance-parity mode: reassociate A_KP (A_PP^-1 S_P) as (A_KP A_PP^-1) S_P,
+      // with W_KP = A_KP A_PP^-1 formed once per near pair, so the wide
+      // A_PP^-1 S_P products are never formed (g then holds the masked S_P).
+      const bool reassoc = c.fast_solve;
       CopyBatch cb, zb;
       SolveBatch sb;
       for (size_t t = 0; t < gkeys.size(); ++t) {
         const auto [Pp, tk] = gkeys[t];
         cb.copy(mats[t].m, stack[Pp].at(tk).m);
         for (auto& r : gmasks[t]) zb.zero(mats[t].m.sub(0, r.x, mats[t].rows(), r.y - r.x));
-        sb.add(sys.diag_lu[Pp], mats[t].m, SOLVE_FULL);
+        if (!reassoc) sb.add(sys.diag_lu[Pp], mats[t].m, SOLVE_FULL);
         g[gkeys[t]] = mats[t];
       }
       cb.run(c);
       zb.run(c);
       sb.run(c);
+      std::map<std::pair<int64_t, int64_t>, DMat> Wkp;
+      if (reassoc) {
+        // W_KP^T = A_PP^-T A_KP^T: one transpose solve per (K, P) near pair.
+        std::vector<std::pair<int64_t, int64_t>> pk;
+        std::vector<std::pair<int, int>> ws;
+        for (int64_t K = lo; K < hi; ++K)
+          for (int64_t x = 0; x < S.nnear(lvl, K); ++x) {
+            const int64_t Pp = S.near(lvl, K)[x];
+            if (Pp == K || sys.dims[K] == 0 || sys.dims[Pp] == 0) continue;
+            pk.push_back({K, Pp});
+            ws.push_back({sys.dims[Pp], sys.dims[K]});
+          }
+        auto wm = alloc_mats(c, ws);
+        CopyBatch wc;
+        SolveBatch wsb;
+        for (size_t t = 0; t < pk.size(); ++t) {
+          const auto [K, Pp] = pk[t];
+          wc.copy(wm[t].m, block(sys, K, Pp).t());
+          wsb.add(sys.diag_lu[Pp], wm[t].m, SOLVE_TRANSPOSE);
+          Wkp[pk[t]] = wm[t];
+        }
+        wc.run(c);
+        wsb.run(c);
+      }
       // corrected = stack - sum_P A_KP g(P, tk), accumulated over P in order.
       std::vector<std::pair<int64_t, TargetKey>> keys;
       std::vector<std::pair<int, int>> cshapes;
@@ -1086,7 +1114,7 @@ struct Driver {
           if (it == g.end()) continue;
           if (!any) gb.job(cm[t].m, true);
           any = true;
-          gb.seg(block(sys, K, Pp), it->second.m, -1.0);
+          gb.seg(reassoc ? Wkp.at({K, Pp}).m.t() : block(sys, K, Pp), it->second.m, -1.0);
         }
       }
       cc.run(c);
