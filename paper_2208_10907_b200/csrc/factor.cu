@@ -126,7 +126,12 @@ void Problem::build(const double* d_xyz, const double* d_q, int64_t n, int64_t l
   cuda_check(cudaMemcpyAsync(be.data(), T.be, sizeof(int64_t) * 2 * nn, cudaMemcpyDeviceToHost,
                              c.stream),
              "be d2h");
+  std::vector<double> hq(size_t(std::max<int64_t>(n, 1)));
+  if (n > 0)
+    cuda_check(cudaMemcpyAsync(hq.data(), d_q, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, c.stream),
+               "q d2h");
   c.sync();
+  uniform_q = n > 0 && std::all_of(hq.begin(), hq.begin() + n, [&](double v) { return v == hq[0]; });
   double t1 = now_s();
   classify_device(T, opt.eta, opt.structure != 0 ? 1 : 0, S, c.stream);
   if (opt.structure == 2) {
@@ -717,6 +722,8 @@ struct Driver {
     std::vector<int> provR(m, 0);
     std::vector<std::vector<std::pair<int64_t, int>>> couple_at(m);
     bool reuse = false;
+    bool col_reuse = false;
+    std::vector<int> col_reuse_off;
     if (coupling) {
       // Provisional row bases (compression.cpp:203-211), kept as Qs_p.
       std::vector<Members> prow = rows;
@@ -746,6 +753,28 @@ struct Driver {
                   provcopies.jobs.clear();
                 });
       save_rows_ = false;
+      if (reuse && P.uniform_q && getenv("H2G_NO_COL_REUSE") == nullptr) {
+        // Equal charges: the column members A(j, i)^T (j far) and A(I, i)^T (I
+        // an ancestor's far partner) equal the row members A(i, j), A(i, I)
+        // bit for bit and come in the same order, so the final column panels
+        // take the provisional pass's compressed far/ancestor members first
+        // (already compressed) and their own fill members after them.
+        const auto [lo, hi] = own_range(m);
+        col_reuse_off.assign(size_t(m), 0);
+        for (int64_t i = lo; i < hi; ++i) {
+          const Members& sv = saved_rows_[size_t(i)];
+          const size_t nf = FI.by_row[i].size();
+          const size_t nmem = sv.offs.size() - 1;
+          Members C;
+          C.dim = sys.dims[i];
+          for (size_t s = nf; s < nmem; ++s) C.add(int(sv.offs[s + 1] - sv.offs[s]));
+          C.fixed = int(nmem - nf);
+          for (const DMat* F : FI.by_col[i]) C.add(F->rows());
+          col_reuse_off[size_t(i)] = int(sv.offs[nf]);
+          cols[i] = std::move(C);
+        }
+        col_reuse = true;
+      }
       if (reuse) {
         const auto [lo, hi] = own_range(m);
         for (int64_t i = 0; i < m; ++i) {
@@ -791,7 +820,20 @@ struct Driver {
                   for (auto [p, off] : couple_at[i])
                     gemm1(gb, rows[i].slice(off, provR[p]), block(sys, i, p), X[p].m);
                 // Column members: F(c, j)^T | A(i, j)^T | A(I, j)^T.
-                for (int64_t j = k0; j < k1; ++j) {
+                for (int64_t j = k0; j < k1 && col_reuse; ++j) {
+                  // reused far/ancestor members first, then the fill members
+                  Members& C = cols[j];
+                  const Members& sv = saved_rows_[size_t(j)];
+                  const int w0 = sv.width - col_reuse_off[size_t(j)];
+                  if (w0 > 0 && C.dim > 0)
+                    cb.copy(C.slice(0, w0), sv.concat.m.sub(0, col_reuse_off[size_t(j)], C.dim, w0));
+                  int off = w0;
+                  for (const DMat* F : FI.by_col[j]) {
+                    cb.copy(C.slice(off, F->rows()).t(), F->m);
+                    off += F->rows();
+                  }
+                }
+                for (int64_t j = k0; j < k1 && !col_reuse; ++j) {
                   Members& C = cols[j];
                   int off = 0;
                   for (const DMat* F : FI.by_col[j]) {

@@ -89,6 +89,9 @@ class Problem {
   LuF top;
   std::vector<double> max_fill_resid;
   bool built = false, factored = false;
+  // All charges equal: A(I, i)^T == A(i, I) bit for bit (kernel_pair is
+  // symmetric in the two points), so column members can reuse row members.
+  bool uniform_q = false;
   bool auto_budget_ = true;
   // Multi-GPU level partition (null: single GPU). The partitioned stages
   // compute only this rank's box range and all-gather their outputs, so
