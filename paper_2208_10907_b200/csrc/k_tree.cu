@@ -6,9 +6,9 @@
 //   seed_kernel    farthest pair of 32 strided candidates (first strict max
 //                  in (a, b) loop order), one warp per node;
 //   lloyd_kernel   <=100 Lloyd iterations, one CTA per node: assignment in
-//                  parallel, centroid sums as sequential chains (lanes 0-5 of
-//                  warp 0; adding +0.0 for the other cluster is exact), then
-//                  the signed margins;
+//                  parallel, centroid sums as sequential chains over the
+//                  members compacted per chunk in shared memory (one warp
+//                  per cluster), then the signed margins;
 //   merge passes   stable merge sort of the margins inside every node, each
 //                  element placed by binary search in the sibling run
 //                  (std::stable_sort semantics incl. -0.0 == +0.0);
@@ -88,60 +88,95 @@ __global__ void seed_kernel(TreeBufs P, const int64_t* be, int level, double* ce
 
 constexpr int LT = 256;
 
+// Lloyd iterations of one node (geometry.cpp:148-170). Per iteration the
+// points stream through in chunks of LT (one point per thread, the next
+// chunk prefetched into registers): each thread assigns its point, the
+// chunk's members are compacted in point order into shared memory per
+// cluster (ballot + warp-count scan), and lanes 0-2 of warp 0 (cluster 0)
+// and warp 1 (cluster 1) extend their sequential coordinate sums over the
+// compacted members. Each chain adds exactly the reference's members in the
+// reference's order, so the sums are bitwise the reference's; the two
+// clusters' chains run concurrently and never wait on global loads.
 __global__ void __launch_bounds__(LT) lloyd_kernel(TreeBufs P, const int64_t* be, int level,
                                                    double* cent, unsigned char* assign,
                                                    double* margin) {
   __shared__ double c[6];
   __shared__ double sums[6];
-  __shared__ long long n1s;
+  __shared__ int wc[LT / 32];
+  __shared__ double mv[2][3][LT];
   const int node = blockIdx.x;
   const int64_t hb = (int64_t(1) << level) - 1 + node;
   const int64_t b = be[2 * hb], e = be[2 * hb + 1], len = e - b;
+  const int wid = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  const bool chain = wid < 2 && ln < 3;
   if (threadIdx.x < 6) c[threadIdx.x] = cent[6 * node + threadIdx.x];
   for (int64_t i = threadIdx.x; i < len; i += LT) assign[b + i] = 0;
   __syncthreads();
   for (int iter = 0; iter < 100; ++iter) {
     int changed = 0;
-    for (int64_t i = threadIdx.x; i < len; i += LT) {
-      const int64_t p = b + i;
-      const double px = P.x[p], py = P.y[p], pz = P.z[p];
-      const unsigned char a = d2(px, py, pz, c[3], c[4], c[5]) < d2(px, py, pz, c[0], c[1], c[2]);
-      if (a != assign[p]) {
-        assign[p] = a;
-        changed = 1;
+    double s = 0.0;
+    int64_t n1 = 0;  // members of cluster 0 (uniform)
+    double px = 0.0, py = 0.0, pz = 0.0;
+    unsigned char pa = 0;
+    if (threadIdx.x < len) {
+      px = P.x[b + threadIdx.x]; py = P.y[b + threadIdx.x]; pz = P.z[b + threadIdx.x];
+      pa = assign[b + threadIdx.x];
+    }
+    for (int64_t i0 = 0; i0 < len; i0 += LT) {
+      const int64_t i = i0 + threadIdx.x;
+      const bool live = i < len;
+      const double cx = px, cy = py, cz = pz;
+      const unsigned char old = pa;
+      if (i + LT < len) {
+        px = P.x[b + i + LT]; py = P.y[b + i + LT]; pz = P.z[b + i + LT];
+        pa = assign[b + i + LT];
       }
+      unsigned char a = 0;
+      if (live) {
+        a = d2(cx, cy, cz, c[3], c[4], c[5]) < d2(cx, cy, cz, c[0], c[1], c[2]);
+        if (a != old) {
+          assign[b + i] = a;
+          changed = 1;
+        }
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, live && a == 0);
+      if (ln == 0) wc[wid] = __popc(bal);
+      __syncthreads();  // also: the previous chunk's chains are done with mv
+      int off = 0, tot = 0;
+#pragma unroll
+      for (int w = 0; w < LT / 32; ++w) {
+        const int cw = wc[w];
+        off += w < wid ? cw : 0;
+        tot += cw;
+      }
+      if (live) {
+        const int r0 = off + __popc(bal & ((1u << ln) - 1u));
+        const int cl = a == 0 ? 0 : 1, r = a == 0 ? r0 : threadIdx.x - r0;
+        mv[cl][0][r] = cx;
+        mv[cl][1][r] = cy;
+        mv[cl][2][r] = cz;
+      }
+      __syncthreads();
+      if (chain) {
+        const int64_t rem = len - i0;
+        const int m = wid == 0 ? tot : int(rem < LT ? rem : LT) - tot;
+        const double* v = mv[wid][ln];
+        int k = 0;
+        for (; k + 8 <= m; k += 8) {
+          double t[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) t[u] = v[k + u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) s += t[u];
+        }
+        for (; k < m; ++k) s += v[k];
+      }
+      n1 += tot;
     }
     changed = __syncthreads_or(changed);
-    // Sequential centroid sums (geometry.cpp:160-165): lane d sums coord d
-    // of cluster d / 3, in point order.
-    if (threadIdx.x < 6) {
-      const int d = threadIdx.x % 3;
-      const unsigned char want = threadIdx.x >= 3;
-      const double* src = d == 0 ? P.x : (d == 1 ? P.y : P.z);
-      double s = 0.0;
-      long long cnt = 0;
-      int64_t i = 0;
-      for (; i + 4 <= len; i += 4) {
-        const double v0 = src[b + i], v1 = src[b + i + 1], v2 = src[b + i + 2], v3 = src[b + i + 3];
-        const unsigned char a0 = assign[b + i], a1 = assign[b + i + 1], a2 = assign[b + i + 2],
-                            a3 = assign[b + i + 3];
-        s += (a0 == want) ? v0 : 0.0;
-        s += (a1 == want) ? v1 : 0.0;
-        s += (a2 == want) ? v2 : 0.0;
-        s += (a3 == want) ? v3 : 0.0;
-        cnt += (a0 == 0) + (a1 == 0) + (a2 == 0) + (a3 == 0);
-      }
-      for (; i < len; ++i) {
-        const unsigned char a = assign[b + i];
-        s += (a == want) ? src[b + i] : 0.0;
-        cnt += (a == 0);
-      }
-      sums[threadIdx.x] = s;
-      if (threadIdx.x == 0) n1s = cnt;
-    }
+    if (chain) sums[3 * wid + ln] = s;
     __syncthreads();
     if (threadIdx.x < 6) {
-      const long long n1 = n1s;
       if (threadIdx.x < 3) {
         if (n1 > 0) c[threadIdx.x] = sums[threadIdx.x] / double(n1);
       } else {
