@@ -117,11 +117,16 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def splitmix_signed(n, seed):
+    from paper_2208_10907_b200.pipeline import splitmix_signed as f
+    return f(n, seed)
+
+
 def make_points(n, seed):
-    from paper_2208_10907_b200.pipeline import _fib_spheres
-    if seed == 42:
-        return _fib_spheres(n, 1, 3.0, seed)
-    return _fib_spheres(n, 1, 3.0, seed)
+    """The reference's unit-sphere cloud (geometry.cpp:64-95), bit for bit:
+    h2g_generate_points (host C++, glibc cos/sin, the reference's contractions)."""
+    from paper_2208_10907_b200 import generate_points
+    return generate_points("sphere", n, seed)
 
 
 def cpu_reference(n, steps, warmup, threads):
@@ -145,6 +150,21 @@ def cpu_reference(n, steps, warmup, threads):
     return times
 
 
+def full_config_reference_run():
+    """The unmodified reference's one-off run of the whole benched config
+    (tools/ref_pin_c2.py; development container, not this host)."""
+    path = os.path.join(HERE, "tests", "golden", "c2_65536_native.json")
+    try:
+        with open(path) as f:
+            g = json.load(f)
+    except (OSError, ValueError):
+        return None
+    t = g["wall_build_s"] + g["wall_factor_s"] + g["wall_solve_s"]
+    return {"n": g["n"], "value": g["n"] / t, "unit": UNIT, "seconds": t, "cores": g["threads"],
+            "where": "development container (8-core Xeon, 62 GB), -march=native build, peak RSS "
+                     f"{g['peak_rss_gb']:.0f} GB", "source": "tests/golden/c2_65536_native.json"}
+
+
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -155,14 +175,14 @@ def run_reference_arm(args):
     t = sum(times) / len(times)
     value = CPU_SAMPLE_N / t
     sample = (f"reference build+factor+solve of N={CPU_SAMPLE_N} (same sphere/Yukawa/leaf 256/"
-              f"cap 100/tol 1e-6 family; N=65,536 is projected at ~13 h on the CPU)")
+              f"cap 100/tol 1e-6 family); the full N=65,536 config was run once: see full_config_measured")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": dict(WORKLOAD, n=CPU_SAMPLE_N, sample_of="c2_sphere_yukawa"),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": sample},
+                         "sample": sample, "full_config_measured": full_config_reference_run()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -201,16 +221,19 @@ def run_b200_arm(args):
     xyz, q = make_points(n, seed)
     d_xyz = torch.from_numpy(np.ascontiguousarray(xyz)).cuda()
     d_q = torch.from_numpy(np.ascontiguousarray(q)).cuda()
-    b = np.random.default_rng(7 if partitioned else 7 + rank).uniform(-1.0, 1.0, n)
+    # b = SplitMix64(7).next_signed() as in the reference's runs (golden x comparable)
+    b = splitmix_signed(n, 7 if partitioned else 7 + rank)
     d_b = torch.from_numpy(b).cuda()
     d_x = torch.empty_like(d_b)
     stream = torch.cuda.Stream()
+    compat = args.compat
 
-    def new_problem():
+    def new_problem(mode=None, ref_compat=None):
         p = h2.Problem()
         p.set_stream(stream.cuda_stream)
         p.set_kernel("yukawa", WORKLOAD["alpha_m"], WORKLOAD["scale"], WORKLOAD["reg"])
-        p.set_options(tol=WORKLOAD["tol"], cap=WORKLOAD["cap"], eta=WORKLOAD["eta"], qr_mode=qr_mode)
+        p.set_options(tol=WORKLOAD["tol"], cap=WORKLOAD["cap"], eta=WORKLOAD["eta"],
+                      qr_mode=mode or qr_mode, reference_compat=compat if ref_compat is None else ref_compat)
         if comm is not None:
             p.set_comm(comm)
         return p
@@ -236,31 +259,19 @@ def run_b200_arm(args):
         clocks.start()
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
-        kstats = {}
-        launches = 0
-        t_factor = []
-        t_phase = {"build": 0.0, "factor": 0.0, "solve": 0.0}
         # One problem object for the timed steps: every step rebuilds the tree,
         # factors and solves (h2g_build resets the factorization); creating and
-        # destroying the handle is not part of the hot path.
+        # destroying the handle is not part of the hot path. No per-kernel
+        # profiling and no statistics reads inside the timed region.
         p = new_problem()
-        p.set_profile(True)
-        p.reset_profile()
+        launches0 = p.stats()["launches"]
         ev0.record(stream)
         for _ in range(args.steps):
             step(p)
-            sd = p.stats_dev()
-            for k in t_phase:
-                t_phase[k] += sd[k]
-            t_factor.append(sd["factor"])
         ev1.record(stream)
         barrier()
         clk = clocks.stop()
-        for k, v in p.kernel_stats().items():
-            agg = kstats.setdefault(k, dict(ms=0.0, launches=0, flops=0.0, bytes=0.0))
-            for f in agg:
-                agg[f] += v[f]
-        launches = p.stats()["launches"]
+        launches = (p.stats()["launches"] - launches0) // max(1, args.steps)
         p.close()
     elapsed = ev0.elapsed_time(ev1) * 1e-3
     t_max = elapsed
@@ -271,7 +282,7 @@ def run_b200_arm(args):
     points = n if partitioned else n * world
     value = points * args.steps / t_max
 
-    # residual of the last solve through the matrix-free direct sum
+    # residual of the last timed solve through the matrix-free direct sum
     x = d_x.cpu().numpy()
     p = new_problem()
     p.build_dev(d_xyz.data_ptr(), d_q.data_ptr(), n, leaf)
@@ -279,12 +290,27 @@ def run_b200_arm(args):
     resid = float(np.linalg.norm(y - b) / np.linalg.norm(b))
     p.close()
 
+    # Breakdown pass (separate from the timed region): per-kernel-family CUDA
+    # events and per-phase device time of one more step.
+    with torch.cuda.stream(stream):
+        p = new_problem()
+        p.set_profile(True)
+        p.reset_profile()
+        step(p)
+        barrier()
+        sd = p.stats_dev()
+        t_phase = {k: sd[k] for k in ("build", "factor", "solve")}
+        kstats = p.kernel_stats()
+        p.close()
+
     # e2e through the public C-ABI with host buffers (H2D/D2H inside the region).
     # Like the device-timed steps, one handle serves every e2e step (creating it
-    # allocates the arenas once; that is setup, not the hot path).
+    # allocates the arenas once; that is setup, not the hot path). Reported
+    # statistic: the mean over the e2e steps (their total time / steps).
     pe = h2.Problem()
     pe.set_kernel("yukawa", WORKLOAD["alpha_m"], WORKLOAD["scale"], WORKLOAD["reg"])
-    pe.set_options(tol=WORKLOAD["tol"], cap=WORKLOAD["cap"], eta=WORKLOAD["eta"], qr_mode=qr_mode)
+    pe.set_options(tol=WORKLOAD["tol"], cap=WORKLOAD["cap"], eta=WORKLOAD["eta"], qr_mode=qr_mode,
+                   reference_compat=compat)
     if comm is not None:
         pe.set_comm(comm)
     barrier()
@@ -296,31 +322,41 @@ def run_b200_arm(args):
     barrier()
     e2e_t = (time.perf_counter() - t0) / max(args.e2e_steps, 1)
     pe.close()
+    # the host-buffer path must produce the device path's solution
+    e2e_dx = float(np.linalg.norm(xe - x) / np.linalg.norm(x))
+    if not e2e_dx <= 1e-12:
+        raise SystemExit(f"e2e solution differs from the device-timed one: {e2e_dx:.3e}")
     if world > 1:
         tt = torch.tensor([e2e_t], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         e2e_t = float(tt.item())
 
-    # the same step in exact QR mode (bit-exact with the reference), for comparison
+    # the same step with the reference's own assembly and per-step QR rounding
+    # (bit-exact with the unmodified reference; tests/test_bench_parity.py)
     exact = None
-    if qr_mode != "exact" and args.exact_steps > 0:
-        qr_mode_saved, qr_mode = qr_mode, "exact"
+    if args.exact_steps > 0:
         times = []
         with torch.cuda.stream(stream):
             for _ in range(args.exact_steps):
-                p = new_problem()
+                p = new_problem("exact", True)
+                barrier()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
                 step(p)
-                sd = p.stats_dev()
-                times.append(sd["build"] + sd["factor"] + sd["solve"])
+                e1.record(stream)
+                barrier()
+                times.append(e0.elapsed_time(e1) * 1e-3)
                 p.close()
-        qr_mode = qr_mode_saved
         te = max(times)
         if world > 1:
             tt = torch.tensor([te], device="cuda", dtype=torch.float64)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             te = float(tt.item())
-        exact = {"qr_mode": "exact", "points_per_s": points / te, "steps": len(times),
-                 "note": "same workload with the reference's per-step QR rounding (bit-exact); device time"}
+        exact = {"qr_mode": "exact", "reference_compat": True, "points_per_s": points / te,
+                 "steps": len(times),
+                 "note": "same workload, the reference's assembly and QR rounding (bit-exact with "
+                         "the unmodified reference, tests/test_bench_parity.py); device time"}
 
     # dominant kernel family and its roofline
     import json as _json
@@ -356,6 +392,27 @@ def run_b200_arm(args):
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback",
                     "share_of_step": st["ms"] * 1e-3 / max(1e-12, t_phase["build"] + t_phase["factor"] + t_phase["solve"]) if st else None}
 
+    # every kernel family against the roof that bounds it:
+    # FP64 work (DMMA GEMMs, LU, pivoted Cholesky) against the measured FP64
+    # peak, data movement (evaluation writes, copies, QR panel sweeps, solves)
+    # against the measured HBM bandwidth
+    fp64_families = {"gemm", "gram", "lu", "pchol", "trsm"}
+    families = {}
+    for k, v in kstats.items():
+        base = k.split("@")[0]
+        sec = v["ms"] * 1e-3
+        if not sec:
+            continue
+        if base in fp64_families:
+            a = v["flops"] / sec / 1e12
+            families[k] = {"bound": "fp64", "achieved": a, "unit": "TFLOP/s", "peak": FP64_DMMA_TFLOPS,
+                           "frac": a / FP64_DMMA_TFLOPS, "ms": v["ms"], "launches": v["launches"]}
+        else:
+            a = v["bytes"] / sec / 1e9
+            families[k] = {"bound": "hbm", "achieved": a, "unit": "GB/s", "peak": hbm_peak,
+                           "frac": a / hbm_peak, "ms": v["ms"], "launches": v["launches"]}
+    roofline["families"] = families
+
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.skip_cpu:
         try:
@@ -367,6 +424,9 @@ def run_b200_arm(args):
         except Exception as e:  # reference library not built on this host
             cpu_baseline = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                             "sample": f"unavailable: {e}"}
+        full = full_config_reference_run()
+        if full:
+            cpu_baseline["full_config_measured"] = full
 
     if rank == 0:
         line = {
@@ -374,15 +434,18 @@ def run_b200_arm(args):
             "warmup": args.warmup, "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong" if partitioned else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Fibonacci-lattice sphere, seed 42" + ("" if partitioned else "+rank") + ")",
-            "config": dict(WORKLOAD, n=n, qr_mode=qr_mode,
+            "config": dict(WORKLOAD, n=n, qr_mode=qr_mode, reference_compat=compat,
+                           rhs="SplitMix64(7).next_signed()",
                            parallelism=(f"box-partitioned x{world} (NCCL all-gather of bases)" if partitioned
                                         else f"replica x{world}"),
                            l2="inputs larger than L2 (near-field arena and member panels are GBs)"),
-            "phase_s_per_step": {k: v / args.steps for k, v in t_phase.items()},
-            "factor_points_per_s": n / (sum(t_factor) / len(t_factor)),
+            "phase_s_per_step": t_phase,
+            "factor_points_per_s": n / t_phase["factor"],
+            "phase_note": "phase_s_per_step from a separate profiled step after the timed region",
             "solve_rel_residual": resid,
             "e2e": {"value": points / e2e_t, "unit": UNIT, "h2d_bytes_per_step": int(8 * (4 * n + n)),
-                    "d2h_bytes_per_step": int(8 * n)},
+                    "d2h_bytes_per_step": int(8 * n), "statistic": f"mean of {args.e2e_steps} steps",
+                    "x_rel_diff_vs_device_path": e2e_dx},
             "gpu_launches": launches,
             "roofline": roofline,
             "kernels": {k: dict(v, avg_ms=v["ms"] / max(1, v["launches"])) for k, v in kstats.items()},
@@ -412,6 +475,9 @@ def main():
                          "rounding, bit-exact)")
     ap.add_argument("--exact-steps", type=int, default=1,
                     help="extra device-timed steps in exact QR mode, reported beside the headline")
+    ap.add_argument("--compat", action="store_true",
+                    help="the reference's h2/nodep assembly bit for bit, covered-coupling defect "
+                         "included (default: the corrected assembly, reference_compat = 0)")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: one independent problem per rank instead of one partitioned problem")
     args = ap.parse_args()

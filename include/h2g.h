@@ -47,7 +47,14 @@ typedef struct {
                                    2 = compressed (each member of width >= 48 replaced by
                                    a pivoted-Cholesky factor of its Gram matrix, then the
                                    blocked QR; same stopping rule, tolerance parity,
-                                   meant for tol >= 1e-7) */
+                                   meant for tol >= 2.5e-7; below it the blocked
+                                   mode runs) */
+  int32_t reference_compat;     /* 1 = the reference's h2/nodep assembly, bit for bit,
+                                   including its covered-coupling defect (ulv.cpp:424-463,
+                                   :583-603); 0 = corrected assembly (covered T terms, far
+                                   fills at upper levels, neighbour content from every
+                                   overlapping target; oracle/fix_reference.py), accurate
+                                   to the tolerance */
 } h2g_options;
 
 const char* h2g_last_error(void);
@@ -78,16 +85,16 @@ int h2g_levels(h2g_problem* p);
 int h2g_tree_perm(h2g_problem* p, int64_t* original_index);          /* geometry.hpp:40 */
 int h2g_nodes(h2g_problem* p, int64_t* begin_end, double* center_radius); /* heap order */
 int h2g_reordered_points(h2g_problem* p, double* xyz, double* q);
-int64_t h2g_list_count(h2g_problem* p, int level, int far);
+int64_t h2g_list_count(h2g_problem* p, int level, int far); /* -1: bad level */
 int h2g_list(h2g_problem* p, int level, int far, int64_t* ptr, int64_t* idx); /* hstructure.hpp:41-42 */
 int64_t h2g_near_entries(h2g_problem* p);
 int h2g_near_dense(h2g_problem* p, double* out); /* HMatrix::leaf_dense, row-major over blocks */
 int h2g_num_factor_levels(h2g_problem* p);
-int h2g_factor_level(h2g_problem* p, int li, int64_t* ranks); /* returns tree level */
+int h2g_factor_level(h2g_problem* p, int li, int64_t* ranks); /* returns tree level, -1: bad li */
 int64_t h2g_cutoff(h2g_problem* p, int64_t* dims);           /* count | level << 32 */
 int64_t h2g_top_n(h2g_problem* p);
 int h2g_top(h2g_problem* p, double* lu, int64_t* perm);      /* ULVFactors::top */
-int64_t h2g_basis(h2g_problem* p, int level, int64_t k, int side, double* sq); /* dim | rank<<32 */
+int64_t h2g_basis(h2g_problem* p, int level, int64_t k, int side, double* sq); /* dim | rank<<32, -1: bad index */
 double h2g_max_fill_residual(h2g_problem* p);
 
 /* Timings [tree, classify, near, factor, solve] (s); counted flops
@@ -139,6 +146,24 @@ int h2g_set_comm(h2g_problem* p, h2g_comm* c);
 /* Box range [lo, hi) of an m-box level owned by rank (host logic, no GPU). */
 int h2g_partition_range(int64_t m, int nranks, int rank, int64_t* lo, int64_t* hi);
 
+/* ---- seeded point clouds (host code, no device needed) ----
+ * generate_uniform_cube / generate_line / generate_sphere_surface
+ * (geometry.cpp:42-95, SplitMix64 prng.hpp:10-29) bit for bit, plus the two
+ * BASELINE.json geometries the reference lacks. xyz is AoS n x 3, q = 1.
+ * `spheres` is the sphere count (perfect cube) for H2G_GEOM_SPHERE and the
+ * ellipsoid count for H2G_GEOM_ELLIPSOIDS; `spacing` is the sphere lattice
+ * spacing (RunConfig default 3.0). Errors: h2g_points_last_error(). */
+enum {
+  H2G_GEOM_CUBE = 0,
+  H2G_GEOM_LINE = 1,
+  H2G_GEOM_SPHERE = 2,          /* Fibonacci lattice per sphere (the reference's "sphere") */
+  H2G_GEOM_UNIFORM_SPHERE = 3,  /* i.i.d. uniform on the unit sphere */
+  H2G_GEOM_ELLIPSOIDS = 4       /* union of seeded random ellipsoids */
+};
+int h2g_generate_points(int32_t geometry, int64_t n, uint64_t seed, int64_t spheres, double spacing,
+                        double* xyz, double* q);
+const char* h2g_points_last_error(void);
+
 /* ---- single-primitive entry points (kernel parity tests) ---- */
 /* lu_factor (linalg.cpp:352-388) on one n x n column-major block. */
 int h2g_lu_factor(int64_t n, const double* a, double tol, double* lu, int64_t* perm);
@@ -159,6 +184,10 @@ int h2g_lu_solve(int64_t n, const double* lu, const int64_t* perm, int kind, int
 /* gemm (linalg.cpp:86-116): C = alpha op(A) op(B) (+ C when acc). */
 int h2g_gemm(int64_t m, int64_t n, int64_t k, double alpha, const double* a, int transa,
              const double* b, int transb, int acc, double* c);
+/* The device's restatement of glibc's exp (the Yukawa kernel's std::exp,
+ * kernels.cpp:36,58) evaluated on the host: y[i] = exp(x[i]), bitwise equal
+ * to glibc >= 2.28 on x86-64 with FMA for |x| < 512 (host code, no device). */
+int h2g_exp_glibc_host(int64_t n, const double* x, double* y);
 
 #ifdef __cplusplus
 }

@@ -138,7 +138,7 @@ inline std::shared_ptr<Handle> build(const PointCloud& cloud, int64_t leaf, cons
                                      std::optional<int64_t> cap, bool absorb, int qr_mode = 0) {
   auto h = std::make_shared<Handle>();
   h2g_kernel hk{k.kind == KernelKind::laplace ? 0 : k.kind == KernelKind::yukawa ? 1 : 2, k.alpha_m, k.permittivity_scale, k.eta_reg};
-  h2g_options o{tol, cap.value_or(0), 1e-13, absorb ? 1 : 0, 100.0, v == StructureVariant::h2 ? 0 : v == StructureVariant::hss ? 1 : 2, eta, 0, qr_mode};
+  h2g_options o{tol, cap.value_or(0), 1e-13, absorb ? 1 : 0, 100.0, v == StructureVariant::h2 ? 0 : v == StructureVariant::hss ? 1 : 2, eta, 0, qr_mode, 1};
   check(h2g_set_kernel(h->p, &hk));
   check(h2g_set_options(h->p, &o));
   std::vector<double> xyz;

@@ -11,8 +11,12 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_ref", "libh2ref.so")
-_lib = None
+# H2REF_LIB selects another build of the same sources (e.g. oracle/_ref_native,
+# the reference's own -march=native flags; oracle/Makefile ref-native).
+LIB_PATH = os.environ.get("H2REF_LIB") or os.path.join(_HERE, "_ref", "libh2ref.so")
+# The reference with its covered-coupling defect corrected (oracle/fix_reference.py).
+FIXED_PATH = os.path.join(_HERE, "_ref_fixed", "libh2ref.so")
+_libs = {}
 
 i64 = ctypes.c_int64
 f64 = ctypes.c_double
@@ -27,16 +31,20 @@ class RefConfig(ctypes.Structure):
     ]
 
 
-def available():
-    return os.path.exists(LIB_PATH)
+def available(path=None):
+    return os.path.exists(path or LIB_PATH)
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        if not available():
-            raise RuntimeError(f"reference oracle not built: {LIB_PATH} (run make -C oracle ref)")
-        L = ctypes.CDLL(LIB_PATH)
+def fixed_available():
+    return os.path.exists(FIXED_PATH)
+
+
+def lib(path=None):
+    path = path or LIB_PATH
+    if path not in _libs:
+        if not available(path):
+            raise RuntimeError(f"reference oracle not built: {path} (run make -C oracle ref ref-fixed)")
+        L = ctypes.CDLL(path)
         L.ref_last_error.restype = ctypes.c_char_p
         L.ref_new.restype = P
         L.ref_new.argtypes = [i64, P, P]
@@ -77,17 +85,17 @@ def lib():
         L.ref_basis_from_members.argtypes = [i64, i64, P, i64, P, f64, i64, i64, P, P]
         L.ref_gemm.argtypes = [i64, i64, i64, f64, P, ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P]
         L.ref_lu_solve.argtypes = [i64, P, P, ctypes.c_int, i64, i64, P]
-        _lib = L
-    return _lib
+        _libs[path] = L
+    return _libs[path]
 
 
 def _p(a):
     return a.ctypes.data_as(ctypes.c_void_p)
 
 
-def _check(rc):
+def _check(rc, L=None):
     if rc != 0:
-        raise RuntimeError(lib().ref_last_error().decode())
+        raise RuntimeError((L or lib()).ref_last_error().decode())
 
 
 GEOMETRY = {"cube": 0, "line": 1, "sphere": 2}
@@ -115,8 +123,9 @@ def make_config(leaf_size, tol=1e-8, cap=None, kernel="laplace", structure="h2",
 class RefRun:
     """One reference pipeline over a given point cloud (original order)."""
 
-    def __init__(self, xyz, q, cfg):
-        self.L = lib()
+    def __init__(self, xyz, q, cfg, fixed=False):
+        """fixed=True: the corrected build (oracle/_ref_fixed, fix_reference.py)."""
+        self.L = lib(FIXED_PATH if fixed else None)
         self.xyz = np.ascontiguousarray(xyz, dtype=np.float64)
         self.q = np.ascontiguousarray(q, dtype=np.float64)
         self.n = len(self.q)
@@ -129,11 +138,11 @@ class RefRun:
             self.h = None
 
     def build(self):
-        _check(self.L.ref_build(self.h, ctypes.byref(self.cfg)))
+        _check(self.L.ref_build(self.h, ctypes.byref(self.cfg)), self.L)
         return self
 
     def factor(self):
-        _check(self.L.ref_factor(self.h, ctypes.byref(self.cfg)))
+        _check(self.L.ref_factor(self.h, ctypes.byref(self.cfg)), self.L)
         return self
 
     @property
@@ -214,19 +223,19 @@ class RefRun:
         b = np.asfortranarray(b, dtype=np.float64)
         nrhs = 1 if b.ndim == 1 else b.shape[1]
         x = np.zeros_like(b)
-        _check(self.L.ref_solve(self.h, nrhs, _p(b), _p(x)))
+        _check(self.L.ref_solve(self.h, nrhs, _p(b), _p(x)), self.L)
         return x
 
     def dense_matvec(self, x):
         x = np.ascontiguousarray(x, dtype=np.float64)
         y = np.zeros(self.n)
-        _check(self.L.ref_dense_matvec(self.h, _p(x), _p(y)))
+        _check(self.L.ref_dense_matvec(self.h, _p(x), _p(y)), self.L)
         return y
 
     def dense_solve(self, b):
         b = np.ascontiguousarray(b, dtype=np.float64)
         x = np.zeros(self.n)
-        _check(self.L.ref_dense_solve(self.h, _p(b), _p(x)))
+        _check(self.L.ref_dense_solve(self.h, _p(b), _p(x)), self.L)
         return x
 
 

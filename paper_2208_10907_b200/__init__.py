@@ -6,9 +6,9 @@ implemented by the in-tree sm_100a library libh2g.so. There is no CPU
 fallback: importing works anywhere, but every compute call raises if the
 library or a CUDA device is missing.
 """
-from ._lib import (Comm, H2GError, Problem, gloo_allgather, lib, lib_path,  # noqa: F401
-                   nccl_unique_id, partition_range)
+from ._lib import (Comm, H2GError, Problem, generate_points, gloo_allgather, lib,  # noqa: F401
+                   lib_path, nccl_unique_id, partition_range)
 from .pipeline import RunConfig, Pipeline, make_cloud, run_pipeline  # noqa: F401
 
 __all__ = ["H2GError", "Problem", "RunConfig", "Pipeline", "make_cloud", "run_pipeline", "lib",
-           "lib_path", "Comm", "nccl_unique_id", "partition_range", "gloo_allgather"]
+           "lib_path", "Comm", "nccl_unique_id", "partition_range", "gloo_allgather", "generate_points"]

@@ -25,7 +25,8 @@ class Kernel(ctypes.Structure):
 class Options(ctypes.Structure):
     _fields_ = [("tol", f64), ("cap", i64), ("rr_pivot_tol", f64), ("absorb_coupling", ctypes.c_int32),
                 ("abort_residual_factor", f64), ("structure", ctypes.c_int32), ("eta", f64),
-                ("qr_mem_budget", i64), ("qr_mode", ctypes.c_int32)]
+                ("qr_mem_budget", i64), ("qr_mode", ctypes.c_int32),
+                ("reference_compat", ctypes.c_int32)]
 
 
 EXPORTS = [
@@ -38,7 +39,8 @@ EXPORTS = [
     "h2g_basis_from_members", "h2g_basis_from_members_mode", "h2g_lu_solve", "h2g_gemm", "h2g_stats_dev", "h2g_set_profile",
     "h2g_reset_profile", "h2g_kernel_stats", "h2g_set_stream", "h2g_phase_seconds",
     "h2g_nccl_unique_id", "h2g_comm_nccl", "h2g_comm_host", "h2g_comm_destroy", "h2g_set_comm",
-    "h2g_partition_range", "h2g_kernel_evals",
+    "h2g_partition_range", "h2g_kernel_evals", "h2g_generate_points", "h2g_points_last_error",
+    "h2g_exp_glibc_host",
 ]
 
 # h2g_host_allgather_fn (include/h2g.h)
@@ -53,6 +55,9 @@ def lib():
             raise H2GError(f"libh2g.so not built at {lib_path}; run `make -C paper_2208_10907_b200`")
         L = ctypes.CDLL(lib_path)
         L.h2g_last_error.restype = ctypes.c_char_p
+        L.h2g_points_last_error.restype = ctypes.c_char_p
+        L.h2g_exp_glibc_host.argtypes = [i64, P, P]
+        L.h2g_generate_points.argtypes = [ctypes.c_int32, i64, ctypes.c_uint64, i64, f64, P, P]
         L.h2g_create.argtypes = [ctypes.POINTER(P)]
         L.h2g_destroy.argtypes = [P]
         L.h2g_set_kernel.argtypes = [P, ctypes.POINTER(Kernel)]
@@ -216,9 +221,11 @@ class Problem:
         _check(self.L.h2g_set_kernel(self.h, ctypes.byref(k)))
 
     def set_options(self, tol=1e-8, cap=None, rr_pivot_tol=1e-13, absorb_coupling=True,
-                    abort_residual_factor=100.0, structure="h2", eta=1.0, qr_mem_budget=0, qr_mode="exact"):
+                    abort_residual_factor=100.0, structure="h2", eta=1.0, qr_mem_budget=0, qr_mode="exact",
+                    reference_compat=True):
         o = Options(tol, cap or 0, rr_pivot_tol, 1 if absorb_coupling else 0, abort_residual_factor,
-                    {"h2": 0, "hss": 1, "blr2": 2}[structure], eta, qr_mem_budget, {"exact": 0, "blocked": 1, "compressed": 2}[qr_mode])
+                    {"h2": 0, "hss": 1, "blr2": 2}[structure], eta, qr_mem_budget, {"exact": 0, "blocked": 1, "compressed": 2}[qr_mode],
+                    1 if reference_compat else 0)
         _check(self.L.h2g_set_options(self.h, ctypes.byref(o)))
 
     def build(self, xyz, q, leaf):
@@ -276,6 +283,8 @@ class Problem:
 
     def lists(self, lvl, far):
         cnt = self.L.h2g_list_count(self.h, lvl, 1 if far else 0)
+        if cnt < 0:
+            raise RuntimeError(self.L.h2g_last_error().decode())
         ptr = np.zeros((1 << lvl) + 1, dtype=np.int64)
         idx = np.zeros(max(cnt, 1), dtype=np.int64)
         _check(self.L.h2g_list(self.h, lvl, 1 if far else 0, _p(ptr), _p(idx)))
@@ -291,6 +300,8 @@ class Problem:
         for li in range(self.L.h2g_num_factor_levels(self.h)):
             ranks = np.zeros(1 << self.levels, dtype=np.int64)
             lvl = self.L.h2g_factor_level(self.h, li, _p(ranks))
+            if lvl < 0:
+                raise RuntimeError(self.L.h2g_last_error().decode())
             out.append((lvl, ranks[: 1 << lvl].copy()))
         return out
 
@@ -308,6 +319,8 @@ class Problem:
 
     def basis(self, lvl, k, side):
         v = self.L.h2g_basis(self.h, lvl, k, side, None)
+        if v < 0:
+            raise RuntimeError(self.L.h2g_last_error().decode())
         dim, rank = v & 0xFFFFFFFF, v >> 32
         out = np.zeros((dim, dim), order="F")
         if dim:
@@ -403,6 +416,28 @@ def gemm(a, b, alpha=1.0, transa=False, transb=False, c=None):
     out = np.array(c, dtype=np.float64, order="F") if acc else np.zeros((m, n), order="F")
     _check(lib().h2g_gemm(m, n, k, alpha, _p(a), int(transa), _p(b), int(transb), int(acc), _p(out)))
     return out
+
+
+GEOMETRIES = {"cube": 0, "line": 1, "sphere": 2, "uniform_sphere": 3, "ellipsoids": 4}
+
+
+def generate_points(geometry, n, seed, spheres=1, spacing=3.0):
+    """h2g_generate_points: the reference's seeded generators bit for bit
+    (geometry.cpp:42-95) plus uniform_sphere / ellipsoids (host code)."""
+    L = lib()
+    xyz = np.zeros((n, 3))
+    q = np.zeros(n)
+    if L.h2g_generate_points(GEOMETRIES[geometry], n, seed, spheres, spacing, _p(xyz), _p(q)) != 0:
+        raise H2GError(L.h2g_points_last_error().decode())
+    return xyz, q
+
+
+def exp_glibc_host(x):
+    """The device exp restatement (common.cuh exp_glibc_core) run on the host."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.zeros_like(x)
+    lib().h2g_exp_glibc_host(x.size, _p(x), _p(y))
+    return y
 
 
 def basis_from_members(concat, offsets, tol, cap=None, min_rank=0, qr_mode="exact"):

@@ -1,6 +1,7 @@
 // extern "C" boundary (include/h2g.h). Converts C++ exceptions into status
 // codes + h2g_last_error(), copies host buffers in/out, and exposes the
 // factor objects for inspection and parity tests.
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -41,6 +42,18 @@ struct DevBuf {
   ~DevBuf() { cudaFree(p); }
   double* d() { return static_cast<double*>(p); }
 };
+
+// Host <-> device copies ordered on the problem's stream (a non-blocking
+// stream is not ordered against the legacy default stream, and a pageable
+// cudaMemcpy may return before its DMA lands), completed before returning.
+void h2d(h2g::Problem& P, void* dst, const void* src, size_t bytes) {
+  h2g::cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, P.c.stream), "h2d");
+  h2g::cuda_check(cudaStreamSynchronize(P.c.stream), "h2d");
+}
+void d2h(h2g::Problem& P, void* dst, const void* src, size_t bytes) {
+  h2g::cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, P.c.stream), "d2h");
+  h2g::cuda_check(cudaStreamSynchronize(P.c.stream), "d2h");
+}
 
 void require_device() {
   int n = 0;
@@ -94,7 +107,12 @@ int h2g_set_options(h2g_problem* p, const h2g_options* o) {
     op.eta = o->eta;
     if (o->qr_mode < 0 || o->qr_mode > 2)
       throw std::invalid_argument("config: qr_mode must be 0 (exact), 1 (blocked) or 2 (compressed)");
-    op.qr_mode = o->qr_mode;
+    // Compressed mode drops up to eta >= 64 eps of each member's Gram trace
+    // (batch.cu pchol), a relative member residual of sqrt(64 eps) ~ 1.2e-7;
+    // below tol = 2.5e-7 the member rule (tol / 2) cannot be met, so those
+    // tolerances run the blocked QR on the uncompressed panels instead.
+    op.qr_mode = (o->qr_mode == 2 && o->tol < 2.5e-7) ? 1 : o->qr_mode;
+    op.reference_compat = o->reference_compat != 0;
     if (o->qr_mem_budget > 0) {
       op.qr_mem_budget = size_t(o->qr_mem_budget);
       p->P.auto_budget_ = false;
@@ -109,8 +127,8 @@ int h2g_build_dev(h2g_problem* p, int64_t n, const double* d_xyz, const double* 
 int h2g_build(h2g_problem* p, int64_t n, const double* xyz, const double* q, int64_t leaf) {
   return guarded([&] {
     DevBuf a(sizeof(double) * 3 * n), b(sizeof(double) * n);
-    h2g::cuda_check(cudaMemcpy(a.p, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice), "h2d");
-    h2g::cuda_check(cudaMemcpy(b.p, q, sizeof(double) * n, cudaMemcpyHostToDevice), "h2d");
+    h2d(p->P, a.p, xyz, sizeof(double) * 3 * n);
+    h2d(p->P, b.p, q, sizeof(double) * n);
     p->P.build(a.d(), b.d(), n, leaf);
   });
 }
@@ -127,9 +145,9 @@ int h2g_solve(h2g_problem* p, int64_t nrhs, const double* b, double* x) {
   return guarded([&] {
     const size_t bytes = sizeof(double) * size_t(p->P.T.n) * nrhs;
     DevBuf db(bytes), dx(bytes);
-    h2g::cuda_check(cudaMemcpy(db.p, b, bytes, cudaMemcpyHostToDevice), "h2d");
+    h2d(p->P, db.p, b, bytes);
     p->P.solve(db.d(), dx.d(), int(nrhs));
-    h2g::cuda_check(cudaMemcpy(x, dx.p, bytes, cudaMemcpyDeviceToHost), "d2h");
+    d2h(p->P, x, dx.p, bytes);
   });
 }
 
@@ -137,9 +155,9 @@ int h2g_matvec(h2g_problem* p, int64_t nrhs, const double* x, double* y) {
   return guarded([&] {
     const size_t bytes = sizeof(double) * size_t(p->P.T.n) * nrhs;
     DevBuf dx(bytes), dy(bytes);
-    h2g::cuda_check(cudaMemcpy(dx.p, x, bytes, cudaMemcpyHostToDevice), "h2d");
+    h2d(p->P, dx.p, x, bytes);
     p->P.matvec(dx.d(), dy.d(), int(nrhs));
-    h2g::cuda_check(cudaMemcpy(y, dy.p, bytes, cudaMemcpyDeviceToHost), "d2h");
+    d2h(p->P, y, dy.p, bytes);
   });
 }
 
@@ -147,7 +165,7 @@ int h2g_levels(h2g_problem* p) { return p->P.T.levels; }
 
 int h2g_tree_perm(h2g_problem* p, int64_t* out) {
   return guarded([&] {
-    h2g::cuda_check(cudaMemcpy(out, p->P.T.order, sizeof(int64_t) * p->P.T.n, cudaMemcpyDeviceToHost), "d2h");
+    d2h(p->P, out, p->P.T.order, sizeof(int64_t) * p->P.T.n);
   });
 }
 
@@ -155,7 +173,7 @@ int h2g_nodes(h2g_problem* p, int64_t* be, double* geo) {
   return guarded([&] {
     const int64_t nn = (int64_t(1) << (p->P.T.levels + 1)) - 1;
     std::memcpy(be, p->P.be.data(), sizeof(int64_t) * 2 * nn);
-    h2g::cuda_check(cudaMemcpy(geo, p->P.T.geo, sizeof(double) * 4 * nn, cudaMemcpyDeviceToHost), "d2h");
+    d2h(p->P, geo, p->P.T.geo, sizeof(double) * 4 * nn);
   });
 }
 
@@ -163,10 +181,10 @@ int h2g_reordered_points(h2g_problem* p, double* xyz, double* q) {
   return guarded([&] {
     const int64_t n = p->P.T.n;
     std::vector<double> x(n), y(n), z(n);
-    h2g::cuda_check(cudaMemcpy(x.data(), p->P.T.x, 8 * n, cudaMemcpyDeviceToHost), "d2h");
-    h2g::cuda_check(cudaMemcpy(y.data(), p->P.T.y, 8 * n, cudaMemcpyDeviceToHost), "d2h");
-    h2g::cuda_check(cudaMemcpy(z.data(), p->P.T.z, 8 * n, cudaMemcpyDeviceToHost), "d2h");
-    h2g::cuda_check(cudaMemcpy(q, p->P.T.q, 8 * n, cudaMemcpyDeviceToHost), "d2h");
+    d2h(p->P, x.data(), p->P.T.x, 8 * n);
+    d2h(p->P, y.data(), p->P.T.y, 8 * n);
+    d2h(p->P, z.data(), p->P.T.z, 8 * n);
+    d2h(p->P, q, p->P.T.q, 8 * n);
     for (int64_t i = 0; i < n; ++i) {
       xyz[3 * i] = x[i];
       xyz[3 * i + 1] = y[i];
@@ -175,14 +193,26 @@ int h2g_reordered_points(h2g_problem* p, double* xyz, double* q) {
   });
 }
 
+void check_level(h2g_problem* p, int level) {
+  if (level < 0 || size_t(level) >= p->P.S.level.size())
+    throw std::out_of_range("h2g_list: no level " + std::to_string(level));
+}
+
 int64_t h2g_list_count(h2g_problem* p, int level, int far) {
-  const auto& L = p->P.S.level[level];
-  return int64_t(far ? L.far_idx.size() : L.near_idx.size());
+  int64_t out = -1;
+  if (guarded([&] {
+        check_level(p, level);
+        const auto& L = p->P.S.level[size_t(level)];
+        out = int64_t(far ? L.far_idx.size() : L.near_idx.size());
+      }))
+    return -1;
+  return out;
 }
 
 int h2g_list(h2g_problem* p, int level, int far, int64_t* ptr, int64_t* idx) {
   return guarded([&] {
-    const auto& L = p->P.S.level[level];
+    check_level(p, level);
+    const auto& L = p->P.S.level[size_t(level)];
     const auto& pv = far ? L.far_ptr : L.near_ptr;
     const auto& iv = far ? L.far_idx : L.near_idx;
     std::memcpy(ptr, pv.data(), sizeof(int64_t) * pv.size());
@@ -200,7 +230,7 @@ int h2g_near_dense(h2g_problem* p, double* out) {
   return guarded([&] {
     int64_t at = 0;
     for (auto& b : p->P.near) {
-      h2g::cuda_check(cudaMemcpy(out + at, b.m.p, sizeof(double) * b.m.size(), cudaMemcpyDeviceToHost), "d2h");
+      d2h(p->P, out + at, b.m.p, sizeof(double) * b.m.size());
       at += b.m.size();
     }
   });
@@ -209,9 +239,16 @@ int h2g_near_dense(h2g_problem* p, double* out) {
 int h2g_num_factor_levels(h2g_problem* p) { return int(p->P.levels.size()); }
 
 int h2g_factor_level(h2g_problem* p, int li, int64_t* ranks) {
-  const auto& lf = p->P.levels.at(li);
-  for (size_t k = 0; k < lf.ranks.size(); ++k) ranks[k] = lf.ranks[k];
-  return lf.level;
+  int level = -1;
+  if (guarded([&] {
+        if (li < 0 || size_t(li) >= p->P.levels.size())
+          throw std::out_of_range("h2g_factor_level: no factorized level " + std::to_string(li));
+        const auto& lf = p->P.levels[size_t(li)];
+        for (size_t k = 0; k < lf.ranks.size(); ++k) ranks[k] = lf.ranks[k];
+        level = lf.level;
+      }))
+    return -1;
+  return level;
 }
 
 int64_t h2g_cutoff(h2g_problem* p, int64_t* dims) {
@@ -224,16 +261,24 @@ int64_t h2g_top_n(h2g_problem* p) { return p->P.top.n(); }
 int h2g_top(h2g_problem* p, double* lu, int64_t* perm) {
   return guarded([&] {
     const int64_t n = p->P.top.n();
-    h2g::cuda_check(cudaMemcpy(lu, p->P.top.lu.m.p, sizeof(double) * n * n, cudaMemcpyDeviceToHost), "d2h");
-    h2g::cuda_check(cudaMemcpy(perm, p->P.top.perm, sizeof(int64_t) * n, cudaMemcpyDeviceToHost), "d2h");
+    d2h(p->P, lu, p->P.top.lu.m.p, sizeof(double) * n * n);
+    d2h(p->P, perm, p->P.top.perm, sizeof(int64_t) * n);
   });
 }
 
 int64_t h2g_basis(h2g_problem* p, int level, int64_t k, int side, double* sq) {
-  const auto& B = side == 0 ? p->P.U.at(level).at(k) : p->P.V.at(level).at(k);
-  if (sq && B.dim > 0)
-    cudaMemcpy(sq, B.SQ.m.p, sizeof(double) * B.dim * B.dim, cudaMemcpyDeviceToHost);
-  return int64_t(B.dim) | (int64_t(B.rank) << 32);
+  int64_t out = -1;
+  if (guarded([&] {
+        const auto& sets = side == 0 ? p->P.U : p->P.V;
+        if (level < 0 || size_t(level) >= sets.size() || k < 0 || size_t(k) >= sets[size_t(level)].size())
+          throw std::out_of_range("h2g_basis: no basis at level " + std::to_string(level) + " box " +
+                                  std::to_string(k));
+        const auto& B = sets[size_t(level)][size_t(k)];
+        if (sq && B.dim > 0) d2h(p->P, sq, B.SQ.m.p, sizeof(double) * B.dim * B.dim);
+        out = int64_t(B.dim) | (int64_t(B.rank) << 32);
+      }))
+    return -1;
+  return out;
 }
 
 double h2g_max_fill_residual(h2g_problem* p) { return p->P.stats.max_fill_residual; }
@@ -441,6 +486,19 @@ int h2g_basis_from_members_mode(int64_t dim, int64_t width, const double* concat
     }
     *rank = r;
   });
+}
+
+
+// glibc exp restated (common.cuh exp_glibc_core) on the host, for the CPU
+// tests that pin the restatement against libm without a device.
+int h2g_exp_glibc_host(int64_t n, const double* x, double* y) {
+  static const uint64_t tab[2 * 128] = {H2G_EXP_TABLE_INIT};
+  for (int64_t i = 0; i < n; ++i) {
+    bool special = false;
+    const double v = h2g::exp_glibc_core(x[i], tab, &special);
+    y[i] = special ? std::exp(x[i]) : v;
+  }
+  return 0;
 }
 
 }  // extern "C"

@@ -5,6 +5,9 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <map>
+#include <mutex>
+
 #include "batch.hpp"
 
 #include <cstring>
@@ -14,6 +17,18 @@ namespace h2g {
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
     throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+void smem_attr(const void* kernel, size_t bytes, const char* what) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), what);
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{kernel, dev}];
+  if (bytes <= have) return;
+  cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)), what);
+  have = bytes;
 }
 
 Slab Ctx::alloc(size_t bytes) {
@@ -727,21 +742,28 @@ static void compress_members(Ctx& c, std::vector<QrBatch::Item>& items, size_t m
     auto* dj = upload(c, pj, kj);
     auto ev = c.prof_begin();
     launch_pchol(dj, int(pj.size()), max_m, max_k, c.stream);
-    c.prof_end("pchol", ev, 0.0, 0.0);
+    c.prof_end("pchol", ev, 0.0, 0.0);  // flops/bytes filled in once the counts are back
+    const size_t prof_at = c.prec.size();
     c.launches++;
     cuda_check(cudaGetLastError(), "pchol launch");
     std::vector<int> cnt(g1 - g0);
     cuda_check(cudaMemcpyAsync(cnt.data(), dcount, sizeof(int) * cnt.size(), cudaMemcpyDeviceToHost, c.stream),
                "pchol counts");
     c.sync();
-    double fl = 0;
+    double fl = 0, by = 0;
     std::vector<std::pair<int, int>> cs;
     for (size_t g = g0; g < g1; ++g) {
       const int m = items[wide[g].item].m, k = cnt[g - g0];
       fl += double(m) * k * k;  // left-looking updates: m * k^2 / 2 FMAs
+      // lower triangle of G read once, k columns of the factor written
+      by += 8.0 * (0.5 * double(m) * (m + 1) + double(m) * std::max(k, 0));
       cs.push_back({m, std::max(k, 0)});
     }
     c.add_flops(fl);
+    if (prof_at > 0 && prof_at == c.prec.size() && c.prec.back().name == "pchol") {
+      c.prec.back().flops = fl;
+      c.prec.back().bytes = by;
+    }
     std::vector<DMat> cm = alloc_mats(c, cs);
     CopyBatch cb;
     for (size_t g = g0; g < g1; ++g) {

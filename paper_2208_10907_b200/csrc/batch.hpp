@@ -17,6 +17,9 @@
 namespace h2g {
 
 void cuda_check(cudaError_t e, const char* what);
+// Raise a kernel's dynamic shared-memory limit to at least `bytes` on the
+// current device (kept per device and kernel; thread-safe; checked).
+void smem_attr(const void* kernel, size_t bytes, const char* what);
 
 using Slab = std::shared_ptr<void>;
 

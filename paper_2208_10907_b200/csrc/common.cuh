@@ -11,7 +11,10 @@
 // results bitwise equal to the reference for the Laplace kernel.
 #pragma once
 #include <cstdint>
+#include <cstring>
 #include <cuda_runtime.h>
+
+#include "exp_table.cuh"
 
 namespace h2g {
 
@@ -54,9 +57,61 @@ struct Cloud {
   int64_t n = 0;
 };
 
+// The double-precision exp of glibc >= 2.28 (x86-64 FMA variant, the
+// algorithm of ARM optimized-routines' exp: N = 128 table, degree-5
+// polynomial, its published coefficients), restated operation by operation
+// with the contractions of libm's __exp_fma, so the result has the same bits
+// as the std::exp the reference's Yukawa kernel calls (kernels.cpp:36,58).
+// Covered bit for bit: |x| < 512 (the main path and the tiny-|x| path);
+// larger |x| (over/underflow handling) falls back to CUDA exp.
+static __device__ const uint64_t k_exp_tab[2 * 128] = {H2G_EXP_TABLE_INIT};
+
+__host__ __device__ __forceinline__ double exp_glibc_core(double x, const uint64_t* tab, bool* special) {
+  const double inv_ln2_n = 0x1.71547652b82fep+7, shift = 0x1.8p52;
+  const double neg_ln2_hi_n = -0x1.62e42fefa0000p-8, neg_ln2_lo_n = -0x1.cf79abc9e3b3ap-47;
+  const double c2 = 0x1.ffffffffffdbdp-2, c3 = 0x1.555555555543cp-3;
+  const double c4 = 0x1.55555cf172b91p-5, c5 = 0x1.1111167a4d017p-7;
+  uint64_t ix;
+  memcpy(&ix, &x, 8);
+  const int abstop = int((ix >> 52) & 0x7ff);
+  *special = false;
+  if (unsigned(abstop - 0x3c9) > 0x3eu) {
+    if (abstop - 0x3c9 < 0) return x + 1.0;  // |x| < 2^-54
+    *special = true;                         // |x| >= 512, inf, nan
+    return 0.0;
+  }
+  const double z = fma(x, inv_ln2_n, shift);
+  uint64_t ki;
+  memcpy(&ki, &z, 8);
+  const double kd = z - shift;
+  double r = fma(kd, neg_ln2_hi_n, x);
+  r = fma(kd, neg_ln2_lo_n, r);
+  const int idx = int(2 * (ki & 127));
+  const uint64_t top = ki << 45;
+  double tail;
+  memcpy(&tail, &tab[idx], 8);
+  const uint64_t sbits = tab[idx + 1] + top;
+  const double p23 = fma(r, c3, c2);
+  const double t0 = r + tail;
+  const double r2 = r * r;
+  const double p45 = fma(r, c5, c4);
+  const double t1 = fma(p23, r2, t0);
+  const double r4 = r2 * r2;
+  const double tmp = fma(r4, p45, t1);
+  double scale;
+  memcpy(&scale, &sbits, 8);
+  return fma(scale, tmp, scale);
+}
+
+__device__ __forceinline__ double exp_glibc(double x) {
+  bool special;
+  const double v = exp_glibc_core(x, k_exp_tab, &special);
+  return special ? exp(x) : v;
+}
+
 // kernel_eval / assemble_block entry (kernels.cpp:232-268): bitwise equal to
-// the reference for Laplace (r = sqrt(fma(dz,dz,fma(dx,dx,dy*dy))), IEEE
-// sqrt and division). Yukawa uses CUDA exp (<= 1 ulp from glibc).
+// the reference (r = sqrt(fma(dz,dz,fma(dx,dx,dy*dy))), IEEE sqrt and
+// division, glibc's exp for Yukawa).
 template <int KIND>
 __device__ __forceinline__ double kernel_pair_k(const KernelParams& kp, double xi, double yi,
                                                 double zi, double xj, double yj, double zj,
@@ -64,7 +119,7 @@ __device__ __forceinline__ double kernel_pair_k(const KernelParams& kp, double x
   const double dx = xi - xj, dy = yi - yj, dz = zi - zj;
   if (KIND == 2) {
     const double r2 = fma(dz, dz, fma(dx, dx, dy * dy));
-    const double v = exp(-kp.alpha_m * r2) + (r2 == 0.0 ? kp.reg : 0.0);
+    const double v = exp_glibc(-kp.alpha_m * r2) + (r2 == 0.0 ? kp.reg : 0.0);
     return qj * v / kp.scale;
   }
   const double r = sqrt(fma(dz, dz, fma(dx, dx, dy * dy)));
@@ -74,7 +129,7 @@ __device__ __forceinline__ double kernel_pair_k(const KernelParams& kp, double x
     return 0.0;
   }
   if (KIND == 0) return qj / denom;
-  return qj * exp(-kp.alpha_m * r) / denom;
+  return qj * exp_glibc(-kp.alpha_m * r) / denom;
 }
 
 __device__ __forceinline__ double kernel_pair(const KernelParams& kp, double xi, double yi,

@@ -276,6 +276,24 @@ struct Driver {
     return m;
   }
 
+  // Targets of a piece map whose column ranges overlap target tk's range
+  // (tree ranges nest, so each is inside tk's range or contains it): the
+  // column slice [src, src + len) of that piece lands at [dst, dst + len).
+  struct Overlap {
+    TargetKey tk;
+    int src, dst, len;
+  };
+  std::vector<Overlap> overlapping(const PieceMap& pm, const TargetKey& tk) const {
+    std::vector<Overlap> out;
+    const int64_t jb = rb(tk.first, tk.second), je = jb + rs(tk.first, tk.second);
+    for (auto& [tk2, pc] : pm) {
+      const int64_t b2 = rb(tk2.first, tk2.second), e2 = b2 + rs(tk2.first, tk2.second);
+      const int64_t lo = std::max(jb, b2), hi = std::min(je, e2);
+      if (lo < hi) out.push_back({tk2, int(lo - b2), int(lo - jb), int(hi - lo)});
+    }
+    return out;
+  }
+
   // ---- precompute_fillins (compression.cpp:55-109) -------------------------
   FillSet precompute_fillins(SysL& sys) {
     PhaseTimer pt(c, P.stats, "fill_precompute");
@@ -1073,7 +1091,8 @@ struct Driver {
           const int64_t Pp = S.near(lvl, K)[x];
           if (Pp == K) continue;
           for (auto& [tk, piece] : stack[K]) {
-            if (!stack[Pp].count(tk)) continue;
+            if (opt.reference_compat ? !stack[Pp].count(tk) : overlapping(stack[Pp], tk).empty())
+              continue;
             need.push_back({Pp, tk});
           }
         }
@@ -1100,13 +1119,32 @@ struct Driver {
       SolveBatch sb;
       for (size_t t = 0; t < gkeys.size(); ++t) {
         const auto [Pp, tk] = gkeys[t];
-        cb.copy(mats[t].m, stack[Pp].at(tk).m);
-        for (auto& r : gmasks[t]) zb.zero(mats[t].m.sub(0, r.x, mats[t].rows(), r.y - r.x));
+        if (opt.reference_compat) {
+          cb.copy(mats[t].m, stack[Pp].at(tk).m);
+        } else {
+          // P's content over J's columns from every target of P overlapping J
+          // (oracle/fix_reference.py fix 3); the rest are P's near columns.
+          zb.zero(mats[t].m);
+          for (auto& o : overlapping(stack[Pp], tk))
+            cb.copy(mats[t].m.sub(0, o.dst, mats[t].rows(), o.len),
+                    stack[Pp].at(o.tk).m.sub(0, o.src, mats[t].rows(), o.len));
+        }
+        if (opt.reference_compat)
+          for (auto& r : gmasks[t]) zb.zero(mats[t].m.sub(0, r.x, mats[t].rows(), r.y - r.x));
         if (!reassoc) sb.add(sys.diag_lu[Pp], mats[t].m, SOLVE_FULL);
         g[gkeys[t]] = mats[t];
       }
-      cb.run(c);
-      zb.run(c);
+      if (opt.reference_compat) {
+        cb.run(c);
+        zb.run(c);
+      } else {
+        zb.run(c);  // zero-fill first, then the overlapping slices, then the masks
+        cb.run(c);
+        CopyBatch mz;
+        for (size_t t = 0; t < gkeys.size(); ++t)
+          for (auto& r : gmasks[t]) mz.zero(mats[t].m.sub(0, r.x, mats[t].rows(), r.y - r.x));
+        mz.run(c);
+      }
       sb.run(c);
       std::map<std::pair<int64_t, int64_t>, DMat> Wkp;
       if (reassoc) {
@@ -1172,7 +1210,10 @@ struct Driver {
     std::vector<std::pair<int, int>> shapes;
     for (auto& [key, F] : fills) {
       const auto [cc, j] = key;
-      if (cc == j || S.is_far(lvl, cc, j) || S.is_near(lvl, cc, j)) continue;
+      if (cc == j || S.is_near(lvl, cc, j)) continue;
+      // The reference adds only covered fills here; far ones are lost
+      // (oracle/fix_reference.py fix 2).
+      if (opt.reference_compat && S.is_far(lvl, cc, j)) continue;
       fk.push_back(key);
       shapes.push_back({F.rows(), int(rs(lvl, j))});
     }
@@ -1186,7 +1227,7 @@ struct Driver {
       const Mat v0 = Vbig[2 * j], v1 = Vbig[2 * j + 1];
       gemm1(gb, raws[t].m.sub(0, 0, F.rows, v0.rows), F.sub(0, 0, F.rows, v0.cols), v0.t());
       gemm1(gb, raws[t].m.sub(0, v0.rows, F.rows, v1.rows), F.sub(0, v0.cols, F.rows, v1.cols), v1.t());
-      TargetKey tk = covering_target(lvl, cc, j);
+      TargetKey tk = S.is_far(lvl, cc, j) ? TargetKey{lvl, j} : covering_target(lvl, cc, j);
       const int off = int(rb(lvl, j) - rb(tk.first, tk.second));
       const Mat pc = merged[cc].at(tk).m;
       cb.add(pc.sub(0, off, pc.rows, raws[t].cols()), raws[t].m, 1.0);
@@ -1386,7 +1427,10 @@ struct Driver {
     for (auto [k, j] : pairs)
       for (int64_t x = 0; x < S.nnear(lvl, k); ++x) {
         const int64_t p = S.near(lvl, k)[x];
-        if (p == k || p == j || !S.is_far(lvl, p, j)) continue;
+        if (p == k || p == j) continue;
+        // The reference takes only far (p, j); corrected mode every p not
+        // near j (oracle/fix_reference.py fix 1).
+        if (opt.reference_compat ? !S.is_far(lvl, p, j) : S.is_near(lvl, p, j)) continue;
         triples.push_back({k, j, p});
         gneed.insert({p, j});
       }
@@ -1404,7 +1448,11 @@ struct Driver {
         if (is_leaf) {
           eb.add(mats[t].m, rb(lvl, p), rb(lvl, j));
         } else {
-          cols_to_merged(gb, mats[t].m, {carried[2 * p].at({lvl, j}).m, carried[2 * p + 1].at({lvl, j}).m}, j);
+          // far: the (lvl, j) pieces; covered: j's slice of the covering target's
+          const TargetKey tk = S.is_far(lvl, p, j) ? TargetKey{lvl, j} : covering_target(lvl, p, j);
+          const int off = int(rb(lvl, j) - rb(tk.first, tk.second)), w = int(rs(lvl, j));
+          const Mat a0 = carried[2 * p].at(tk).m, a1 = carried[2 * p + 1].at(tk).m;
+          cols_to_merged(gb, mats[t].m, {a0.sub(0, off, a0.rows, w), a1.sub(0, off, a1.rows, w)}, j);
         }
         sb.add(sys.diag_lu[p], mats[t].m, SOLVE_FULL);
         g[keys[t]] = mats[t];

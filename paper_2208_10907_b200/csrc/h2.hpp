@@ -24,6 +24,9 @@ struct Options {  // FactorOptions (ulv.hpp:29-45) + RunConfig bits
   double eta = 1.0;
   size_t qr_mem_budget = size_t(8) << 30;  // auto (free/3) unless set
   int qr_mode = 0;  // 0 exact (k_qr.cu, bit-exact), 1 blocked (k_qrb.cu, tolerance parity)
+  // true: the reference's assembly bit for bit (covered couplings skipped,
+  // ulv.cpp:424-463, :583-603); false: corrected (oracle/fix_reference.py).
+  bool reference_compat = true;
 };
 
 struct Basis {  // SharedBasis (hstructure.hpp:61-69): square [Qr | Qs]

@@ -518,12 +518,8 @@ __global__ void __launch_bounds__(NTW, 1) gemm_ws_kernel(const GemmJob* __restri
 template <int BM>
 void launch_bm(const GemmJob* jobs, const GemmSeg* segs, const GemmTile* tiles, int ntiles,
                KernelParams kp, Cloud cloud, ErrWord* err, int tag, cudaStream_t st) {
-  static bool attr = false;
   const int smem = int(sizeof(Smem<BM>));
-  if (!attr) {
-    cudaFuncSetAttribute(gemm_kernel<BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  smem_attr((const void*)gemm_kernel<BM>, smem, "gemm smem attribute");
   gemm_kernel<BM><<<ntiles, 2 * BM, smem, st>>>(jobs, segs, tiles, kp, cloud, err, tag);
 }
 
@@ -536,13 +532,9 @@ void launch_gemm(const GemmJob* jobs, const GemmSeg* segs, const GemmTile* tiles
   if (ntiles <= 0) return;
   static const bool use_ws = getenv("H2G_GEMM_CLASSIC") == nullptr;
   if (bm == 128 && use_ws) {
-    static bool attr = false;
     const int smem = int(sizeof(ws::Smem));
-    if (!attr) {
-      cudaFuncSetAttribute(ws::gemm_ws_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      cudaFuncSetAttribute(ws::gemm_ws_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      attr = true;
-    }
+    smem_attr((const void*)ws::gemm_ws_kernel<0>, smem, "gemm_ws smem attribute");
+    smem_attr((const void*)ws::gemm_ws_kernel<1>, smem, "gemm_ws smem attribute");
     if (kind == 1)
       ws::gemm_ws_kernel<1><<<ntiles, ws::NTW, smem, st>>>(jobs, segs, tiles, kp, cloud, err, tag);
     else

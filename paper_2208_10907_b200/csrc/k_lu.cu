@@ -554,11 +554,8 @@ void launch_trsm_block(const TrsmBlockJob* jobs, const int2* tiles, int ntiles, 
 void launch_trsm_chunk(const SolveJob* jobs, const int2* tiles, int ntiles, int max_m, cudaStream_t st) {
   if (ntiles <= 0) return;
   const size_t smem = sizeof(double) * size_t(TRSM_NC) * size_t(max_m | 1);
-  static size_t attr = 0;
-  if (smem > attr) {  // static shared memory (blk) counts against the 48 KB default too
-    cudaFuncSetAttribute(trsm_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = smem;
-  }
+  // static shared memory (blk) counts against the 48 KB default too
+  smem_attr((const void*)trsm_chunk_kernel, smem, "trsm_chunk smem attribute");
   trsm_chunk_kernel<<<ntiles, 256, smem, st>>>(jobs, tiles);  // errors surface at the caller's check
 }
 
@@ -575,11 +572,7 @@ void launch_lu_amax(const LuJob& job, double* out, cudaStream_t st) {
 void launch_lu_panel(const LuJob& job, int kb, int nb, const double* amax, ErrWord* err, int tag,
                      cudaStream_t st) {
   const size_t smem = sizeof(double) * size_t(job.A.rows);
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(lu_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = smem;
-  }
+  smem_attr((const void*)lu_panel_kernel, smem, "lu_panel smem attribute");
   lu_panel_kernel<<<1, 1024, smem, st>>>(job, kb, nb, amax, err, tag);
 }
 
@@ -590,7 +583,7 @@ void launch_lu_rows(const LuJob& job, int kb, int nb, cudaStream_t st) {
 
 void launch_lu(const LuJob* jobs, int njobs, int max_n, ErrWord* err, int tag, cudaStream_t st) {
   const size_t smem = sizeof(double) * size_t(max_n > 0 ? max_n : 1);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  smem_attr((const void*)lu_kernel, smem, "lu smem attribute");
   if (njobs > 0) lu_kernel<<<njobs, NT, smem, st>>>(jobs, err, tag);
 }
 
@@ -604,11 +597,7 @@ void launch_solve(const SolveJob* jobs, const SolveChunk* chunks, int nchunks,
                   size_t smem_doubles, cudaStream_t st) {
   if (nchunks <= 0) return;
   const size_t smem = sizeof(double) * (smem_doubles > 0 ? smem_doubles : 1);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  smem_attr((const void*)solve_kernel, 227 * 1024, "solve smem attribute");
   solve_kernel<<<nchunks, 256, smem, st>>>(jobs, chunks);
 }
 

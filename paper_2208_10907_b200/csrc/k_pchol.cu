@@ -127,11 +127,7 @@ __global__ void __launch_bounds__(NT) pchol_kernel(const PcholJob* __restrict__ 
 void launch_pchol(const PcholJob* jobs, int njobs, int max_m, int max_k, cudaStream_t st) {
   if (njobs <= 0) return;
   const size_t smem = sizeof(double) * size_t(max_m + max_k);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaFuncSetAttribute(pchol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    attr = smem;
-  }
+  smem_attr((const void*)pchol_kernel, smem, "pchol smem attribute");
   pchol_kernel<<<njobs, NT, smem, st>>>(jobs);
 }
 

@@ -875,13 +875,7 @@ size_t qr_scratch_doubles(int m, int n, int nmem) {
 }
 
 static void qr_attr() {
-  static bool attr = false;
-  if (!attr) {
-    cuda_check(cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    220 * 1024),
-               "qr smem attribute");
-    attr = true;
-  }
+  smem_attr((const void*)qr_kernel, 220 * 1024, "qr smem attribute");
 }
 
 static cudaLaunchConfig_t qr_config(int njobs, int cluster, size_t smem, cudaStream_t st,

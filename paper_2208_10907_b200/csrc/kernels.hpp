@@ -7,6 +7,9 @@
 
 namespace h2g {
 
+void cuda_check(cudaError_t e, const char* what);                   // batch.cu
+void smem_attr(const void* kernel, size_t bytes, const char* what);  // batch.cu
+
 // ---- batched GEMM (k_gemm.cu) ---------------------------------------------
 // C = [acc ? C : 0] + sum_s A_s * (alpha_s * B_s), each C element accumulated
 // with fma over the segments in order and over k in order: the reference's

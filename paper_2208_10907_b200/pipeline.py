@@ -13,61 +13,46 @@ from typing import Optional
 
 import numpy as np
 
-from ._lib import Problem
+from ._lib import Problem, generate_points
 
-_GOLDEN = 0x9E3779B97F4A7C15
-_M64 = 0xFFFFFFFFFFFFFFFF
-
-
-def _splitmix_stream(seed, count):
-    """The first `count` SplitMix64 doubles of a stream (prng.hpp:14-25), vectorised."""
-    k = np.arange(1, count + 1, dtype=np.uint64)
+def splitmix_signed(n, seed):
+    """b_i = SplitMix64(seed).next_signed() = 2 u - 1 (prng.hpp:14-25): the
+    right-hand side of the reference's runs (seed 7)."""
+    k = np.arange(1, n + 1, dtype=np.uint64)
     with np.errstate(over="ignore"):
-        z = np.uint64(seed) + k * np.uint64(_GOLDEN)
+        z = np.uint64(seed) + k * np.uint64(0x9E3779B97F4A7C15)
         z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
         z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
         z = z ^ (z >> np.uint64(31))
-    return (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+    u = (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+    return 2.0 * u - 1.0
 
 
 def generate_uniform_cube(n, seed):
     """geometry.cpp:42-52: point i = draws 3i..3i+2; unit charges."""
-    if n < 2:
-        raise ValueError("generate_uniform_cube: n must be >= 2")
-    return _splitmix_stream(seed, 3 * n).reshape(n, 3), np.ones(n)
+    return generate_points("cube", n, seed)
 
 
 def generate_line(n, seed):
-    if n < 2:
-        raise ValueError("generate_line: n must be >= 2")
-    xyz = np.zeros((n, 3))
-    xyz[:, 0] = _splitmix_stream(seed, n)
-    return xyz, np.ones(n)
+    """geometry.cpp:54-62."""
+    return generate_points("line", n, seed)
+
+
+def generate_sphere_surface(n, spheres, spacing, seed):
+    """geometry.cpp:64-95 (Fibonacci lattices), bit for bit with the reference."""
+    return generate_points("sphere", n, seed, spheres, spacing)
 
 
 def generate_uniform_sphere(n, seed):
-    """i.i.d. uniform points on the unit sphere (BASELINE config 2): z = 2u-1,
-    phi = 2 pi u'. No reference counterpart (fed to it as a point cloud)."""
-    u = _splitmix_stream(seed, 2 * n).reshape(n, 2)
-    z = 2.0 * u[:, 0] - 1.0
-    phi = 2.0 * math.pi * u[:, 1]
-    r = np.sqrt(np.maximum(0.0, 1.0 - z * z))
-    return np.stack([r * np.cos(phi), r * np.sin(phi), z], axis=1), np.ones(n)
+    """i.i.d. uniform points on the unit sphere (BASELINE configs[1] as worded):
+    z = 2u - 1, phi = 2 pi u'. No reference counterpart."""
+    return generate_points("uniform_sphere", n, seed)
 
 
 def generate_ellipsoids(n, count, seed):
     """Surface points on `count` seeded random ellipsoids, semi-axes U(0.05, 0.2),
-    centres U[0,1]^3 (BASELINE config 5 surrogate). No reference counterpart."""
-    u = _splitmix_stream(seed, 6 * count + 2 * n)
-    cen = u[: 3 * count].reshape(count, 3)
-    ax = 0.05 + 0.15 * u[3 * count: 6 * count].reshape(count, 3)
-    v = u[6 * count:].reshape(n, 2)
-    which = np.arange(n) % count
-    z = 2.0 * v[:, 0] - 1.0
-    phi = 2.0 * math.pi * v[:, 1]
-    r = np.sqrt(np.maximum(0.0, 1.0 - z * z))
-    unit = np.stack([r * np.cos(phi), r * np.sin(phi), z], axis=1)
-    return cen[which] + ax[which] * unit, np.ones(n)
+    centres U[0,1]^3 (BASELINE configs[4] surrogate). No reference counterpart."""
+    return generate_points("ellipsoids", n, seed, count)
 
 
 @dataclass
@@ -113,34 +98,6 @@ class RunConfig:
             raise ValueError("config: unknown structure " + self.structure)
 
 
-def _fib_spheres(n, spheres, spacing, seed):
-    """generate_sphere_surface (geometry.cpp:64-95) via libm-equivalent numpy."""
-    side = int(round(spheres ** (1.0 / 3.0)))
-    if side < 1 or side ** 3 != spheres:
-        raise ValueError("generate_sphere_surface: spheres must be a perfect cube count")
-    origin = -0.5 * spacing * (side - 1)
-    golden = (1.0 + math.sqrt(5.0)) / 2.0
-    phases = _splitmix_stream(seed, spheres)
-    out = []
-    remaining = n
-    idx = 0
-    for ix in range(side):
-        for iy in range(side):
-            for iz in range(side):
-                left = spheres - idx
-                m = (remaining + left - 1) // left
-                remaining -= m
-                c = (origin + spacing * ix, origin + spacing * iy, origin + spacing * iz)
-                phase = phases[idx] * 2.0 * math.pi
-                t = np.arange(m, dtype=np.float64)
-                z = 1.0 - 2.0 * (t + 0.5) / m
-                r = np.sqrt(np.maximum(0.0, 1.0 - z * z))
-                phi = 2.0 * math.pi * (t / golden) + phase
-                out.append(np.stack([c[0] + r * np.cos(phi), c[1] + r * np.sin(phi), c[2] + z], 1))
-                idx += 1
-    return np.concatenate(out), np.ones(n)
-
-
 def make_cloud(cfg):
     """report.cpp:60-65 (+ the BASELINE geometries)."""
     if cfg.points is not None:
@@ -154,7 +111,7 @@ def make_cloud(cfg):
         return generate_uniform_sphere(cfg.n, cfg.seed)
     if cfg.geometry == "ellipsoids":
         return generate_ellipsoids(cfg.n, cfg.spheres, cfg.seed)
-    return _fib_spheres(cfg.n, cfg.spheres, cfg.spacing, cfg.seed)
+    return generate_sphere_surface(cfg.n, cfg.spheres, cfg.spacing, cfg.seed)
 
 
 def domain_diameter(xyz):

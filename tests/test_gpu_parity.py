@@ -90,6 +90,25 @@ def test_solve_residual_matches_reference(golden, name):
     p.close()
 
 
+YUKAWA = [n for n in E2E if "yukawa" in n]
+
+
+@pytest.mark.parametrize("name", YUKAWA)
+def test_yukawa_bitwise_vs_reference(golden, name):
+    """Yukawa entries go through the glibc exp restatement (common.cuh
+    exp_glibc): ranks, cutoff and x equal the unmodified reference's bits."""
+    rec = golden[0]["cases"][name]
+    xyz, q = cpu.generate(rec["geometry"], rec["n"], 42, rec["spheres"])
+    p = make_problem(rec, xyz, q)
+    assert fbits(p.leaf_dense()) == rec["near_fnv"]
+    p.factor()
+    x = p.solve(ref.splitmix_signed(rec["n"], 7))
+    assert {str(l): rk.tolist() for l, rk in p.factor_levels()} == rec["ranks"]
+    assert p.cutoff()[1].tolist() == rec["cutoff"][1]
+    assert fbits(x) == rec["x_fnv"]
+    p.close()
+
+
 def test_hss_is_exact():
     """Weak admissibility has no covered pairs: the solve is tolerance-exact."""
     xyz, q = cpu.generate("cube", 1024, 42)
