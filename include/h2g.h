@@ -96,6 +96,23 @@ int64_t h2g_top_n(h2g_problem* p);
 int h2g_top(h2g_problem* p, double* lu, int64_t* perm);      /* ULVFactors::top */
 int64_t h2g_basis(h2g_problem* p, int level, int64_t k, int side, double* sq); /* dim | rank<<32, -1: bad index */
 double h2g_max_fill_residual(h2g_problem* p);
+/* LevelFactors of factorized level li (ulv.hpp:60-68): returns the box count m
+ * (-1 on error) and fills dims/ranks (m each, may be NULL) and use_z. */
+int h2g_level_dims(h2g_problem* p, int li, int64_t* dims, int64_t* ranks, int32_t* use_z);
+/* DenseSystem::block(i, j) of level li (compression.hpp:33): rows/cols out;
+ * out (column-major rows x cols) may be NULL to query the shape. */
+int h2g_level_block(h2g_problem* p, int li, int64_t i, int64_t j, int64_t* rows, int64_t* cols,
+                    double* out);
+/* Packed LU factors of level li, box k (linalg.hpp:73-92): which = 0 the
+ * cached diagonal LU of the DenseSystem (DenseSystem::diag_lu), 1 the pivot
+ * LU of S^RR (ClusterFactors::pivot). n out; lu (n x n) / perm (n) may be NULL. */
+int h2g_level_lu(h2g_problem* p, int li, int which, int64_t k, int64_t* n, double* lu, int64_t* perm);
+/* ClusterFactors::urs (which 0, rdim x sdim) / lsr (which 1, sdim x rdim). */
+int h2g_level_elim(h2g_problem* p, int li, int64_t k, int which, int64_t* rows, int64_t* cols, double* out);
+/* assemble_block (kernels.hpp:38-39) of a host cloud (AoS xyz, charges q),
+ * evaluated on the device: out = K(rows [r0, r1), cols [c0, c1)), column-major. */
+int h2g_assemble_block(const h2g_kernel* k, int64_t n, const double* xyz, const double* q, int64_t r0,
+                       int64_t r1, int64_t c0, int64_t c1, double* out);
 
 /* Timings [tree, classify, near, factor, solve] (s); counted flops
  * [fill_precompute, basis, skeleton, factorize, assemble, solve] following the

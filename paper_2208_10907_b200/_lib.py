@@ -40,7 +40,8 @@ EXPORTS = [
     "h2g_reset_profile", "h2g_kernel_stats", "h2g_set_stream", "h2g_phase_seconds",
     "h2g_nccl_unique_id", "h2g_comm_nccl", "h2g_comm_host", "h2g_comm_destroy", "h2g_set_comm",
     "h2g_partition_range", "h2g_kernel_evals", "h2g_generate_points", "h2g_points_last_error",
-    "h2g_exp_glibc_host",
+    "h2g_exp_glibc_host", "h2g_level_dims", "h2g_level_block", "h2g_level_lu", "h2g_level_elim",
+    "h2g_assemble_block",
 ]
 
 # h2g_host_allgather_fn (include/h2g.h)

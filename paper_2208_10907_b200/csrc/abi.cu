@@ -1,6 +1,7 @@
 // extern "C" boundary (include/h2g.h). Converts C++ exceptions into status
 // codes + h2g_last_error(), copies host buffers in/out, and exposes the
 // factor objects for inspection and parity tests.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -488,6 +489,136 @@ int h2g_basis_from_members_mode(int64_t dim, int64_t width, const double* concat
   });
 }
 
+
+// ---- ULVFactors views (the façade's LevelFactors / DenseSystem / ClusterFactors) ----
+namespace {
+const h2g::LevelF& level_of(h2g_problem* p, int li) {
+  if (!p->P.factored) throw std::logic_error("h2g: factor first");
+  if (li < 0 || size_t(li) >= p->P.levels.size())
+    throw std::out_of_range("h2g: no factorized level " + std::to_string(li));
+  return p->P.levels[size_t(li)];
+}
+void copy_mat(h2g_problem* p, const h2g::Mat& m, int64_t* rows, int64_t* cols, double* out) {
+  *rows = m.rows;
+  *cols = m.cols;
+  if (!out || m.rows == 0 || m.cols == 0) return;
+  // strided device view -> column-major host copy
+  if (m.rs == 1 && m.cs == m.rows) {
+    d2h(p->P, out, m.p, sizeof(double) * size_t(m.rows) * m.cols);
+    return;
+  }
+  if (m.rs == 1) {
+    h2g::cuda_check(cudaMemcpy2DAsync(out, sizeof(double) * m.rows, m.p, sizeof(double) * m.cs,
+                                      sizeof(double) * m.rows, m.cols, cudaMemcpyDeviceToHost, p->P.c.stream),
+                    "d2h");
+    h2g::cuda_check(cudaStreamSynchronize(p->P.c.stream), "d2h");
+    return;
+  }
+  throw std::logic_error("h2g: unexpected row-strided factor view");
+}
+}  // namespace
+
+int h2g_level_dims(h2g_problem* p, int li, int64_t* dims, int64_t* ranks, int32_t* use_z) {
+  int64_t m = -1;
+  if (guarded([&] {
+        const auto& lf = level_of(p, li);
+        m = int64_t(lf.dims.size());
+        for (size_t k = 0; k < lf.dims.size(); ++k) {
+          if (dims) dims[k] = lf.dims[k];
+          if (ranks) ranks[k] = lf.ranks[k];
+        }
+        if (use_z) *use_z = lf.use_z ? 1 : 0;
+      }))
+    return -1;
+  return int(m);
+}
+
+int h2g_level_block(h2g_problem* p, int li, int64_t i, int64_t j, int64_t* rows, int64_t* cols,
+                    double* out) {
+  return guarded([&] {
+    const auto& lf = level_of(p, li);
+    const auto& S = p->P.S;
+    const int l = lf.level;
+    if (i < 0 || i >= (int64_t(1) << l)) throw std::out_of_range("DenseSystem::block: no dense block");
+    const int64_t* b = S.near(l, i);
+    const int64_t n = S.nnear(l, i);
+    const int64_t* it = std::lower_bound(b, b + n, j);
+    if (it == b + n || *it != j) throw std::out_of_range("DenseSystem::block: no dense block");
+    const size_t t = size_t(S.level[l].near_ptr[i] + (it - b));
+    if (t >= lf.sys.blocks.size()) throw std::out_of_range("DenseSystem::block: no dense block");
+    copy_mat(p, lf.sys.blocks[t].m, rows, cols, out);
+  });
+}
+
+int h2g_level_lu(h2g_problem* p, int li, int which, int64_t k, int64_t* n, double* lu, int64_t* perm) {
+  return guarded([&] {
+    const auto& lf = level_of(p, li);
+    if (k < 0 || size_t(k) >= lf.dims.size()) throw std::out_of_range("h2g_level_lu: no box " + std::to_string(k));
+    const h2g::LuF* f = nullptr;
+    if (which == 0) {
+      if (lf.sys.diag_lu.empty()) throw std::out_of_range("h2g_level_lu: level has no cached diagonal LUs");
+      f = &lf.sys.diag_lu[size_t(k)];
+    } else {
+      f = &lf.elim[size_t(k)].piv;
+    }
+    const int64_t nn = f->n();
+    *n = nn;
+    if (nn == 0 || !lu) return;
+    d2h(p->P, lu, f->lu.m.p, sizeof(double) * size_t(nn) * nn);
+    d2h(p->P, perm, f->perm, sizeof(int64_t) * size_t(nn));
+  });
+}
+
+int h2g_level_elim(h2g_problem* p, int li, int64_t k, int which, int64_t* rows, int64_t* cols, double* out) {
+  return guarded([&] {
+    const auto& lf = level_of(p, li);
+    if (k < 0 || size_t(k) >= lf.elim.size()) throw std::out_of_range("h2g_level_elim: no box " + std::to_string(k));
+    const auto& e = lf.elim[size_t(k)];
+    const h2g::DMat& m = which == 0 ? e.urs : e.lsr;
+    if (!m.m.p) {
+      *rows = which == 0 ? e.rdim : e.sdim;
+      *cols = which == 0 ? e.sdim : e.rdim;
+      if (out && *rows * *cols > 0) throw std::logic_error("h2g_level_elim: factor not stored");
+      return;
+    }
+    copy_mat(p, m.m, rows, cols, out);
+  });
+}
+
+// assemble_block (kernels.cpp:242-268) of a host cloud on the device:
+// out (rows x cols, column-major) = kernel(x_{r0+i}, x_{c0+j}, q_{c0+j}).
+int h2g_assemble_block(const h2g_kernel* k, int64_t n, const double* xyz, const double* q, int64_t r0,
+                       int64_t r1, int64_t c0, int64_t c1, double* out) {
+  return guarded([&] {
+    require_device();
+    if (r1 <= r0 || c1 <= c0) throw std::invalid_argument("assemble_block: empty range");
+    if (r0 < 0 || c0 < 0 || r1 > n || c1 > n) throw std::out_of_range("assemble_block: range outside cloud");
+    h2g::Problem P;
+    h2g::KernelParams kp;
+    kp.kind = k->kind;
+    kp.alpha_m = k->alpha_m;
+    kp.scale = k->permittivity_scale;
+    kp.reg = k->eta_reg;
+    P.c.kp = kp;
+    std::vector<double> soa(size_t(4 * n));
+    for (int64_t i = 0; i < n; ++i) {
+      soa[size_t(i)] = xyz[3 * i];
+      soa[size_t(n + i)] = xyz[3 * i + 1];
+      soa[size_t(2 * n + i)] = xyz[3 * i + 2];
+      soa[size_t(3 * n + i)] = q[i];
+    }
+    DevBuf pts(sizeof(double) * soa.size());
+    h2d(P, pts.p, soa.data(), sizeof(double) * soa.size());
+    const double* d = pts.d();
+    P.c.cloud = h2g::Cloud{d, d + n, d + 2 * n, d + 3 * n, n};
+    auto B = h2g::alloc_mat(P.c, int(r1 - r0), int(c1 - c0));
+    h2g::EvalBatch eb;
+    eb.add(B.m, r0, c0);
+    eb.run(P.c);
+    P.c.sync();  // reports a singular evaluation with the reference's message
+    d2h(P, out, B.m.p, sizeof(double) * size_t(r1 - r0) * size_t(c1 - c0));
+  });
+}
 
 // glibc exp restated (common.cuh exp_glibc_core) on the host, for the CPU
 // tests that pin the restatement against libm without a device.

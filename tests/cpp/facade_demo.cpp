@@ -1,4 +1,4 @@
-// Drives the B200 path through the C++ façade (include/h2ulv_b200.hpp) the
+// Drives the B200 path through the drop-in header tree (include/h2ulv/) the
 // way a caller of the reference's Pipeline would (report.hpp:73-99), and
 // prints what tests/test_facade.py checks against the reference's golden
 // fixtures: tree permutation and solution bit hashes, the ranks, the
@@ -7,9 +7,10 @@
 #include <cstring>
 #include <stdexcept>
 
-#include "h2ulv_b200.hpp"
+#include "h2ulv/prng.hpp"
+#include "h2ulv/report.hpp"
 
-using namespace h2ulv_b200;
+using namespace h2ulv;
 
 static uint64_t fnv(const void* p, size_t n64) {
   uint64_t h = 0xcbf29ce484222325ULL;
@@ -47,30 +48,45 @@ int main(int argc, char** argv) {
     Matrix b(n, 1);
     SplitMix64 rng(7);
     for (int64_t i = 0; i < n; ++i) b(i, 0) = rng.next_signed();
-    Matrix x = solve(pipe, b);
+    Matrix x = solve(pipe.factors(), b);  // solve(const ULVFactors&, const Matrix&)
     Matrix y = pipe.matvec(x);
     double rn = 0, bn = 0;
     for (int64_t i = 0; i < n; ++i) {
       rn += (y(i, 0) - b(i, 0)) * (y(i, 0) - b(i, 0));
       bn += b(i, 0) * b(i, 0);
     }
-    ClusterTreeResult t = pipe.tree();
+    // The free-function path: build_cluster_tree -> classify_blocks ->
+    // materialize_dense -> build_and_factorize -> solve (hstructure.hpp,
+    // ulv.hpp, solve.hpp), against the Pipeline's tree, lists and x.
+    const HMatrix& H = pipe.hmatrix();
     ClusterTreeResult t2 = build_cluster_tree(pipe.original_cloud(), leaf);
-    BlockStructure s = pipe.structure();
-    BlockStructure s2 = classify_blocks(pipe.original_cloud(), leaf, AdmissibilityRule{});
-    bool same_lists = s.levels == s2.levels;
-    for (int l = 1; l <= s.levels && same_lists; ++l)
-      same_lists = s.level[size_t(l)].near_cols == s2.level[size_t(l)].near_cols &&
-                   s.level[size_t(l)].far_cols == s2.level[size_t(l)].far_cols;
+    BlockStructure s2 = classify_blocks(t2.tree, AdmissibilityRule{}, StructureVariant::h2);
+    bool same_lists = H.structure.levels == s2.levels;
+    for (int l = 1; l <= s2.levels && same_lists; ++l)
+      same_lists = H.structure.level[size_t(l)].near_cols == s2.level[size_t(l)].near_cols &&
+                   H.structure.level[size_t(l)].far_cols == s2.level[size_t(l)].far_cols;
+    HMatrix H2 = materialize_dense(s2, t2.tree, t2.cloud, pipe.kernel(), StructureVariant::h2);
+    FactorOptions fo;
+    fo.tol = cfg.tol;
+    ULVFactors f2 = build_and_factorize(H2, fo);
+    Matrix x2 = solve(f2, b);
+    bool same_near = H2.leaf_dense.size() == H.leaf_dense.size();
+    for (size_t i = 0; i < H.leaf_dense.size() && same_near; ++i)
+      for (size_t c = 0; c < H.leaf_dense[i].size() && same_near; ++c)
+        same_near = fnv(H.leaf_dense[i][c].data(), size_t(H.leaf_dense[i][c].size())) ==
+                    fnv(H2.leaf_dense[i][c].data(), size_t(H2.leaf_dense[i][c].size()));
     int64_t rank_sum = 0;
-    for (auto& [lvl, r] : pipe.ranks())
-      for (int64_t v : r) rank_sum += v;
+    for (const auto& lf : pipe.factors().levels)
+      for (int64_t v : lf.ranks) rank_sum += v;
+    const ClusterTree& t = H.tree;
     printf("{\"n\": %lld, \"levels\": %d, \"perm_fnv\": %llu, \"x_fnv\": %llu, \"residual\": %.17g, "
-           "\"same_tree\": %s, \"same_lists\": %s, \"rank_sum\": %lld}\n",
-           (long long)n, t.tree.levels, (unsigned long long)fnv(t.tree.original_index.data(), size_t(n)),
+           "\"same_tree\": %s, \"same_lists\": %s, \"same_near\": %s, \"same_x_free_api\": %s, "
+           "\"rank_sum\": %lld}\n",
+           (long long)n, t.levels, (unsigned long long)fnv(t.original_index.data(), size_t(n)),
            (unsigned long long)fnv(x.data(), size_t(n)), std::sqrt(rn / bn),
-           t.tree.original_index == t2.tree.original_index ? "true" : "false", same_lists ? "true" : "false",
-           (long long)rank_sum);
+           t.original_index == t2.tree.original_index ? "true" : "false", same_lists ? "true" : "false",
+           same_near ? "true" : "false",
+           fnv(x.data(), size_t(n)) == fnv(x2.data(), size_t(n)) ? "true" : "false", (long long)rank_sum);
   } catch (const std::runtime_error& e) {
     printf("{\"runtime_error\": \"%s\"}\n", e.what());
     return 2;

@@ -1,6 +1,7 @@
-"""C++ façade (include/h2ulv_b200.hpp): the reference's Pipeline / build_cluster_tree /
-classify_blocks / solve API over the C ABI, exercised by tests/cpp/facade_demo.cpp
-(built by `make -C paper_2208_10907_b200`)."""
+"""C++ façade (the drop-in header tree include/h2ulv/): the reference's Pipeline /
+build_cluster_tree / classify_blocks / materialize_dense / build_and_factorize /
+solve API over the C ABI, exercised by tests/cpp/facade_demo.cpp (built by
+`make -C paper_2208_10907_b200`)."""
 import json
 import os
 import subprocess
@@ -47,6 +48,6 @@ def test_facade_pipeline_matches_reference(golden):
     assert out["levels"] == rec["levels"]
     assert out["perm_fnv"] == rec["perm_fnv"]
     assert out["x_fnv"] == rec["x_fnv"]
-    assert out["same_tree"] and out["same_lists"]
+    assert out["same_tree"] and out["same_lists"] and out["same_near"] and out["same_x_free_api"]
     assert out["rank_sum"] == sum(sum(v) for v in rec["ranks"].values())
     assert abs(out["residual"] - rec["residual"]) <= 1e-12 * rec["residual"]

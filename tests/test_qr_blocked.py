@@ -69,9 +69,8 @@ def test_blocked_matches_exact_on_bench_family():
     """The bench workload family (Fibonacci sphere, Yukawa, leaf 256, cap 100,
     tol 1e-6) at N = 16,384: blocked and exact QR give the same solve
     residual to 1e-6 relative and the same per-level rank sums."""
-    from paper_2208_10907_b200.pipeline import _fib_spheres
     n = 16384
-    xyz, q = _fib_spheres(n, 1, 3.0, 42)
+    xyz, q = h2.generate_points("sphere", n, 42)
     b = np.random.default_rng(7).uniform(-1, 1, n)
     out = {}
     for mode in ("exact", "blocked"):
@@ -122,9 +121,8 @@ def test_compressed_is_deterministic(golden):
 def test_compressed_matches_exact_on_bench_family():
     """Bench workload family at N = 16,384: compressed and exact QR give the
     same solve residual to 1e-4 relative and per-level rank sums within 10 %."""
-    from paper_2208_10907_b200.pipeline import _fib_spheres
     n = 16384
-    xyz, q = _fib_spheres(n, 1, 3.0, 42)
+    xyz, q = h2.generate_points("sphere", n, 42)
     b = np.random.default_rng(7).uniform(-1, 1, n)
     out = {}
     for mode in ("exact", "compressed"):
