@@ -58,6 +58,8 @@ def lib():
         L.h2g_last_error.restype = ctypes.c_char_p
         L.h2g_points_last_error.restype = ctypes.c_char_p
         L.h2g_exp_glibc_host.argtypes = [i64, P, P]
+        L.h2g_level_dims.argtypes = [P, ctypes.c_int, P, P, P]
+        L.h2g_level_block.argtypes = [P, ctypes.c_int, i64, i64, P, P, P]
         L.h2g_generate_points.argtypes = [ctypes.c_int32, i64, ctypes.c_uint64, i64, f64, P, P]
         L.h2g_create.argtypes = [ctypes.POINTER(P)]
         L.h2g_destroy.argtypes = [P]
@@ -327,6 +329,25 @@ class Problem:
         if dim:
             self.L.h2g_basis(self.h, lvl, k, side, _p(out))
         return out, rank
+
+    def level_block(self, li, i, j):
+        """DenseSystem::block(i, j) of factorized level li (h2g_level_block)."""
+        r, c = ctypes.c_int64(), ctypes.c_int64()
+        _check(self.L.h2g_level_block(self.h, li, i, j, ctypes.byref(r), ctypes.byref(c), None))
+        out = np.zeros((r.value, c.value), order="F")
+        if out.size:
+            _check(self.L.h2g_level_block(self.h, li, i, j, ctypes.byref(r), ctypes.byref(c), _p(out)))
+        return out
+
+    def level_dims(self, li):
+        m = self.L.h2g_level_dims(self.h, li, None, None, None)
+        if m < 0:
+            raise H2GError(self.L.h2g_last_error().decode())
+        dims = np.zeros(m, dtype=np.int64)
+        ranks = np.zeros(m, dtype=np.int64)
+        z = ctypes.c_int32()
+        self.L.h2g_level_dims(self.h, li, _p(dims), _p(ranks), ctypes.byref(z))
+        return dims, ranks, bool(z.value)
 
     def set_stream(self, stream_ptr):
         _check(self.L.h2g_set_stream(self.h, stream_ptr))
