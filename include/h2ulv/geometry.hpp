@@ -161,7 +161,10 @@ struct Handle {
 
 // Device settings a handle is built with (KernelSpec / structure / options).
 struct Setup {
-  h2g_kernel kernel{0, 0.0, 4.0 * 3.14159265358979323846, 0.0};
+  // A tree-only build (build_cluster_tree / classify_blocks) still evaluates
+  // the near field on the device; a unit regularisation keeps r = 0 regular
+  // there (those blocks are discarded).
+  h2g_kernel kernel{0, 0.0, 4.0 * 3.14159265358979323846, 1.0};
   h2g_options options{1e-8, 0, 1e-13, 1, 100.0, 0, 1.0, 0, 0, 1};
 };
 

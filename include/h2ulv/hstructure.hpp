@@ -162,6 +162,8 @@ struct Device {
   Setup setup;
   PointCloud original;
   int64_t leaf = 0;
+  bool factored = false;
+  h2g_options factored_with{};
 };
 }  // namespace b200
 

@@ -94,10 +94,11 @@ inline std::string jnum(double v) {
   return s;
 }
 inline std::string jstr(const std::string& s) { return "\"" + s + "\""; }
-// Sorted-key object writer with nlohmann's 2-space layout.
+// Insertion-ordered object writer with nlohmann::ordered_json's 2-space
+// layout (report.cpp:13 uses ordered_json).
 struct JObj {
-  std::map<std::string, std::string> kv;  // value already serialised (may span lines)
-  void put(const std::string& k, const std::string& v) { kv[k] = v; }
+  std::vector<std::pair<std::string, std::string>> kv;  // values already serialised
+  void put(const std::string& k, const std::string& v) { kv.emplace_back(k, v); }
   std::string dump(int indent) const {
     if (kv.empty()) return "{}";
     std::string pad(size_t(indent + 2), ' '), out = "{\n";
@@ -244,8 +245,7 @@ class Pipeline {
     build();
     if (factored_) return;
     const auto t0 = std::chrono::steady_clock::now();
-    b200::apply_options(*dev_, factor_options());
-    b200::check(h2g_factor(dev_->handle->p));
+    b200::factor_once(*dev_, factor_options());
     factored_ = true;
     factor_seconds_ = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }

@@ -229,29 +229,66 @@ inline FactorVariant variant_of(StructureVariant v) {
 }
 }  // namespace b200
 
-// prepare_factor_inputs (ulv.cpp:1108-1126). The device factorization does the
-// leaf fills and bases as its first stage, so preparing applies the options to
-// the HMatrix's device problem; factorize runs everything.
+namespace b200 {
+inline bool same_options(const h2g_options& a, const h2g_options& b) {
+  return a.tol == b.tol && a.cap == b.cap && a.rr_pivot_tol == b.rr_pivot_tol &&
+         a.absorb_coupling == b.absorb_coupling && a.abort_residual_factor == b.abort_residual_factor &&
+         a.structure == b.structure && a.eta == b.eta && a.qr_mode == b.qr_mode &&
+         a.reference_compat == b.reference_compat;
+}
+// One device factorization per option set: the leaf fills, the fill-augmented
+// leaf bases and the level-parallel elimination run as one h2g_factor call.
+inline void factor_once(Device& d, const FactorOptions& o) {
+  apply_options(d, o);
+  if (d.factored && same_options(d.factored_with, d.setup.options)) return;
+  check(h2g_factor(d.handle->p));
+  d.factored = true;
+  d.factored_with = d.setup.options;
+}
+}  // namespace b200
+
+// prepare_factor_inputs (ulv.cpp:1108-1126): the leaf DenseSystem with its
+// cached diagonal LUs and the fill-augmented leaf bases. On the device these
+// are the first stage of h2g_factor, so preparing runs the factorization and
+// returns its leaf stage (the fills stay on the device: leaf_fills is empty).
 inline FactorInputs prepare_factor_inputs(const HMatrix& H, const FactorOptions& opts) {
   if (!H.b200) throw std::invalid_argument("prepare_factor_inputs: HMatrix not from materialize_dense");
   if (opts.variant == FactorVariant::h2dep)
     throw std::invalid_argument("prepare_factor_inputs: h2dep is not on the B200 path (sequential driver)");
-  b200::apply_options(*H.b200, opts);
+  b200::factor_once(*H.b200, opts);
+  h2g_problem* p = H.b200->handle->p;
   FactorInputs in;
   in.b200 = H.b200;
+  const int L = H.tree.levels;
+  const int64_t m = int64_t(1) << L;
+  in.bases.init(L);
+  for (int64_t k = 0; k < m; ++k) {
+    in.bases.U[size_t(L)][size_t(k)] = b200::read_basis(p, L, k, 0);
+    in.bases.V[size_t(L)][size_t(k)] = b200::read_basis(p, L, k, 1);
+  }
+  in.leaf_sys.near_cols = H.structure.level[size_t(L)].near_cols;
+  for (int64_t k = 0; k < m; ++k) in.leaf_sys.dims.push_back(H.cluster_range(L, k).size());
+  for (int64_t i = 0; i < m; ++i)
+    for (int64_t j : in.leaf_sys.near_cols[size_t(i)]) in.leaf_sys.put_view(i, j, &H.leaf_block(i, j));
+  if (in.leaf_sys.has_offdiag() && H.variant != StructureVariant::blr2)
+    for (int64_t k = 0; k < m; ++k) in.leaf_sys.diag_lu.push_back(b200::read_lu(p, 0, 0, k));
   return in;
 }
 
-// factorize (ulv.cpp:1128-1143): h2g_factor, then the host snapshot.
+// factorize (ulv.cpp:1128-1143): h2g_factor (once per option set), then the
+// host snapshot of the factors.
 inline ULVFactors factorize(const HMatrix& H, FactorInputs inputs, const FactorOptions& opts) {
-  if (!inputs.b200) inputs = prepare_factor_inputs(H, opts);
-  b200::apply_options(*inputs.b200, opts);
-  b200::check(h2g_factor(inputs.b200->handle->p));
+  if (!inputs.b200) inputs.b200 = H.b200;
+  if (!inputs.b200) throw std::invalid_argument("factorize: HMatrix not from materialize_dense");
+  b200::factor_once(*inputs.b200, opts);
   return b200::snapshot(H, inputs.b200, opts.variant == FactorVariant::h2nodep ? b200::variant_of(H.variant) : opts.variant);
 }
 
 inline ULVFactors build_and_factorize(const HMatrix& H, const FactorOptions& opts) {
-  return factorize(H, prepare_factor_inputs(H, opts), opts);
+  if (!H.b200) throw std::invalid_argument("build_and_factorize: HMatrix not from materialize_dense");
+  FactorInputs in;
+  in.b200 = H.b200;
+  return factorize(H, std::move(in), opts);
 }
 
 }  // namespace h2ulv

@@ -60,6 +60,7 @@ def lib():
         L.h2g_exp_glibc_host.argtypes = [i64, P, P]
         L.h2g_level_dims.argtypes = [P, ctypes.c_int, P, P, P]
         L.h2g_level_block.argtypes = [P, ctypes.c_int, i64, i64, P, P, P]
+        L.h2g_assemble_block.argtypes = [ctypes.POINTER(Kernel), i64, P, P, i64, i64, i64, i64, P]
         L.h2g_generate_points.argtypes = [ctypes.c_int32, i64, ctypes.c_uint64, i64, f64, P, P]
         L.h2g_create.argtypes = [ctypes.POINTER(P)]
         L.h2g_destroy.argtypes = [P]
@@ -452,6 +453,18 @@ def generate_points(geometry, n, seed, spheres=1, spacing=3.0):
     if L.h2g_generate_points(GEOMETRIES[geometry], n, seed, spheres, spacing, _p(xyz), _p(q)) != 0:
         raise H2GError(L.h2g_points_last_error().decode())
     return xyz, q
+
+
+def assemble_block(kind, alpha_m, scale, reg, xyz, q, rows, cols):
+    """assemble_block (kernels.cpp:242-268) of a host cloud, evaluated on the
+    device (h2g_assemble_block): rows/cols are (begin, end) index ranges."""
+    xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    k = Kernel({"laplace": 0, "yukawa": 1, "gaussian": 2}[kind], alpha_m, scale, reg)
+    out = np.zeros((rows[1] - rows[0], cols[1] - cols[0]), order="F")
+    _check(lib().h2g_assemble_block(ctypes.byref(k), len(q), _p(xyz), _p(q), rows[0], rows[1], cols[0],
+                                    cols[1], _p(out)))
+    return out
 
 
 def exp_glibc_host(x):

@@ -9,10 +9,11 @@
   ``write_vector`` / ``read_vector`` (solve.cpp:249-268): the same ``%.17g``
   ASCII formats and error messages, so files move between the two.
 
-``solve_rel_error``: the reference compares x with the dense LU solution of
-A x = A 1 (N <= oracle_guard); the dense LU is the O(N^3) oracle this path
-replaces, so x is compared with the exact solution 1 directly (the two
-definitions differ by the dense LU's own error, ~1e-15 relative).
+``solve_rel_error`` is the reference's (report.cpp:170-178): b = A 1 by the
+dense matvec (h2g_matvec, bitwise equal to matvec_dense_oracle), x_ref the
+dense LU solution of A x = b (lu_factor(A, 1e-15) + solve, dense_solve_oracle,
+solve.cpp:241-247, run on the device with the bit-exact LU primitives), and
+rel_error(x, x_ref) (linalg.cpp:618-630), for N <= oracle_guard.
 """
 import json
 
@@ -101,9 +102,10 @@ def report_of(pipe):
     pipe.factor()
     p = pipe.prob
     st = p.stats()
+    # the reference's phase keys (flops.cpp phase_name), in its std::map order
     flops = {"assemble": st["flops_assemble"], "fill_precompute": st["flops_fills"],
              "basis": st["flops_basis"], "skeleton": st["flops_skeleton"],
-             "factorize": st["flops_factorize"], "solve": st["flops_solve"], "oracle": 0}
+             "factorize": st["flops_factorize"], "solve": st["flops_solve"], "oracle": 0, "other": 0}
     walls = {k: 0.0 for k in flops}
     walls.update(p.phase_seconds())
     walls["assemble"] = st["t_tree"] + st["t_classify"] + st["t_near"]
@@ -155,10 +157,25 @@ def report_of(pipe):
         "solve_rel_error": -1.0,
     }
     if cfg.oracle and cfg.n <= cfg.oracle_guard:
-        ones = np.ones(cfg.n)
-        x = pipe.solve_rhs(p.matvec(ones))
-        rep["solve_rel_error"] = float(np.linalg.norm(x - ones) / np.linalg.norm(ones))
+        rep["solve_rel_error"] = dense_oracle_error(pipe)
     return rep
+
+
+def dense_oracle_error(pipe):
+    """rel_error(x, x_ref) of Pipeline::report's oracle check (report.cpp:170-178)."""
+    from . import _lib
+    p = pipe.prob
+    n = pipe.cfg.n
+    b = p.matvec(np.ones(n))
+    k = pipe.kernel
+    A = _lib.assemble_block(k["kind"], k["alpha_m"], k["scale"], k["reg"], pipe.xyz, pipe.q, (0, n), (0, n))
+    lu, perm = _lib.lu_factor(A, 1e-15)
+    x_ref = _lib.lu_solve(lu, perm, b.reshape(n, 1), "solve")[:, 0]
+    x = pipe.solve_rhs(b)
+    den = float(np.sum(x_ref * x_ref))
+    if den == 0.0:
+        raise ValueError("rel_error: reference is zero")
+    return float(np.sqrt(np.sum((x - x_ref) ** 2) / den))
 
 
 def sweep(cfg, axis, values):

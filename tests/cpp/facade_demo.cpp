@@ -25,6 +25,16 @@ static uint64_t fnv(const void* p, size_t n64) {
 int main(int argc, char** argv) {
   const int64_t n = argc > 1 ? atoll(argv[1]) : 4096;
   const int64_t leaf = argc > 2 ? atoll(argv[2]) : 128;
+  if (argc > 3 && std::strcmp(argv[3], "report") == 0) {  // RunReport::to_json of run_pipeline
+    RunConfig cfg;
+    cfg.n = n;
+    cfg.leaf_size = leaf;
+    cfg.scale = 1.0;
+    cfg.reg = 1e-3;
+    cfg.tol = 1e-8;
+    printf("%s\n", run_pipeline(cfg).to_json().c_str());
+    return 0;
+  }
   // Configuration errors are the reference's invalid_argument (report.cpp:43-58).
   try {
     RunConfig bad;

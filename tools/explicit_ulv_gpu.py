@@ -44,10 +44,11 @@ def main():
     Xt = torch.tensor(X, device=dev)
     Qt = torch.tensor(Q, device=dev)
     M = torch.empty((n, n), dtype=torch.float64, device=dev)
-    for i0 in range(0, n, 4096):
-        d = torch.cdist(Xt[i0:i0 + 4096], Xt)
+    for i0 in range(0, n, 2048):
+        # exact differences (torch.cdist's matmul form loses digits for close points)
+        d = torch.sqrt(((Xt[i0:i0 + 2048, None, :] - Xt[None, :, :]) ** 2).sum(-1))
         K = (torch.exp(-d) if kern == "yukawa" else torch.ones_like(d)) / (d + 1e-3)
-        M[i0:i0 + 4096] = K * Qt[None, :]
+        M[i0:i0 + 2048] = K * Qt[None, :]
         del d, K
     flv = p.factor_levels()
     print(f"N={n} leaf={leaf} tol={tol} cap={cap} compat={compat} mode={mode} L={L} "

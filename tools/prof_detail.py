@@ -5,21 +5,23 @@ import sys
 import numpy as np
 sys.path.insert(0, '.')
 import paper_2208_10907_b200 as h2
-from paper_2208_10907_b200.pipeline import _fib_spheres
+import os
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
 warm = "--warm" in sys.argv  # one untimed factorization first (grown memory pool, as in bench.py)
-xyz, q = _fib_spheres(n, 1, 3.0, 42)
+xyz, q = h2.generate_points("sphere", n, 42)
+MODE = os.environ.get("QR_MODE", "compressed")
+COMPAT = os.environ.get("COMPAT", "0") == "1"
 if warm:
     w = h2.Problem()
     w.set_kernel("yukawa", 1.0, 1.0, 1e-3)
-    w.set_options(tol=1e-6, cap=100)
+    w.set_options(tol=1e-6, cap=100, qr_mode=MODE, reference_compat=COMPAT)
     w.build(xyz, q, 256)
     w.factor()
     w.close()
 p = h2.Problem()
 p.set_kernel("yukawa", 1.0, 1.0, 1e-3)
-p.set_options(tol=1e-6, cap=100)
+p.set_options(tol=1e-6, cap=100, qr_mode=MODE, reference_compat=COMPAT)
 p.set_profile(True)
 p.build(xyz, q, 256)
 p.factor()
