@@ -892,6 +892,142 @@ struct Driver {
     return d;
   }
 
+  // Leaf pieces with the kernel block generated inside the GEMM (every
+  // A(p, J) is re-evaluated for each box c having p as a near neighbour and
+  // J as a target; H2G_LEAF_GEN=1).
+  void leaf_pieces_generated(SysL& sys, const std::vector<std::pair<int64_t, TargetKey>>& pkeys,
+                             const std::vector<DMat>& mats, const std::map<int64_t, DMat>& usT,
+                             const std::map<std::pair<int64_t, int64_t>, DMat>& qcm, int64_t lo, int64_t hi) {
+    const auto& Ub = P.U[L];
+    GemmBatch gb;
+    for (size_t t = 0; t < pkeys.size(); ++t) {
+      const auto [cc, tk] = pkeys[t];
+      if (cc < lo || cc >= hi) continue;
+      const int64_t jb = rb(tk.first, tk.second), je = jb + rs(tk.first, tk.second);
+      const int w = int(je - jb);
+      gb.job(mats[t].m, false);
+      gb.seg_gen(Ub[cc].rank > 0 ? usT.at(cc).m : Ub[cc].Qs().t(), rb(L, cc), jb, w, false, 1.0);
+      if (Ub[cc].rank > 0 && sys.offdiag)
+        for (int64_t x = 0; x < S.nnear(L, cc); ++x) {
+          const int64_t p = S.near(L, cc)[x];
+          if (p == cc) continue;
+          bool all_zero;
+          auto mask = mask_for(L, p, jb, je, all_zero);
+          if (all_zero) continue;
+          gb.seg_gen(qcm.at({cc, p}).m, rb(L, p), jb, w, false, -1.0, mask);
+        }
+    }
+    gb.run(c);
+  }
+
+  // Leaf pieces from materialized kernel blocks (the default): per target J
+  // the rows every piece toward J needs -- A(c, J) of each box c with target
+  // J, and A(p, J) with p's near columns zeroed for each of their near
+  // neighbours p -- are evaluated ONCE into one column-major block and shared
+  // by all the pieces' GEMM segments (the generated path evaluates A(p, J)
+  // once per (c, p, J), ~26 times at the bench size). Targets are processed
+  // in chunks under a memory budget. Same values (one kernel_pair per entry,
+  // masked entries +0), same segments in the same order: bit-identical pieces.
+  void leaf_pieces_materialized(SysL& sys, const std::vector<std::pair<int64_t, TargetKey>>& pkeys,
+                                const std::vector<DMat>& mats, const std::map<int64_t, DMat>& usT,
+                                const std::map<std::pair<int64_t, int64_t>, DMat>& qcm, int64_t lo,
+                                int64_t hi) {
+    const auto& Ub = P.U[L];
+    struct Plan {
+      TargetKey tk;
+      int64_t jb = 0;
+      int w = 0, rows = 0;
+      std::map<std::pair<int64_t, int>, int> off;  // (box, masked) -> row offset
+      std::vector<std::pair<int64_t, int>> order;  // row blocks in layout order
+      std::vector<size_t> jobs;                     // indices into pkeys
+    };
+    std::map<TargetKey, size_t> at;
+    std::vector<Plan> plans;
+    auto add_rows = [&](Plan& pl, int64_t box, int masked) {
+      if (pl.off.count({box, masked})) return;
+      pl.off[{box, masked}] = pl.rows;
+      pl.order.push_back({box, masked});
+      pl.rows += int(rs(L, box));
+    };
+    for (size_t t = 0; t < pkeys.size(); ++t) {
+      const auto [cc, tk] = pkeys[t];
+      if (cc < lo || cc >= hi) continue;
+      auto it = at.find(tk);
+      if (it == at.end()) {
+        it = at.emplace(tk, plans.size()).first;
+        plans.emplace_back();
+        plans.back().tk = tk;
+        plans.back().jb = rb(tk.first, tk.second);
+        plans.back().w = int(rs(tk.first, tk.second));
+      }
+      Plan& pl = plans[it->second];
+      pl.jobs.push_back(t);
+      add_rows(pl, cc, 0);
+      if (Ub[cc].rank > 0 && sys.offdiag)
+        for (int64_t x = 0; x < S.nnear(L, cc); ++x) {
+          const int64_t p = S.near(L, cc)[x];
+          if (p == cc) continue;
+          bool all_zero;
+          mask_for(L, p, pl.jb, pl.jb + pl.w, all_zero);
+          if (!all_zero) add_rows(pl, p, 1);
+        }
+    }
+    size_t fr = 0, tot = 0;
+    cuda_check(cudaMemGetInfo(&fr, &tot), "meminfo");
+    const size_t budget = std::max<size_t>(size_t(1) << 28, fr / 3);
+    size_t p0 = 0;
+    while (p0 < plans.size()) {
+      size_t p1 = p0, bytes = 0;
+      while (p1 < plans.size()) {
+        const size_t need = sizeof(double) * size_t(plans[p1].rows) * size_t(plans[p1].w);
+        if (p1 > p0 && bytes + need > budget) break;
+        bytes += need;
+        ++p1;
+      }
+      std::vector<std::pair<int, int>> bshapes;
+      for (size_t q = p0; q < p1; ++q) bshapes.push_back({plans[q].rows, plans[q].w});
+      auto B = alloc_mats(c, bshapes);
+      EvalBatch eb;
+      CopyBatch zb;
+      for (size_t q = p0; q < p1; ++q) {
+        const Plan& pl = plans[q];
+        const Mat Bm = B[q - p0].m;
+        for (auto [box, masked] : pl.order) {
+          const int r0 = pl.off.at({box, masked}), nr = int(rs(L, box));
+          eb.add(Bm.sub(r0, 0, nr, pl.w), rb(L, box), pl.jb);
+          if (masked) {
+            bool all_zero;
+            for (auto& r : mask_for(L, box, pl.jb, pl.jb + pl.w, all_zero))
+              zb.zero(Bm.sub(r0, r.x, nr, r.y - r.x));
+          }
+        }
+      }
+      eb.run(c);
+      zb.run(c);
+      GemmBatch gb;
+      for (size_t q = p0; q < p1; ++q) {
+        const Plan& pl = plans[q];
+        const Mat Bm = B[q - p0].m;
+        auto rows_of = [&](int64_t box, int masked) {
+          return Bm.sub(pl.off.at({box, masked}), 0, int(rs(L, box)), pl.w);
+        };
+        for (size_t t : pl.jobs) {
+          const int64_t cc = pkeys[t].first;
+          gb.job(mats[t].m, false);
+          gb.seg(Ub[cc].rank > 0 ? usT.at(cc).m : Ub[cc].Qs().t(), rows_of(cc, 0), 1.0);
+          if (Ub[cc].rank > 0 && sys.offdiag)
+            for (int64_t x = 0; x < S.nnear(L, cc); ++x) {
+              const int64_t p = S.near(L, cc)[x];
+              if (p == cc || !pl.off.count({p, 1})) continue;
+              gb.seg(qcm.at({cc, p}).m, rows_of(p, 1), -1.0);
+            }
+        }
+      }
+      gb.run(c);
+      p0 = p1;  // B is freed (stream-ordered) when it goes out of scope
+    }
+  }
+
   // ---- build_leaf_pieces (ulv.cpp:336-401) -----------------------------------
   void build_leaf_pieces(SysL& sys, const FillSet& fills, std::vector<PieceMap>& pieces,
                          double* level_max) {
@@ -940,7 +1076,7 @@ struct Driver {
       for (auto& [key, m] : qT) qcm[key] = colmajor_copy(cb, m.m.t());
       cb.run(c);
     }
-    // Pieces: Us_c^T A(c, J) - sum_p q_cp A(p, J)[masked], B generated in-kernel.
+    // Pieces: Us_c^T A(c, J) - sum_p q_cp A(p, J)[masked].
     std::vector<std::pair<int64_t, TargetKey>> pkeys;
     std::vector<std::pair<int, int>> shapes;
     for (int64_t cc = 0; cc < m; ++cc)
@@ -949,28 +1085,14 @@ struct Driver {
         shapes.push_back({Ub[cc].rank, int(rs(tk.first, tk.second))});
       }
     auto mats = alloc_mats(c, shapes);
-    GemmBatch gb;
-    for (size_t t = 0; t < pkeys.size(); ++t) {
-      const auto [cc, tk] = pkeys[t];
-      pieces[cc][tk] = mats[t];
-      if (cc < lo || cc >= hi) continue;
-      const int64_t jb = rb(tk.first, tk.second), je = jb + rs(tk.first, tk.second);
-      const int w = int(je - jb);
-      gb.job(mats[t].m, false);
-      gb.seg_gen(Ub[cc].rank > 0 ? usT.at(cc).m : Ub[cc].Qs().t(), rb(L, cc), jb, w, false, 1.0);
-      if (Ub[cc].rank > 0 && sys.offdiag)
-        for (int64_t x = 0; x < S.nnear(L, cc); ++x) {
-          const int64_t p = S.near(L, cc)[x];
-          if (p == cc) continue;
-          bool all_zero;
-          auto mask = mask_for(L, p, jb, je, all_zero);
-          if (all_zero) continue;
-          gb.seg_gen(qcm.at({cc, p}).m, rb(L, p), jb, w, false, -1.0, mask);
-        }
-    }
+    for (size_t t = 0; t < pkeys.size(); ++t) pieces[pkeys[t].first][pkeys[t].second] = mats[t];
     {
       PhaseTimer pt2(c, P.stats, "skeleton_leaf_pieces");
-      gb.run(c);
+      static const bool generated = getenv("H2G_LEAF_GEN") != nullptr;
+      if (generated)
+        leaf_pieces_generated(sys, pkeys, mats, usT, qcm, lo, hi);
+      else
+        leaf_pieces_materialized(sys, pkeys, mats, usT, qcm, lo, hi);
     }
     {
       std::vector<int64_t> box(pkeys.size());
