@@ -107,7 +107,10 @@ def report_of(pipe):
              "basis": st["flops_basis"], "skeleton": st["flops_skeleton"],
              "factorize": st["flops_factorize"], "solve": st["flops_solve"], "oracle": 0, "other": 0}
     walls = {k: 0.0 for k in flops}
-    walls.update(p.phase_seconds())
+    for k, v in p.phase_seconds().items():
+        # driver sub-phases ("skeleton_leaf_pieces") fold into their reference phase
+        base = next((ph for ph in flops if k == ph or k.startswith(ph + "_")), "other")
+        walls[base] += v
     walls["assemble"] = st["t_tree"] + st["t_classify"] + st["t_near"]
     levels_n = p.levels
     flev = {lvl: ranks for lvl, ranks in p.factor_levels()}
