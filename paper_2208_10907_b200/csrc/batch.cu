@@ -265,14 +265,44 @@ void GemmBatch::run(Ctx& c, int tag) {
       }
       nseg += j.nseg;
     }
+    int rmin = 1 << 30, rmax = 0, cmin = 1 << 30, cmax = 0, kmin = 1 << 30, kmax = 0, acc = 0, acm = 0, bcm = 0;
+    for (auto& j : jobs) {
+      rmin = std::min(rmin, j.C.rows); rmax = std::max(rmax, j.C.rows);
+      cmin = std::min(cmin, j.C.cols); cmax = std::max(cmax, j.C.cols);
+      acc += j.acc ? 1 : 0;
+      int kt = 0;
+      for (int q = 0; q < j.nseg; ++q) {
+        kt += segs[j.seg0 + q].A.cols;
+        acm += segs[j.seg0 + q].A.rs == 1;
+        bcm += segs[j.seg0 + q].B.rs == 1;
+      }
+      kmin = std::min(kmin, kt); kmax = std::max(kmax, kt);
+    }
+    fprintf(stderr, "GEMMRANGE rows %d-%d cols %d-%d Ktot %d-%d acc %d Acolmajor %d Bcolmajor %d of %.0f segs\n", rmin, rmax,
+            cmin, cmax, kmin, kmax, acc, acm, bcm, nseg);
     const double nj = double(jobs.size());
     fprintf(stderr, "GEMMSHAPE %s@%s jobs %zu tiles %zu bm %d rows %.0f cols %.0f segs %.1f K/seg %.0f gen %.0f%% GF %.2f\n",
             name ? name : "gemm", c.phase.c_str(), jobs.size(), tiles.size(), bm, sr / nj, sc / nj, nseg / nj,
             sk / std::max(1.0, nseg), 100.0 * ngen / std::max(1.0, nseg), fl * 1e-9);
   }
+  cudaEvent_t sh0 = nullptr, sh1 = nullptr;
+  if (shapes) {  // per-launch time of the census (serialises the stream: profiling only)
+    cudaEventCreate(&sh0);
+    cudaEventCreate(&sh1);
+    cudaEventRecord(sh0, c.stream);
+  }
   auto ev = c.prof_begin();
   launch_gemm(dj, ds, dt, int(tiles.size()), bm, c.kp, c.cloud, c.err, tag, c.stream,
               name && std::string(name) == "gram" ? 1 : 0);
+  if (shapes) {
+    cudaEventRecord(sh1, c.stream);
+    cudaEventSynchronize(sh1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, sh0, sh1);
+    fprintf(stderr, "GEMMTIME %.3f ms %.2f TF/s\n", ms, ms > 0 ? fl / (ms * 1e-3) * 1e-12 : 0.0);
+    cudaEventDestroy(sh0);
+    cudaEventDestroy(sh1);
+  }
   const std::string nm = name ? name : "gemm";
   c.prof_end(c.prof_detail ? (nm + "@" + c.phase).c_str() : nm.c_str(), ev, fl, by);
   c.launches++;

@@ -82,7 +82,11 @@ def check_against_reference(rep, gold):
     for k in ("top_level_max_rank", "max_leaf_rank", "dense_blocks_leaf", "stored_entries",
               "memory_bytes", "dependency_edges"):
         assert rep[k] == gold[k], k
-    assert rep["max_fill_residual_rel"] == pytest.approx(gold["max_fill_residual_rel"], rel=1e-10)
+    # resid/nf = sqrt(nf^2 - kept^2)/nf (ulv.cpp:386-388) cancels to ~1e-7 of nf: one ulp of
+    # either norm (the golden's build vectorises norm_frobenius 8 wide, -march=native) moves it
+    # by eps/ratio^2 relative, so the comparison carries that conditioning (a few ulps).
+    ratio = gold["max_fill_residual_rel"]
+    assert rep["max_fill_residual_rel"] == pytest.approx(ratio, rel=min(0.5, 8 * 2.3e-16 / ratio ** 2))
     assert rep["solve_rel_error"] == pytest.approx(gold["solve_rel_error"], rel=1e-6)
 
 
