@@ -214,9 +214,23 @@ void GemmBatch::run(Ctx& c, int tag) {
   int max_rows = 0;
   for (auto& j : jobs) max_rows = std::max(max_rows, j.C.rows);
   const int bm = gemm_tile_rows(max_rows);
+  // Plain operands (no generated B, no symmetric tile skipping): the persistent
+  // m8n8k4 kernel with 8-row tile granularity (k_gemm8.cu).
+  static const bool p8_on = getenv("H2G_GEMM_P8") == nullptr || atoi(getenv("H2G_GEMM_P8")) != 0;
+  bool p8 = p8_on && bm == 128;
+  for (size_t j = 0; p8 && j < jobs.size(); ++j) p8 = !lower[j];
+  for (size_t s = 0; p8 && s < segs.size(); ++s) p8 = !segs[s].gen;
   for (size_t j = 0; j < jobs.size(); ++j) {
     const Mat& C = jobs[j].C;
     if (C.rows <= 0 || C.cols <= 0) continue;
+    if (p8) {
+      for (int s = 0; s < jobs[j].nseg; ++s)
+        fl += 2.0 * C.rows * double(segs[jobs[j].seg0 + s].A.cols) * C.cols;
+      const int tm = gemm_p8_row_tiles(C.rows), tn = gemm_p8_col_tiles(C.cols);
+      for (int b = 0; b < tn; ++b)
+        for (int a = 0; a < tm; ++a) tiles.push_back({int(j), a, b});
+      continue;
+    }
     const int tm = (C.rows + bm - 1) / bm, tn = (C.cols + 63) / 64;
     // Symmetric C: tiles entirely above the diagonal are skipped (and not counted).
     auto above = [&](int a, int b) { return lower[j] && b * 64 >= (a + 1) * bm; };
@@ -292,8 +306,11 @@ void GemmBatch::run(Ctx& c, int tag) {
     cudaEventRecord(sh0, c.stream);
   }
   auto ev = c.prof_begin();
-  launch_gemm(dj, ds, dt, int(tiles.size()), bm, c.kp, c.cloud, c.err, tag, c.stream,
-              name && std::string(name) == "gram" ? 1 : 0);
+  if (p8)
+    launch_gemm_p8(dj, ds, dt, int(tiles.size()), c.stream);
+  else
+    launch_gemm(dj, ds, dt, int(tiles.size()), bm, c.kp, c.cloud, c.err, tag, c.stream,
+                name && std::string(name) == "gram" ? 1 : 0);
   if (shapes) {
     cudaEventRecord(sh1, c.stream);
     cudaEventSynchronize(sh1);

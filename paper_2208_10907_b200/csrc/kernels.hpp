@@ -46,6 +46,14 @@ void launch_gemm(const GemmJob* jobs, const GemmSeg* segs, const GemmTile* tiles
                  int bm, KernelParams kp, Cloud cloud, ErrWord* err, int tag, cudaStream_t st,
                  int kind = 0);
 
+// Persistent m8n8k4 kernel for plain operands (k_gemm8.cu): tiles are up to
+// 104 rows (a job's 8-row fragments split evenly over gemm_p8_row_tiles) x 128
+// columns; GemmTile {job, row tile, column tile}.
+int gemm_p8_row_tiles(int rows);
+int gemm_p8_col_tiles(int cols);
+void launch_gemm_p8(const GemmJob* jobs, const GemmSeg* segs, const GemmTile* tiles, int ntiles,
+                    cudaStream_t st);
+
 // ---- batched kernel-block evaluation (k_eval.cu) ---------------------------
 // out(i, j) = K(x[rb + i], x[cb + j]) (assemble_block, kernels.cpp:242-268).
 struct EvalJob {
