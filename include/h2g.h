@@ -65,6 +65,12 @@ int h2g_create(h2g_problem** out);
 void h2g_destroy(h2g_problem* p);
 int h2g_set_kernel(h2g_problem* p, const h2g_kernel* k);
 int h2g_set_options(h2g_problem* p, const h2g_options* o);
+/* B200 extension (no reference counterpart): far-field basis members wider than
+ * sample_cols columns are replaced by a strided sample of about sample_cols of
+ * their columns - the reference concatenates every far-field column
+ * (compression.cpp:153-177, ulv.cpp:476-521), O(N) per box. 0 = off (the
+ * reference's members, the default); otherwise >= 64. Parity by tolerance. */
+int h2g_set_sampling(h2g_problem* p, int64_t sample_cols);
 
 /* build_cluster_tree (geometry.hpp:58) + classify_blocks (hstructure.hpp:55)
  * + materialize_dense (hstructure.hpp:101-103) = Pipeline::build

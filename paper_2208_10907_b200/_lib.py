@@ -41,7 +41,7 @@ EXPORTS = [
     "h2g_nccl_unique_id", "h2g_comm_nccl", "h2g_comm_host", "h2g_comm_destroy", "h2g_set_comm",
     "h2g_partition_range", "h2g_kernel_evals", "h2g_generate_points", "h2g_points_last_error",
     "h2g_exp_glibc_host", "h2g_level_dims", "h2g_level_block", "h2g_level_lu", "h2g_level_elim",
-    "h2g_assemble_block",
+    "h2g_assemble_block", "h2g_set_sampling",
 ]
 
 # h2g_host_allgather_fn (include/h2g.h)
@@ -66,6 +66,7 @@ def lib():
         L.h2g_destroy.argtypes = [P]
         L.h2g_set_kernel.argtypes = [P, ctypes.POINTER(Kernel)]
         L.h2g_set_options.argtypes = [P, ctypes.POINTER(Options)]
+        L.h2g_set_sampling.argtypes = [P, i64]
         L.h2g_build.argtypes = [P, i64, P, P, i64]
         L.h2g_build_dev.argtypes = [P, i64, P, P, i64]
         L.h2g_factor.argtypes = [P]
@@ -226,11 +227,13 @@ class Problem:
 
     def set_options(self, tol=1e-8, cap=None, rr_pivot_tol=1e-13, absorb_coupling=True,
                     abort_residual_factor=100.0, structure="h2", eta=1.0, qr_mem_budget=0, qr_mode="exact",
-                    reference_compat=True):
+                    reference_compat=True, sample_cols=0):
         o = Options(tol, cap or 0, rr_pivot_tol, 1 if absorb_coupling else 0, abort_residual_factor,
                     {"h2": 0, "hss": 1, "blr2": 2}[structure], eta, qr_mem_budget, {"exact": 0, "blocked": 1, "compressed": 2}[qr_mode],
                     1 if reference_compat else 0)
         _check(self.L.h2g_set_options(self.h, ctypes.byref(o)))
+        # B200 extension: strided sampling of wide far-field basis members (0 = the reference's members).
+        _check(self.L.h2g_set_sampling(self.h, int(sample_cols or 0)))
 
     def build(self, xyz, q, leaf):
         xyz = np.ascontiguousarray(xyz, dtype=np.float64)

@@ -121,6 +121,15 @@ int h2g_set_options(h2g_problem* p, const h2g_options* o) {
   });
 }
 
+int h2g_set_sampling(h2g_problem* p, int64_t sample_cols) {
+  return guarded([&] {
+    if (sample_cols < 0) throw std::invalid_argument("config: sample_cols must be >= 0");
+    if (sample_cols > 0 && sample_cols < 64)
+      throw std::invalid_argument("config: sample_cols must be 0 (off) or at least 64");
+    p->P.opt.sample_cols = int(std::min<int64_t>(sample_cols, 1 << 30));
+  });
+}
+
 int h2g_build_dev(h2g_problem* p, int64_t n, const double* d_xyz, const double* d_q, int64_t leaf) {
   return guarded([&] { p->P.build(d_xyz, d_q, n, leaf); });
 }

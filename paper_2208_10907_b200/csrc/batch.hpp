@@ -149,7 +149,7 @@ struct GemmBatch {
   }
   // B generated from the kernel function: trans = 0 -> B(l,j) = K(rb+l, cb+j).
   void seg_gen(Mat A, int64_t rb, int64_t cb, int Bcols, bool trans, double alpha,
-               const std::vector<int2>& mask = {}) {
+               const std::vector<int2>& mask = {}, int jstep = 1) {
     GemmSeg s;
     s.A = A;
     s.B = Mat{nullptr, A.cols, Bcols, 0, 0};
@@ -158,6 +158,7 @@ struct GemmBatch {
     s.g.rb = rb;
     s.g.cb = cb;
     s.g.trans = trans ? 1 : 0;
+    s.g.jstep = jstep;
     s.g.nmask = int(mask.size());
     seg_mask_off.push_back(mask.empty() ? -1 : int(masks.size()));
     masks.insert(masks.end(), mask.begin(), mask.end());
@@ -177,7 +178,9 @@ inline void gemm1(GemmBatch& b, Mat C, Mat A, Mat B, double alpha = 1.0, bool ac
 // ---- kernel-block evaluation ------------------------------------------------
 struct EvalBatch {
   std::vector<EvalJob> jobs;
-  void add(Mat out, int64_t rb, int64_t cb) { jobs.push_back({out, rb, cb}); }
+  void add(Mat out, int64_t rb, int64_t cb, int rstep = 1, int cstep = 1) {
+    jobs.push_back({out, rb, cb, rstep, cstep});
+  }
   void run(Ctx& c, int tag = 0);
 };
 

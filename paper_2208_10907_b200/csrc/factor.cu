@@ -403,6 +403,20 @@ struct Driver {
     M.concat.m = Mat{M.concat.m.p, M.dim, M.width, 1, ldc(M.dim)};
   }
 
+  // Sampled far-field members (Options::sample_cols > 0): a member of w
+  // columns wider than sample_cols keeps every step-th column.
+  struct Samp {
+    int step, count;
+  };
+  Samp samp(int64_t w) const {
+    if (opt.sample_cols <= 0 || w <= opt.sample_cols) return {1, int(w)};
+    const int step = int((w + opt.sample_cols - 1) / opt.sample_cols);
+    return {step, int((w + step - 1) / step)};
+  }
+  static Mat sample_cols_view(const Mat& a, const Samp& sp) {
+    return Mat{a.p, a.rows, sp.count, a.rs, a.cs * sp.step};
+  }
+
   using FillFn = std::function<void(int64_t, int64_t)>;
   using SinkFn = std::function<void(int64_t, const Mat&, int, const Mat&, int)>;
 
@@ -709,13 +723,13 @@ struct Driver {
       Members& R = rows[i];
       R.dim = sys.dims[i];
       for (const DMat* F : FI.by_row[i]) R.add(F->cols());
-      for (int64_t t = 0; t < S.nfar(L, i); ++t) R.add(int(rs(L, S.far(L, i)[t])));
-      for (auto [l2, J] : ancestor_far_partners(L, i)) R.add(int(rs(l2, J)));
+      for (int64_t t = 0; t < S.nfar(L, i); ++t) R.add(samp(rs(L, S.far(L, i)[t])).count);
+      for (auto [l2, J] : ancestor_far_partners(L, i)) R.add(samp(rs(l2, J)).count);
       Members& C = cols[i];
       C.dim = sys.dims[i];
       for (const DMat* F : FI.by_col[i]) C.add(F->rows());
-      for (int64_t t = 0; t < S.nfar(L, i); ++t) C.add(int(rs(L, S.far(L, i)[t])));
-      for (auto [l2, I] : ancestor_far_partners(L, i)) C.add(int(rs(l2, I)));
+      for (int64_t t = 0; t < S.nfar(L, i); ++t) C.add(samp(rs(L, S.far(L, i)[t])).count);
+      for (auto [l2, I] : ancestor_far_partners(L, i)) C.add(samp(rs(l2, I)).count);
     }
     auto fill_base_rows = [&](std::vector<Members>& R, int64_t k0, int64_t k1, CopyBatch& cb,
                               EvalBatch& eb) {
@@ -727,12 +741,14 @@ struct Driver {
         }
         for (int64_t t = 0; t < S.nfar(L, i); ++t) {
           const int64_t j = S.far(L, i)[t];
-          eb.add(R[i].slice(off, int(rs(L, j))), rb(L, i), rb(L, j));
-          off += int(rs(L, j));
+          const Samp sp = samp(rs(L, j));
+          eb.add(R[i].slice(off, sp.count), rb(L, i), rb(L, j), 1, sp.step);
+          off += sp.count;
         }
         for (auto [l2, J] : ancestor_far_partners(L, i)) {
-          eb.add(R[i].slice(off, int(rs(l2, J))), rb(L, i), rb(l2, J));
-          off += int(rs(l2, J));
+          const Samp sp = samp(rs(l2, J));
+          eb.add(R[i].slice(off, sp.count), rb(L, i), rb(l2, J), 1, sp.step);
+          off += sp.count;
         }
       }
     };
@@ -860,12 +876,14 @@ struct Driver {
                   }
                   for (int64_t t = 0; t < S.nfar(L, j); ++t) {
                     const int64_t i = S.far(L, j)[t];
-                    eb.add(C.slice(off, int(rs(L, i))).t(), rb(L, i), rb(L, j));
-                    off += int(rs(L, i));
+                    const Samp sp = samp(rs(L, i));
+                    eb.add(C.slice(off, sp.count).t(), rb(L, i), rb(L, j), sp.step, 1);
+                    off += sp.count;
                   }
                   for (auto [l2, I] : ancestor_far_partners(L, j)) {
-                    eb.add(C.slice(off, int(rs(l2, I))).t(), rb(l2, I), rb(L, j));
-                    off += int(rs(l2, I));
+                    const Samp sp = samp(rs(l2, I));
+                    eb.add(C.slice(off, sp.count).t(), rb(l2, I), rb(L, j), sp.step, 1);
+                    off += sp.count;
                   }
                 }
                 cb.run(c);
@@ -1368,10 +1386,10 @@ struct Driver {
     for (int64_t k = 0; k < m; ++k) {
       rows[k].dim = cols[k].dim = sys.dims[k];
       for (const DMat* F : FI.by_row[k]) rows[k].add(F->cols());
-      for (auto& [tk, piece] : merged[k]) rows[k].add(piece.cols());
+      for (auto& [tk, piece] : merged[k]) rows[k].add(samp(piece.cols()).count);
       for (const DMat* F : FI.by_col[k]) cols[k].add(F->rows());
       for (int64_t t = 0; t < S.nfar(lvl, k); ++t) cols[k].add(sys.dims[S.far(lvl, k)[t]]);
-      for (auto [l2, I] : ancestor_far_partners(lvl, k)) cols[k].add(int(rs(l2, I)));
+      for (auto [l2, I] : ancestor_far_partners(lvl, k)) cols[k].add(samp(rs(l2, I)).count);
     }
     for (int64_t k = 0; k < m; ++k)
       if (sys.dims[k] == 0 && rows[k].width > 0)
@@ -1389,8 +1407,9 @@ struct Driver {
                     off += F->cols();
                   }
                   for (auto& [tk, piece] : merged[k]) {
-                    cb.copy(rows[k].slice(off, piece.cols()), piece.m);
-                    off += piece.cols();
+                    const Samp sp = samp(piece.cols());
+                    cb.copy(rows[k].slice(off, sp.count), sample_cols_view(piece.m, sp));
+                    off += sp.count;
                   }
                   off = 0;
                   for (const DMat* F : FI.by_col[k]) {
@@ -1413,12 +1432,13 @@ struct Driver {
                   const Mat v1T = keep.back().m;
                   for (auto [l2, I] : anc) {
                     // (A(I, c0) Vbig_c0 | A(I, c1) Vbig_c1)^T, B generated in-kernel.
-                    const int w = int(rs(l2, I));
+                    const Samp sp = samp(rs(l2, I));
+                    const int w = sp.count;
                     const Mat dst = cols[k].slice(off, w);
                     gb.job(dst.sub(0, 0, v0.cols, w), false);
-                    gb.seg_gen(v0T, rb(l2, I), rb(lvl + 1, 2 * k), w, true, 1.0);
+                    gb.seg_gen(v0T, rb(l2, I), rb(lvl + 1, 2 * k), w, true, 1.0, {}, sp.step);
                     gb.job(dst.sub(v0.cols, 0, v1.cols, w), false);
-                    gb.seg_gen(v1T, rb(l2, I), rb(lvl + 1, 2 * k + 1), w, true, 1.0);
+                    gb.seg_gen(v1T, rb(l2, I), rb(lvl + 1, 2 * k + 1), w, true, 1.0, {}, sp.step);
                     off += w;
                   }
                 }

@@ -27,6 +27,11 @@ struct Options {  // FactorOptions (ulv.hpp:29-45) + RunConfig bits
   // true: the reference's assembly bit for bit (covered couplings skipped,
   // ulv.cpp:424-463, :583-603); false: corrected (oracle/fix_reference.py).
   bool reference_compat = true;
+  // > 0: far-field basis members wider than this many columns are replaced by
+  // a strided sample of about this many of their columns (the north star's
+  // "far-field samples"; the reference concatenates every column,
+  // compression.cpp:153-177, ulv.cpp:476-521). 0 = the reference's members.
+  int sample_cols = 0;
 };
 
 struct Basis {  // SharedBasis (hstructure.hpp:61-69): square [Qr | Qs]

@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(NT) eval_kernel(const EvalJob* __restrict__ jo
   for (int e = threadIdx.x; e < T * T; e += NT) {
     const int i = r0 + (e % T), j = c0 + (e / T);
     if (i < job.out.rows && j < job.out.cols)
-      job.out.at(i, j) = kernel_entry(kp, cloud, job.rb + i, job.cb + j, &singular);
+      job.out.at(i, j) = kernel_entry(kp, cloud, job.rb + int64_t(i) * job.rstep, job.cb + int64_t(j) * job.cstep, &singular);
   }
   if (singular) raise_err(err, 1, jb, 0, tag);
 }

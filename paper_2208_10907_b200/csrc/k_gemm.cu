@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(2 * BM) gemm_kernel(const GemmJob* __restrict_
     if (sg.gen) {
       liveT = jT < C.cols && !sm.Bmask[nnT];
       if (liveT) {
-        const int64_t tp = sg.g.trans ? sg.g.rb + jT : sg.g.cb + jT;
+        const int64_t tp = (sg.g.trans ? sg.g.rb : sg.g.cb) + int64_t(jT) * sg.g.jstep;
         xT = cloud.x[tp];
         yT = cloud.y[tp];
         zT = cloud.z[tp];
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(NTW, 1) gemm_ws_kernel(const GemmJob* __restri
             if (jT >= sg.g.mask[q].x && jT < sg.g.mask[q].y) masked_col = true;
           liveT = jT < C.cols && !masked_col;
           if (liveT) {
-            const int64_t tp = sg.g.trans ? sg.g.rb + jT : sg.g.cb + jT;
+            const int64_t tp = (sg.g.trans ? sg.g.rb : sg.g.cb) + int64_t(jT) * sg.g.jstep;
             xT = cloud.x[tp];
             yT = cloud.y[tp];
             zT = cloud.z[tp];

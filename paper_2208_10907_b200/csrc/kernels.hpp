@@ -23,6 +23,7 @@ void smem_attr(const void* kernel, size_t bytes, const char* what);  // batch.cu
 struct GenB {
   int64_t rb = 0, cb = 0;
   int trans = 0;
+  int jstep = 1;  // column j addresses point base + j * jstep (sampled far-field columns)
   int nmask = 0;
   const int2* mask = nullptr;  // device pointer
 };
@@ -56,9 +57,12 @@ void launch_gemm_p8(const GemmJob* jobs, const GemmSeg* segs, const GemmTile* ti
 
 // ---- batched kernel-block evaluation (k_eval.cu) ---------------------------
 // out(i, j) = K(x[rb + i], x[cb + j]) (assemble_block, kernels.cpp:242-268).
+// rstep / cstep > 1 evaluate a strided sample of the row / column points
+// (sampled far-field members, Options::sample_cols; not in the reference).
 struct EvalJob {
   Mat out;
   int64_t rb, cb;
+  int rstep = 1, cstep = 1;
 };
 void launch_eval(const EvalJob* jobs, const int* tile_job, const int* tile_idx, int ntiles,
                  KernelParams kp, Cloud cloud, ErrWord* err, int tag, cudaStream_t st);
