@@ -218,17 +218,24 @@ void GemmBatch::run(Ctx& c, int tag) {
   // m8n8k4 kernel with 8-row tile granularity (k_gemm8.cu).
   static const bool p8_on = getenv("H2G_GEMM_P8") == nullptr || atoi(getenv("H2G_GEMM_P8")) != 0;
   bool p8 = p8_on && bm == 128;
-  for (size_t j = 0; p8 && j < jobs.size(); ++j) p8 = !lower[j];
   for (size_t s = 0; p8 && s < segs.size(); ++s) p8 = !segs[s].gen;
   for (size_t j = 0; j < jobs.size(); ++j) {
     const Mat& C = jobs[j].C;
     if (C.rows <= 0 || C.cols <= 0) continue;
     if (p8) {
-      for (int s = 0; s < jobs[j].nseg; ++s)
-        fl += 2.0 * C.rows * double(segs[jobs[j].seg0 + s].A.cols) * C.cols;
       const int tm = gemm_p8_row_tiles(C.rows), tn = gemm_p8_col_tiles(C.cols);
+      // Symmetric C: a tile is kept when its first column is below its last row.
+      auto keep = [&](int a, int b) { return !lower[j] || b * gemm_p8_tile_cols() < gemm_p8_row_end(C.rows, a); };
+      int kept = 0;
       for (int b = 0; b < tn; ++b)
-        for (int a = 0; a < tm; ++a) tiles.push_back({int(j), a, b});
+        for (int a = 0; a < tm; ++a)
+          if (keep(a, b)) {
+            tiles.push_back({int(j), a, b});
+            ++kept;
+          }
+      const double frac = double(kept) / (tm * tn);
+      for (int s = 0; s < jobs[j].nseg; ++s)
+        fl += frac * 2.0 * C.rows * double(segs[jobs[j].seg0 + s].A.cols) * C.cols;
       continue;
     }
     const int tm = (C.rows + bm - 1) / bm, tn = (C.cols + 63) / 64;

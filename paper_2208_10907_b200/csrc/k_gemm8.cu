@@ -347,6 +347,12 @@ __global__ void __launch_bounds__(NT, 1) gemm_p8_kernel(const GemmJob* __restric
 
 int gemm_p8_row_tiles(int rows) { return (rows + p8::TM - 1) / p8::TM; }
 int gemm_p8_col_tiles(int cols) { return (cols + p8::TN - 1) / p8::TN; }
+int gemm_p8_tile_cols() { return p8::TN; }
+int gemm_p8_row_end(int rows, int tm) {
+  const int nt = (rows + p8::TM - 1) / p8::TM, F = (rows + 7) >> 3;
+  const int end = 8 * ((tm + 1) * F / nt);
+  return end < rows ? end : rows;
+}
 
 void launch_gemm_p8(const GemmJob* jobs, const GemmSeg* segs, const GemmTile* tiles, int ntiles,
                     cudaStream_t st) {

@@ -52,6 +52,8 @@ void launch_gemm(const GemmJob* jobs, const GemmSeg* segs, const GemmTile* tiles
 // columns; GemmTile {job, row tile, column tile}.
 int gemm_p8_row_tiles(int rows);
 int gemm_p8_col_tiles(int cols);
+int gemm_p8_tile_cols();
+int gemm_p8_row_end(int rows, int tm);  // one past the last row of row tile tm
 void launch_gemm_p8(const GemmJob* jobs, const GemmSeg* segs, const GemmTile* tiles, int ntiles,
                     cudaStream_t st);
 
