@@ -358,6 +358,37 @@ def run_b200_arm(args):
                  "note": "same workload, the reference's assembly and QR rounding (bit-exact with "
                          "the unmodified reference, tests/test_bench_parity.py); device time"}
 
+    # Secondary figure: the same step with sampled far-field basis members
+    # (h2g_set_sampling; the north star's "far-field samples"). The headline
+    # keeps the reference's full members.
+    sampled = None
+    if args.sample_cols > 0 and args.sampled_steps > 0:
+        with torch.cuda.stream(stream):
+            p = new_problem()
+            p.set_options(tol=WORKLOAD["tol"], cap=WORKLOAD["cap"], eta=WORKLOAD["eta"], qr_mode=qr_mode,
+                          reference_compat=compat, sample_cols=args.sample_cols)
+            step(p)  # warm-up
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.sampled_steps):
+                step(p)
+            e1.record(stream)
+            barrier()
+            ts = e0.elapsed_time(e1) * 1e-3 / args.sampled_steps
+            xs = d_x.cpu().numpy()
+            rs_ = float(np.linalg.norm(p.matvec(xs) - b) / np.linalg.norm(b))
+            p.close()
+        if world > 1:
+            tt = torch.tensor([ts], device="cuda", dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            ts = float(tt.item())
+        sampled = {"sample_cols": args.sample_cols, "points_per_s": points / ts, "ms_per_step": ts * 1e3,
+                   "steps": args.sampled_steps, "solve_rel_residual": rs_,
+                   "note": "far-field basis members wider than sample_cols replaced by a strided column "
+                           "sample (tolerance parity, tests/test_qr_blocked.py); device time"}
+
     # dominant kernel family and its roofline
     import json as _json
     peaks = {}
@@ -381,7 +412,8 @@ def run_b200_arm(args):
                     "unit": "TFLOP/s", "frac": achieved / FP64_DMMA_TFLOPS,
                     "traffic": traffic.get("bytes_per_launch") if traffic else None,
                     "algorithmic_flops_per_launch": flops_per_launch, "avg_launch_ms": avg_ms,
-                    "peak_source": "profiles/r01_fp64_peak_probe.txt (DMMA m16n8k16, measured on B200)",
+                    "peak_source": "profiles/r01_fp64_peak_probe.txt (DMMA, measured on B200; MEASURED_PEAKS.json has no FP64 figure)",
+                    "traffic_source": traffic.get("source") if traffic else None,
                     "share_of_step": st["ms"] * 1e-3 / max(1e-12, t_phase["build"] + t_phase["factor"] + t_phase["solve"]) if st else None}
     else:
         achieved = bytes_per_launch / (avg_ms * 1e-3) / 1e9 if avg_ms else 0.0
@@ -452,6 +484,7 @@ def run_b200_arm(args):
             "clocks": clk,
             "cpu_baseline": cpu_baseline,
             "exact_qr": exact,
+            "sampled_members": sampled,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -475,6 +508,9 @@ def main():
                          "rounding, bit-exact)")
     ap.add_argument("--exact-steps", type=int, default=1,
                     help="extra device-timed steps in exact QR mode, reported beside the headline")
+    ap.add_argument("--sample-cols", type=int, default=512,
+                    help="column budget of the secondary sampled-member measurement (0: skip)")
+    ap.add_argument("--sampled-steps", type=int, default=2)
     ap.add_argument("--compat", action="store_true",
                     help="the reference's h2/nodep assembly bit for bit, covered-coupling defect "
                          "included (default: the corrected assembly, reference_compat = 0)")

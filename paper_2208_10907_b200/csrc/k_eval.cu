@@ -16,16 +16,42 @@ __global__ void __launch_bounds__(NT) eval_kernel(const EvalJob* __restrict__ jo
                                                   const int* __restrict__ tile_idx,
                                                   KernelParams kp, Cloud cloud, ErrWord* err,
                                                   int tag) {
+  // A thread's row is fixed (NT is a multiple of T): its point stays in
+  // registers; the tile's 64 column points are staged in shared memory and
+  // read as warp-wide broadcasts (a warp's 32 entries share one column).
+  __shared__ double cpt[T][4];
   const int jb = tile_job[blockIdx.x];
   const EvalJob job = jobs[jb];
   const int tpr = (job.out.rows + T - 1) / T;
   const int ti = tile_idx[blockIdx.x];
   const int r0 = (ti % tpr) * T, c0 = (ti / tpr) * T;
+  {
+    const int jj = threadIdx.x >> 2, comp = threadIdx.x & 3;  // NT = 4 T
+    double v = 0.0;
+    if (c0 + jj < job.out.cols) {
+      const int64_t pj = job.cb + int64_t(c0 + jj) * job.cstep;
+      const double* src = comp == 0 ? cloud.x : comp == 1 ? cloud.y : comp == 2 ? cloud.z : cloud.q;
+      v = src[pj];
+    }
+    cpt[jj][comp] = v;
+  }
+  const int i = r0 + (threadIdx.x % T);
+  double xi = 0.0, yi = 0.0, zi = 0.0;
+  if (i < job.out.rows) {
+    const int64_t pi = job.rb + int64_t(i) * job.rstep;
+    xi = cloud.x[pi];
+    yi = cloud.y[pi];
+    zi = cloud.z[pi];
+  }
+  __syncthreads();
   int singular = 0;
-  for (int e = threadIdx.x; e < T * T; e += NT) {
-    const int i = r0 + (e % T), j = c0 + (e / T);
-    if (i < job.out.rows && j < job.out.cols)
-      job.out.at(i, j) = kernel_entry(kp, cloud, job.rb + int64_t(i) * job.rstep, job.cb + int64_t(j) * job.cstep, &singular);
+  if (i < job.out.rows) {
+    double* dst = &job.out.at(i, c0);
+    const int jn = min(T, job.out.cols - c0);
+#pragma unroll 4
+    for (int jj = threadIdx.x / T; jj < jn; jj += NT / T)
+      dst[int64_t(jj) * job.out.cs] =
+          kernel_pair(kp, xi, yi, zi, cpt[jj][0], cpt[jj][1], cpt[jj][2], cpt[jj][3], &singular);
   }
   if (singular) raise_err(err, 1, jb, 0, tag);
 }
