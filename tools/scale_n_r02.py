@@ -3,7 +3,7 @@ Yukawa, leaf 256, cap 100, tol 1e-6; compressed QR, corrected assembly), with
 the reference's full far-field members and with sampled members
 (h2g_set_sampling 512). The fill-absorption abort (ulv.cpp:140-147) is
 disabled (abort_residual_factor = 1e30) so sizes past 98,304 run; device time
-after one warm-up factorization per size.
+after two warm-up factorizations per size and mode.
 
   python tools/scale_n_r02.py N [N ...]
 """
@@ -30,6 +30,7 @@ for n in map(int, sys.argv[1:]):
             p.factor()
             return p
         try:
+            run().close()
             run().close()
             p = run()
             sd = p.stats_dev()
