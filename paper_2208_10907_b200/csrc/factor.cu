@@ -1394,11 +1394,39 @@ struct Driver {
     for (int64_t k = 0; k < m; ++k)
       if (sys.dims[k] == 0 && rows[k].width > 0)
         throw std::runtime_error("compute_transfer: rank-0 children with nonzero parent blocks");
+    // Tolerance modes: the ancestor-partner column members are nested. With
+    // Vbig_c = blockdiag(Vbig of c's children) Vs_c, the member of child c
+    // toward I is Vs_c^T times c's own member toward I of the previous (finer)
+    // level, so from the second transfer level on no kernel entry is evaluated
+    // again (the reference evaluates A(I, c) Vbig_c from scratch at every
+    // level, ulv.cpp:495-501). The members of this level are kept for the next.
+    const bool nest = c.fast_solve && lvl + 1 < L && int64_t(prev_cols_.size()) == 2 * m;
+    std::vector<DMat> keepm;
+    std::vector<int> anc_off(m, 0), anc_w(m, 0);
+    for (int64_t k = 0; k < m; ++k) {
+      anc_off[k] = cols[k].width;
+      for (auto [l2, I] : ancestor_far_partners(lvl, k)) {
+        const int w = samp(rs(l2, I)).count;
+        anc_off[k] -= w;
+        anc_w[k] += w;
+      }
+    }
+    if (c.fast_solve && lvl >= 3) {
+      size_t need = 0, fr = 0, tot = 0;
+      for (int64_t k = 0; k < m; ++k) need += sizeof(double) * size_t(sys.dims[k]) * size_t(anc_w[k]);
+      cuda_check(cudaMemGetInfo(&fr, &tot), "meminfo");
+      if (need < fr / 4) {
+        std::vector<std::pair<int, int>> ks;
+        for (int64_t k = 0; k < m; ++k) ks.push_back({sys.dims[k], anc_w[k]});
+        keepm = alloc_mats(c, ks);
+      }
+    }
     CopyBatch sqcopies;
     run_bases(rows, &cols,
               [&](int64_t k0, int64_t k1) {
                 CopyBatch cb;
                 GemmBatch gb;
+                CopyBatch kb;            // this level's ancestor members -> keepm
                 std::vector<DMat> keep;  // A operands alive until the GEMMs are queued
                 for (int64_t k = k0; k < k1; ++k) {
                   int off = 0;
@@ -1424,8 +1452,23 @@ struct Driver {
                   }
                   const auto anc = ancestor_far_partners(lvl, k);
                   if (anc.empty()) continue;
-                  // Vbig_c^T column-major (even ld) for the generated GEMMs' A.
                   const Mat v0 = Vbig[2 * k], v1 = Vbig[2 * k + 1];
+                  if (!keepm.empty() && anc_w[k] > 0 && sys.dims[k] > 0)
+                    kb.copy(keepm[k].m, cols[k].slice(anc_off[k], anc_w[k]));
+                  if (nest && prev_cols_[2 * k].m.p && prev_cols_[2 * k + 1].m.p) {
+                    // prev_cols_[c]: c's ancestor members of the finer level, in
+                    // ancestor_far_partners(lvl + 1, c) order = far(lvl, k), then anc.
+                    int skip = 0;
+                    for (int64_t t = 0; t < S.nfar(lvl, k); ++t) skip += samp(rs(lvl, S.far(lvl, k)[t])).count;
+                    const Mat q0 = P.V[lvl + 1][2 * k].Qs().t(), q1 = P.V[lvl + 1][2 * k + 1].Qs().t();
+                    const Mat p0 = prev_cols_[2 * k].m, p1 = prev_cols_[2 * k + 1].m;
+                    const Mat dst = cols[k].slice(off, anc_w[k]);
+                    if (v0.cols > 0) gemm1(gb, dst.sub(0, 0, v0.cols, anc_w[k]), q0, p0.sub(0, skip, p0.rows, anc_w[k]));
+                    if (v1.cols > 0)
+                      gemm1(gb, dst.sub(v0.cols, 0, v1.cols, anc_w[k]), q1, p1.sub(0, skip, p1.rows, anc_w[k]));
+                    continue;
+                  }
+                  // Vbig_c^T column-major (even ld) for the generated GEMMs' A.
                   keep.push_back(colmajor_copy(cb, v0.t()));
                   const Mat v0T = keep.back().m;
                   keep.push_back(colmajor_copy(cb, v1.t()));
@@ -1444,6 +1487,7 @@ struct Driver {
                 }
                 cb.run(c);
                 gb.run(c);
+                kb.run(c);
               },
               [&](int64_t k, const Mat& qu, int ru, const Mat& qv, int rv) {
                 square_sink(P.U[lvl], P.V[lvl], sqcopies)(k, qu, ru, qv, rv);
@@ -1452,7 +1496,16 @@ struct Driver {
                 sqcopies.run(c);
                 sqcopies.jobs.clear();
               });
+    if (!keepm.empty()) {  // multi-GPU: every rank needs every box's members at replicated levels
+      std::vector<int64_t> box;
+      for (int64_t k = 0; k < m; ++k) box.push_back(k);
+      exchange_mats(keepm, box, m);
+    }
+    prev_cols_ = std::move(keepm);
   }
+  // Transfer stage, tolerance modes: per box of the previous (finer) transfer
+  // level, its ancestor-partner column members (dims x sum of sampled widths).
+  std::vector<DMat> prev_cols_;
 
   // ---- assemble_level (ulv.cpp:526-607) ----------------------------------------
   void assemble_level(SysL& sys, const FillSet& fills, const std::vector<PieceMap>& pieces,

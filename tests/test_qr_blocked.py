@@ -235,3 +235,37 @@ def test_sampling_option_validation():
     p.set_options(sample_cols=0)
     p.set_options(sample_cols=512)
     p.close()
+
+
+def test_nested_transfer_column_members_match_evaluated_ones(monkeypatch):
+    """Tolerance modes build the transfer stage's ancestor-partner column members
+    from the finer level's members (Vs_c^T times the child's member; Vbig is
+    nested) instead of evaluating A(I, c) Vbig_c again at every level
+    (ulv.cpp:495-501). Against the evaluated members (H2G_EXACT_SOLVES=1, which
+    also turns the other reassociations off) on a 7-level tree in the solver
+    regime: fewer kernel evaluations, the same ranks, x equal to 1e-9."""
+    from oracle import ref
+    n, leaf = 16384, 128
+    xyz, q = h2.generate_points("sphere", n, 42)
+    b = ref.splitmix_signed(n, 7)
+
+    def run():
+        p = h2.Problem()
+        p.set_kernel("yukawa", 1.0, 1.0, 1e-3)
+        p.set_options(tol=1e-6, cap=100, qr_mode="compressed", reference_compat=False)
+        p.build(xyz, q, leaf)
+        p.factor()
+        x = p.solve(b)
+        r = float(np.linalg.norm(p.matvec(x) - b) / np.linalg.norm(b))
+        out = (x, r, p.stats()["kernel_evals"], [rk.tolist() for _, rk in p.factor_levels()])
+        p.close()
+        return out
+
+    monkeypatch.delenv("H2G_EXACT_SOLVES", raising=False)
+    xn, rn, en, kn = run()
+    monkeypatch.setenv("H2G_EXACT_SOLVES", "1")
+    xe, re_, ee, ke = run()
+    assert rn < 1e-4 and re_ < 1e-4, (rn, re_)
+    assert en < ee, (en, ee)
+    assert kn == ke
+    assert np.linalg.norm(xn - xe) / np.linalg.norm(xe) < 1e-9
