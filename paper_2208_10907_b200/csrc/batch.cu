@@ -349,7 +349,7 @@ void EvalBatch::run(Ctx& c, int tag) {
   auto* dti = upload(c, ti, k3);
   auto ev = c.prof_begin();
   launch_eval(dj, dtj, dti, int(tj.size()), c.kp, c.cloud, c.err, tag, c.stream);
-  c.prof_end("eval", ev, ev_flops_, 8.0 * evn_);
+  c.prof_end(c.prof_detail ? ("eval@" + c.phase).c_str() : "eval", ev, ev_flops_, 8.0 * evn_);
   c.launches++;
   cuda_check(cudaGetLastError(), "eval launch");
 }
@@ -367,7 +367,7 @@ void CopyBatch::run(Ctx& c) {
   for (auto& j : jobs) by += 8.0 * j.dst.rows * double(j.dst.cols) * (1 + (j.src.p ? 1 : 0) + j.add);
   auto ev = c.prof_begin();
   launch_copy(dj, dtj, dti, int(tj.size()), c.stream);
-  c.prof_end("copy", ev, 0.0, by);
+  c.prof_end(c.prof_detail ? ("copy@" + c.phase).c_str() : "copy", ev, 0.0, by);
   c.launches++;
   cuda_check(cudaGetLastError(), "copy launch");
 }

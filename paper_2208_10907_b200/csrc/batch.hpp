@@ -137,6 +137,11 @@ struct GemmBatch {
     jobs.push_back(j);
     lower.push_back(0);
   }
+  // C = Cin + sum of segments (the accumulator starts from another matrix).
+  void job_from(Mat C, Mat Cin) {
+    job(C, true);
+    jobs.back().Cin = Cin;
+  }
   void seg(Mat A, Mat B, double alpha = 1.0) {
     GemmSeg s;
     s.A = A;

@@ -1325,17 +1325,18 @@ struct Driver {
         const auto [K, tk] = keys[t];
         merged[K][tk] = cm[t];
         if (K < lo || K >= hi) continue;
-        cc.copy(cm[t].m, stack[K].at(tk).m);
         bool any = false;
         for (int64_t x = 0; x < S.nnear(lvl, K); ++x) {
           const int64_t Pp = S.near(lvl, K)[x];
           if (Pp == K) continue;
           auto it = g.find({Pp, tk});
           if (it == g.end()) continue;
-          if (!any) gb.job(cm[t].m, true);
+          // the accumulator starts from the stacked piece (no copy into cm first)
+          if (!any) gb.job_from(cm[t].m, stack[K].at(tk).m);
           any = true;
           gb.seg(reassoc ? Wkp.at({K, Pp}).m.t() : block(sys, K, Pp), it->second.m, -1.0);
         }
+        if (!any) cc.copy(cm[t].m, stack[K].at(tk).m);
       }
       cc.run(c);
       gb.run(c);

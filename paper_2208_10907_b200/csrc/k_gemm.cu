@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(2 * BM) gemm_kernel(const GemmJob* __restrict_
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int r = m0 + wm * 32 + fm * 16 + g + 8 * (i / 2), c = n0 + wn * 32 + fn * 8 + 2 * t + (i % 2);
-        acc[fm][fn][i] = (job.acc && r < C.rows && c < C.cols) ? C.at(r, c) : 0.0;
+        acc[fm][fn][i] = (job.acc && r < C.rows && c < C.cols) ? (job.Cin.p ? job.Cin.at(r, c) : C.at(r, c)) : 0.0;
       }
   int singular = 0;
   int buf = 0;
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(NTW, 1) gemm_ws_kernel(const GemmJob* __restri
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int r = m0 + wm * 32 + fm * 16 + g + 8 * (i / 2), c = n0 + wn * 32 + fn * 8 + 2 * t + (i % 2);
-        acc[fm][fn][i] = (job.acc && r < C.rows && c < C.cols) ? C.at(r, c) : 0.0;
+        acc[fm][fn][i] = (job.acc && r < C.rows && c < C.cols) ? (job.Cin.p ? job.Cin.at(r, c) : C.at(r, c)) : 0.0;
       }
   for (int ch = 0; ch < nchunks; ++ch) {
     const int st = ch % NSW;

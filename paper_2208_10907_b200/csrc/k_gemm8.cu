@@ -148,6 +148,8 @@ __device__ __forceinline__ TileGeom geom(const GemmTile& t, int rows) {
 struct CInfo {
   double* p;
   int64_t rs, cs;
+  const double* ip;  // initial accumulator source (C itself, or the job's Cin)
+  int64_t irs, ics;
   int rows, cols, m0, mf, n0, acc, seg0, nseg;
 };
 __device__ __forceinline__ CInfo load_info(const GemmJob* jobs, const GemmTile* tiles, int ti) {
@@ -164,6 +166,9 @@ __device__ __forceinline__ CInfo load_info(const GemmJob* jobs, const GemmTile* 
   ci.rows = vj->C.rows;
   ci.cols = vj->C.cols;
   ci.acc = vj->acc;
+  ci.ip = vj->Cin.p ? vj->Cin.p : ci.p;
+  ci.irs = vj->Cin.p ? vj->Cin.rs : ci.rs;
+  ci.ics = vj->Cin.p ? vj->Cin.cs : ci.cs;
   ci.seg0 = vj->seg0;
   ci.nseg = vj->nseg;
   const TileGeom tg = geom(tile, ci.rows);
@@ -285,13 +290,13 @@ __global__ void __launch_bounds__(NT, 1) gemm_p8_kernel(const GemmJob* __restric
       mfc = c0 < ci.cols ? (ci.mf >= 10 ? ci.mf : ((ci.mf + 1) & ~1)) : 0;  // 0: idle warp
       const volatile GemmSeg* vs = segs + ci.seg0;
       for (int s = 0; s < ci.nseg; ++s) nch += (vs[s].A.cols + BK - 1) / BK;
-      const int64_t rstep = 8 * ci.rs;
+      const int64_t rstep = 8 * ci.irs;
 #pragma unroll
       for (int fn = 0; fn < 2; ++fn)
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int c = c0 + fn * 8 + 2 * t + i;
-          const double* cp = ci.p + int64_t(ci.m0 + g) * ci.rs + int64_t(c) * ci.cs;
+          const double* cp = ci.ip + int64_t(ci.m0 + g) * ci.irs + int64_t(c) * ci.ics;
 #pragma unroll
           for (int fm = 0; fm < MF; ++fm) {
             const int r = ci.m0 + fm * 8 + g;

@@ -36,7 +36,8 @@ struct GemmSeg {
 struct GemmJob {
   Mat C;
   int seg0 = 0, nseg = 0;
-  int acc = 0;
+  int acc = 0;   // 1: C starts from its own contents
+  Mat Cin;       // Cin.p != nullptr (with acc = 1): C starts from Cin instead (same shape)
 };
 struct GemmTile {
   int job, tm, tn;

@@ -252,7 +252,10 @@ def test_nested_transfer_column_members_match_evaluated_ones(monkeypatch):
     def run():
         p = h2.Problem()
         p.set_kernel("yukawa", 1.0, 1.0, 1e-3)
-        p.set_options(tol=1e-6, cap=100, qr_mode="compressed", reference_compat=False)
+        # leaf 128 with cap 100 trips the reference's fill-absorption abort at level 4
+        # (ulv.cpp:140-147) in either variant; it is disabled here, the residual is the gate
+        p.set_options(tol=1e-6, cap=100, qr_mode="compressed", reference_compat=False,
+                      abort_residual_factor=1e30)
         p.build(xyz, q, leaf)
         p.factor()
         x = p.solve(b)
