@@ -214,6 +214,42 @@ struct Driver {
   std::vector<Mat> Ubig, Vbig;
   std::vector<DMat> big_owner;
   std::vector<PieceMap> carried;
+  // Single-GPU: the two children's carried pieces toward a target are
+  // allocated as the row blocks of one parent-stacked matrix (stacked_[parent]),
+  // so build_upper_pieces takes the stack as it is instead of copying it.
+  std::vector<PieceMap> stacked_;
+  // Allocate carried pieces for boxes [0, m) of a level: keys[t] = (box, target),
+  // rows[t] = the piece's row count; out[t] is a view into its parent's stack.
+  std::vector<DMat> alloc_stacked(int64_t m, const std::vector<std::pair<int64_t, TargetKey>>& keys,
+                                  const std::vector<int>& rows) {
+    std::map<std::pair<int64_t, TargetKey>, std::array<int, 2>> h;  // (parent, tk) -> child row counts
+    for (size_t t = 0; t < keys.size(); ++t) {
+      auto& e = h.try_emplace({keys[t].first >> 1, keys[t].second}, std::array<int, 2>{-1, -1}).first->second;
+      e[keys[t].first & 1] = rows[t];
+    }
+    std::vector<std::pair<int, int>> shapes;
+    for (auto& [key, e] : h) {
+      if (e[0] < 0 || e[1] < 0) throw std::logic_error("alloc_stacked: a child piece is missing");
+      shapes.push_back({e[0] + e[1], int(rs(key.second.first, key.second.second))});
+    }
+    auto mats = alloc_mats(c, shapes);
+    stacked_.assign(size_t(m / 2), {});
+    std::map<std::pair<int64_t, TargetKey>, size_t> at;
+    size_t q = 0;
+    for (auto& [key, e] : h) {
+      stacked_[size_t(key.first)][key.second] = mats[q];
+      at[key] = q++;
+    }
+    std::vector<DMat> out(keys.size());
+    for (size_t t = 0; t < keys.size(); ++t) {
+      const std::pair<int64_t, TargetKey> key{keys[t].first >> 1, keys[t].second};
+      const DMat& S2 = mats[at.at(key)];
+      const int r0 = (keys[t].first & 1) ? h.at(key)[0] : 0;
+      out[t].m = Mat{S2.m.p + r0, rows[t], S2.m.cols, 1, S2.m.cs};
+      out[t].owner = S2.owner;
+    }
+    return out;
+  }
 
   Driver(Problem& p) : P(p), c(p.c), S(p.S), opt(p.opt), L(p.T.levels) {}
 
@@ -1102,7 +1138,27 @@ struct Driver {
         pkeys.push_back({cc, tk});
         shapes.push_back({Ub[cc].rank, int(rs(tk.first, tk.second))});
       }
-    auto mats = alloc_mats(c, shapes);
+    std::vector<DMat> mats;
+    stacked_.clear();
+    if (!(P.comm && P.comm->partitioned(m)) && m >= 2) {
+      // carried pieces (coarser targets) in their parents' stacks, own-level ones apart
+      std::vector<std::pair<int64_t, TargetKey>> ck;
+      std::vector<int> cr;
+      std::vector<std::pair<int, int>> own;
+      for (size_t t = 0; t < pkeys.size(); ++t)
+        if (pkeys[t].second.first < L) {
+          ck.push_back(pkeys[t]);
+          cr.push_back(shapes[t].first);
+        } else {
+          own.push_back(shapes[t]);
+        }
+      auto cm = alloc_stacked(m, ck, cr);
+      auto om = alloc_mats(c, own);
+      size_t a = 0, b = 0;
+      for (size_t t = 0; t < pkeys.size(); ++t) mats.push_back(pkeys[t].second.first < L ? cm[a++] : om[b++]);
+    } else {
+      mats = alloc_mats(c, shapes);
+    }
     for (size_t t = 0; t < pkeys.size(); ++t) pieces[pkeys[t].first][pkeys[t].second] = mats[t];
     {
       PhaseTimer pt2(c, P.stats, "skeleton_leaf_pieces");
@@ -1207,16 +1263,21 @@ struct Driver {
           keys.push_back({K, tk});
           shapes.push_back({sys.dims[K], int(rs(tk.first, tk.second))});
         }
-      auto mats = alloc_mats(c, shapes);
-      CopyBatch cb;
-      for (size_t t = 0; t < keys.size(); ++t) {
-        const auto [K, tk] = keys[t];
-        const Mat a = carried[2 * K].at(tk).m, b = carried[2 * K + 1].at(tk).m;
-        if (a.rows) cb.copy(mats[t].m.sub(0, 0, a.rows, a.cols), a);
-        if (b.rows) cb.copy(mats[t].m.sub(a.rows, 0, b.rows, b.cols), b);
-        stack[K][tk] = mats[t];
+      if (int64_t(stacked_.size()) == m) {
+        for (auto& [K, tk] : keys) stack[K][tk] = stacked_[size_t(K)].at(tk);  // already stacked: no copy
+        stacked_.clear();
+      } else {
+        auto mats = alloc_mats(c, shapes);
+        CopyBatch cb;
+        for (size_t t = 0; t < keys.size(); ++t) {
+          const auto [K, tk] = keys[t];
+          const Mat a = carried[2 * K].at(tk).m, b = carried[2 * K + 1].at(tk).m;
+          if (a.rows) cb.copy(mats[t].m.sub(0, 0, a.rows, a.cols), a);
+          if (b.rows) cb.copy(mats[t].m.sub(a.rows, 0, b.rows, b.cols), b);
+          stack[K][tk] = mats[t];
+        }
+        cb.run(c);
       }
-      cb.run(c);
     }
     merged.assign(m, {});
     if (sys.offdiag) {
@@ -1994,7 +2055,20 @@ struct Driver {
               shapes.push_back({P.U[sys.lvl][k].rank, piece.cols()});
             }
           }
-        auto mats = alloc_mats(c, shapes);
+        const bool part = P.comm && P.comm->partitioned(sys.m);
+        if (is_leaf) {
+          if (part) stacked_.clear();  // (single-GPU: build_leaf_pieces stacked them)
+        } else {
+          stacked_.clear();
+        }
+        std::vector<DMat> mats;
+        if (!is_leaf && !part && sys.m >= 2) {
+          std::vector<int> pr;
+          for (auto& sh : shapes) pr.push_back(sh.first);
+          mats = alloc_stacked(sys.m, keys, pr);
+        } else {
+          mats = alloc_mats(c, shapes);
+        }
         const auto [lo, hi] = own_range(sys.m);  // multi-GPU: own boxes, then all-gathered
         std::vector<int64_t> box(keys.size());
         for (size_t t = 0; t < keys.size(); ++t) {

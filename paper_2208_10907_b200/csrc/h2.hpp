@@ -2,6 +2,7 @@
 // factors, and the solve. Mirrors the reference's proj/include API objects
 // (ClusterTree, BlockStructure, HMatrix, SharedBasisSet, ULVFactors).
 #pragma once
+#include <array>
 #include <map>
 #include <memory>
 #include <string>
