@@ -1282,71 +1282,13 @@ struct Driver {
     merged.assign(m, {});
     if (sys.offdiag) {
       // g(P, tk) = A_PP^-1 (stack[P][tk] with P's near columns zeroed), shared across K.
-      std::map<std::pair<int64_t, TargetKey>, DMat> g;
-      std::vector<std::pair<int64_t, TargetKey>> need;
       // Multi-GPU: corrected pieces of this rank's boxes only (all-gathered
       // below); the g's they need may belong to neighbours (recomputed).
       const auto [lo, hi] = own_range(m);
-      for (int64_t K = lo; K < hi; ++K)
-        for (int64_t x = 0; x < S.nnear(lvl, K); ++x) {
-          const int64_t Pp = S.near(lvl, K)[x];
-          if (Pp == K) continue;
-          for (auto& [tk, piece] : stack[K]) {
-            if (opt.reference_compat ? !stack[Pp].count(tk) : overlapping(stack[Pp], tk).empty())
-              continue;
-            need.push_back({Pp, tk});
-          }
-        }
-      std::sort(need.begin(), need.end());
-      need.erase(std::unique(need.begin(), need.end()), need.end());
-      std::vector<std::pair<int, int>> shapes;
-      std::vector<std::pair<int64_t, TargetKey>> gkeys;
-      std::vector<std::vector<int2>> gmasks;
-      for (auto& [Pp, tk] : need) {
-        const int64_t jb = rb(tk.first, tk.second), je = jb + rs(tk.first, tk.second);
-        bool all_zero;
-        auto mask = mask_for(lvl, Pp, jb, je, all_zero);
-        if (all_zero) continue;
-        gkeys.push_back({Pp, tk});
-        gmasks.push_back(mask);
-        shapes.push_back({sys.dims[Pp], int(je - jb)});
-      }
-      auto mats = alloc_mats(c, shapes);
       // Tolerance-parity mode: reassociate A_KP (A_PP^-1 S_P) as (A_KP A_PP^-1) S_P,
       // with W_KP = A_KP A_PP^-1 formed once per near pair, so the wide
       // A_PP^-1 S_P products are never formed (g then holds the masked S_P).
       const bool reassoc = c.fast_solve;
-      CopyBatch cb, zb;
-      SolveBatch sb;
-      for (size_t t = 0; t < gkeys.size(); ++t) {
-        const auto [Pp, tk] = gkeys[t];
-        if (opt.reference_compat) {
-          cb.copy(mats[t].m, stack[Pp].at(tk).m);
-        } else {
-          // P's content over J's columns from every target of P overlapping J
-          // (oracle/fix_reference.py fix 3); the rest are P's near columns.
-          zb.zero(mats[t].m);
-          for (auto& o : overlapping(stack[Pp], tk))
-            cb.copy(mats[t].m.sub(0, o.dst, mats[t].rows(), o.len),
-                    stack[Pp].at(o.tk).m.sub(0, o.src, mats[t].rows(), o.len));
-        }
-        if (opt.reference_compat)
-          for (auto& r : gmasks[t]) zb.zero(mats[t].m.sub(0, r.x, mats[t].rows(), r.y - r.x));
-        if (!reassoc) sb.add(sys.diag_lu[Pp], mats[t].m, SOLVE_FULL);
-        g[gkeys[t]] = mats[t];
-      }
-      if (opt.reference_compat) {
-        cb.run(c);
-        zb.run(c);
-      } else {
-        zb.run(c);  // zero-fill first, then the overlapping slices, then the masks
-        cb.run(c);
-        CopyBatch mz;
-        for (size_t t = 0; t < gkeys.size(); ++t)
-          for (auto& r : gmasks[t]) mz.zero(mats[t].m.sub(0, r.x, mats[t].rows(), r.y - r.x));
-        mz.run(c);
-      }
-      sb.run(c);
       std::map<std::pair<int64_t, int64_t>, DMat> Wkp;
       if (reassoc) {
         // W_KP^T = A_PP^-T A_KP^T: one transpose solve per (K, P) near pair.
@@ -1374,33 +1316,116 @@ struct Driver {
       // corrected = stack - sum_P A_KP g(P, tk), accumulated over P in order.
       std::vector<std::pair<int64_t, TargetKey>> keys;
       std::vector<std::pair<int, int>> cshapes;
-      for (int64_t K = 0; K < m; ++K)
+      std::vector<size_t> first_of(size_t(m) + 1, 0);  // keys of box K: [first_of[K], first_of[K + 1])
+      for (int64_t K = 0; K < m; ++K) {
+        first_of[size_t(K)] = keys.size();
         for (auto& [tk, piece] : stack[K]) {
           keys.push_back({K, tk});
           cshapes.push_back({piece.rows(), piece.cols()});
         }
+      }
+      first_of[size_t(m)] = keys.size();
       auto cm = alloc_mats(c, cshapes);
-      CopyBatch cc;
-      GemmBatch gb;
-      for (size_t t = 0; t < keys.size(); ++t) {
-        const auto [K, tk] = keys[t];
-        merged[K][tk] = cm[t];
-        if (K < lo || K >= hi) continue;
-        bool any = false;
+      for (size_t t = 0; t < keys.size(); ++t) merged[keys[t].first][keys[t].second] = cm[t];
+      // Boxes are processed in chunks so that the g's alive at once stay within
+      // a third of the free memory (they are as large as a whole piece set).
+      size_t fr = 0, tot = 0;
+      cuda_check(cudaMemGetInfo(&fr, &tot), "meminfo");
+      const size_t budget = std::max<size_t>(size_t(1) << 28, fr / 3);
+      auto needed_by = [&](int64_t K, std::vector<std::pair<int64_t, TargetKey>>& out) {
         for (int64_t x = 0; x < S.nnear(lvl, K); ++x) {
           const int64_t Pp = S.near(lvl, K)[x];
           if (Pp == K) continue;
-          auto it = g.find({Pp, tk});
-          if (it == g.end()) continue;
-          // the accumulator starts from the stacked piece (no copy into cm first)
-          if (!any) gb.job_from(cm[t].m, stack[K].at(tk).m);
-          any = true;
-          gb.seg(reassoc ? Wkp.at({K, Pp}).m.t() : block(sys, K, Pp), it->second.m, -1.0);
+          for (auto& [tk, piece] : stack[K]) {
+            if (opt.reference_compat ? !stack[Pp].count(tk) : overlapping(stack[Pp], tk).empty())
+              continue;
+            out.push_back({Pp, tk});
+          }
         }
-        if (!any) cc.copy(cm[t].m, stack[K].at(tk).m);
+      };
+      int64_t K0 = lo;
+      while (K0 < hi) {
+        std::set<std::pair<int64_t, TargetKey>> needset;
+        size_t bytes = 0;
+        int64_t K1 = K0;
+        while (K1 < hi) {
+          std::vector<std::pair<int64_t, TargetKey>> nk;
+          needed_by(K1, nk);
+          size_t add = 0;
+          for (auto& key : nk)
+            if (!needset.count(key))
+              add += sizeof(double) * size_t(sys.dims[key.first]) * size_t(rs(key.second.first, key.second.second));
+          if (K1 > K0 && bytes + add > budget) break;
+          for (auto& key : nk) needset.insert(key);
+          bytes += add;
+          ++K1;
+        }
+        std::map<std::pair<int64_t, TargetKey>, DMat> g;
+        std::vector<std::pair<int, int>> shapes;
+        std::vector<std::pair<int64_t, TargetKey>> gkeys;
+        std::vector<std::vector<int2>> gmasks;
+        for (auto& [Pp, tk] : needset) {
+          const int64_t jb = rb(tk.first, tk.second), je = jb + rs(tk.first, tk.second);
+          bool all_zero;
+          auto mask = mask_for(lvl, Pp, jb, je, all_zero);
+          if (all_zero) continue;
+          gkeys.push_back({Pp, tk});
+          gmasks.push_back(mask);
+          shapes.push_back({sys.dims[Pp], int(je - jb)});
+        }
+        auto mats = alloc_mats(c, shapes);
+        CopyBatch cb, zb;
+        SolveBatch sb;
+        for (size_t t = 0; t < gkeys.size(); ++t) {
+          const auto [Pp, tk] = gkeys[t];
+          if (opt.reference_compat) {
+            cb.copy(mats[t].m, stack[Pp].at(tk).m);
+          } else {
+            // P's content over J's columns from every target of P overlapping J
+            // (oracle/fix_reference.py fix 3); the rest are P's near columns.
+            zb.zero(mats[t].m);
+            for (auto& o : overlapping(stack[Pp], tk))
+              cb.copy(mats[t].m.sub(0, o.dst, mats[t].rows(), o.len),
+                      stack[Pp].at(o.tk).m.sub(0, o.src, mats[t].rows(), o.len));
+          }
+          if (opt.reference_compat)
+            for (auto& r : gmasks[t]) zb.zero(mats[t].m.sub(0, r.x, mats[t].rows(), r.y - r.x));
+          if (!reassoc) sb.add(sys.diag_lu[Pp], mats[t].m, SOLVE_FULL);
+          g[gkeys[t]] = mats[t];
+        }
+        if (opt.reference_compat) {
+          cb.run(c);
+          zb.run(c);
+        } else {
+          zb.run(c);  // zero-fill first, then the overlapping slices, then the masks
+          cb.run(c);
+          CopyBatch mz;
+          for (size_t t = 0; t < gkeys.size(); ++t)
+            for (auto& r : gmasks[t]) mz.zero(mats[t].m.sub(0, r.x, mats[t].rows(), r.y - r.x));
+          mz.run(c);
+        }
+        sb.run(c);
+        CopyBatch cc;
+        GemmBatch gb;
+        for (size_t t = first_of[size_t(K0)]; t < first_of[size_t(K1)]; ++t) {
+          const auto [K, tk] = keys[t];
+          bool any = false;
+          for (int64_t x = 0; x < S.nnear(lvl, K); ++x) {
+            const int64_t Pp = S.near(lvl, K)[x];
+            if (Pp == K) continue;
+            auto it = g.find({Pp, tk});
+            if (it == g.end()) continue;
+            // the accumulator starts from the stacked piece (no copy into cm first)
+            if (!any) gb.job_from(cm[t].m, stack[K].at(tk).m);
+            any = true;
+            gb.seg(reassoc ? Wkp.at({K, Pp}).m.t() : block(sys, K, Pp), it->second.m, -1.0);
+          }
+          if (!any) cc.copy(cm[t].m, stack[K].at(tk).m);
+        }
+        cc.run(c);
+        gb.run(c);
+        K0 = K1;  // this chunk's g's are released stream-ordered behind its GEMMs
       }
-      cc.run(c);
-      gb.run(c);
       std::vector<int64_t> box(keys.size());
       for (size_t t = 0; t < keys.size(); ++t) box[t] = keys[t].first;
       exchange_mats(cm, box, m);
