@@ -263,6 +263,7 @@ void GemmBatch::run(Ctx& c, int tag) {
   const int2* dmask = upload(c, masks, k4);
   for (size_t s = 0; s < segs.size(); ++s)
     if (segs[s].gen && seg_mask_off[s] >= 0) segs[s].g.mask = dmask + seg_mask_off[s];
+  for (size_t j = 0; j < jobs.size(); ++j) jobs[j].lower = lower[j] ? 1 : 0;
   const GemmJob* dj = upload(c, jobs, k1);
   const GemmSeg* ds = upload(c, segs, k2);
   const GemmTile* dt = upload(c, tiles, k3);

@@ -146,6 +146,7 @@ __device__ __forceinline__ TileGeom geom(const GemmTile& t, int rows) {
 // What a consumer needs of its tile, read through volatile pointers so that a
 // second call re-loads instead of keeping the first one's registers alive.
 struct CInfo {
+  int lower;
   double* p;
   int64_t rs, cs;
   const double* ip;  // initial accumulator source (C itself, or the job's Cin)
@@ -166,6 +167,7 @@ __device__ __forceinline__ CInfo load_info(const GemmJob* jobs, const GemmTile* 
   ci.rows = vj->C.rows;
   ci.cols = vj->C.cols;
   ci.acc = vj->acc;
+  ci.lower = vj->lower;
   ci.ip = vj->Cin.p ? vj->Cin.p : ci.p;
   ci.irs = vj->Cin.p ? vj->Cin.rs : ci.rs;
   ci.ics = vj->Cin.p ? vj->Cin.cs : ci.cs;
@@ -176,6 +178,20 @@ __device__ __forceinline__ CInfo load_info(const GemmJob* jobs, const GemmTile* 
   ci.mf = tg.mf;
   ci.n0 = tg.n0;
   return ci;
+}
+
+// A consumer warp's share of its tile: columns [n0 + nb, + 16) and the row
+// fragments it needs. For a symmetric job the fragments entirely above the
+// warp's first column are skipped (returns the number skipped).
+__device__ __forceinline__ int warp_window(CInfo& ci, int nb) {
+  int fs = 0;
+  if (ci.lower) {
+    fs = (ci.n0 + nb - ci.m0) >> 3;
+    fs = fs < 0 ? 0 : (fs > ci.mf ? ci.mf : fs);
+    ci.m0 += 8 * fs;
+    ci.mf -= fs;
+  }
+  return fs;
 }
 
 __global__ void __launch_bounds__(NT, 1) gemm_p8_kernel(const GemmJob* __restrict__ jobs,
@@ -280,14 +296,18 @@ __global__ void __launch_bounds__(NT, 1) gemm_p8_kernel(const GemmJob* __restric
   // else, so nothing about the tile stays live across the chunk loop: the
   // epilogue re-reads the descriptors (volatile loads, a few L2 hits per tile).
   const int g = lane >> 2, t = lane & 3;
-  const int nb = warp * 16;  // this warp's columns within the tile
+  // Column group of the warp: warps w and w + 4 share a scheduler, and in a
+  // symmetric tile the work falls with the column index, so the second four
+  // take the groups in reverse (group s and 7 - s per scheduler).
+  const int nb = 16 * (warp < 4 ? warp : 11 - warp);
   for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
     double acc[MF][2][2];
-    int nch = 0, mfc = 0;
+    int nch = 0, mfc = 0, fskip = 0;
     {
-      const CInfo ci = load_info(jobs, tiles, ti);
+      CInfo ci = load_info(jobs, tiles, ti);
+      fskip = warp_window(ci, nb);
       const int c0 = ci.n0 + nb;
-      mfc = c0 < ci.cols ? (ci.mf >= 10 ? ci.mf : ((ci.mf + 1) & ~1)) : 0;  // 0: idle warp
+      mfc = (c0 < ci.cols && ci.mf > 0) ? (ci.mf >= 10 ? ci.mf : ((ci.mf + 1) & ~1)) : 0;  // 0: idle warp
       const volatile GemmSeg* vs = segs + ci.seg0;
       for (int s = 0; s < ci.nseg; ++s) nch += (vs[s].A.cols + BK - 1) / BK;
       const int64_t rstep = 8 * ci.irs;
@@ -311,7 +331,7 @@ __global__ void __launch_bounds__(NT, 1) gemm_p8_kernel(const GemmJob* __restric
         const Meta me = sm.meta[st];
         const unsigned sAm = me.a_kmajor ? SK : 1, sAk = me.a_kmajor ? 1 : SAM;
         const unsigned sBn = me.b_kmajor ? SK : 1, sBk = me.b_kmajor ? 1 : SBN;
-        const unsigned ap = su32(sm.A[st]) + 8 * (g * sAm + t * sAk);
+        const unsigned ap = su32(sm.A[st]) + 8 * ((g + 8 * fskip) * sAm + t * sAk);
         const unsigned bp = su32(sm.B[st]) + 8 * ((nb + g) * sBn + t * sBk);
         const unsigned sAm8 = 64 * sAm, sAk4 = 32 * sAk, sBn8 = 64 * sBn, sBk4 = 32 * sBk;
         switch (mfc) {
@@ -329,7 +349,8 @@ __global__ void __launch_bounds__(NT, 1) gemm_p8_kernel(const GemmJob* __restric
       if (lane == 0) mb_arrive(&sm.empty[st]);
     }
     if (mfc > 0) {
-      const CInfo ci = load_info(jobs, tiles, ti);
+      CInfo ci = load_info(jobs, tiles, ti);
+      warp_window(ci, nb);
       const int c0 = ci.n0 + nb;
       const int64_t rstep = 8 * ci.rs;
 #pragma unroll

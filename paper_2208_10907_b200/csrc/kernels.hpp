@@ -38,6 +38,7 @@ struct GemmJob {
   int seg0 = 0, nseg = 0;
   int acc = 0;   // 1: C starts from its own contents
   Mat Cin;       // Cin.p != nullptr (with acc = 1): C starts from Cin instead (same shape)
+  int lower = 0; // symmetric C: only entries on or below the diagonal are needed
 };
 struct GemmTile {
   int job, tm, tn;
