@@ -19,6 +19,7 @@ if warm:
     w.build(xyz, q, 256)
     w.factor()
     w.close()
+    print('=== main run', file=sys.stderr, flush=True)
 p = h2.Problem()
 p.set_kernel("yukawa", 1.0, 1.0, 1e-3)
 p.set_options(tol=1e-6, cap=100, qr_mode=MODE, reference_compat=COMPAT)
