@@ -72,6 +72,13 @@ int h2g_set_options(h2g_problem* p, const h2g_options* o);
  * reference's members, the default); otherwise >= 64. Parity by tolerance. */
 int h2g_set_sampling(h2g_problem* p, int64_t sample_cols);
 
+/* Device memory (no reference counterpart): blocks come from a process-wide arena
+ * carved out of a few large cudaMalloc'd segments (the first one
+ * H2G_ARENA_FRACTION, default 0.7, of the free memory at first use), so a
+ * repeated factorization makes no allocator call in its steady state.
+ * h2g_trim_memory returns every segment that is entirely free to the driver. */
+void h2g_trim_memory(void);
+
 /* build_cluster_tree (geometry.hpp:58) + classify_blocks (hstructure.hpp:55)
  * + materialize_dense (hstructure.hpp:101-103) = Pipeline::build
  * (report.cpp:79-91). xyz is AoS n x 3, q has n charges. */

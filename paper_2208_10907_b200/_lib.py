@@ -41,7 +41,7 @@ EXPORTS = [
     "h2g_nccl_unique_id", "h2g_comm_nccl", "h2g_comm_host", "h2g_comm_destroy", "h2g_set_comm",
     "h2g_partition_range", "h2g_kernel_evals", "h2g_generate_points", "h2g_points_last_error",
     "h2g_exp_glibc_host", "h2g_level_dims", "h2g_level_block", "h2g_level_lu", "h2g_level_elim",
-    "h2g_assemble_block", "h2g_set_sampling",
+    "h2g_assemble_block", "h2g_set_sampling", "h2g_trim_memory",
 ]
 
 # h2g_host_allgather_fn (include/h2g.h)
@@ -67,6 +67,8 @@ def lib():
         L.h2g_set_kernel.argtypes = [P, ctypes.POINTER(Kernel)]
         L.h2g_set_options.argtypes = [P, ctypes.POINTER(Options)]
         L.h2g_set_sampling.argtypes = [P, i64]
+        L.h2g_trim_memory.argtypes = []
+        L.h2g_trim_memory.restype = None
         L.h2g_build.argtypes = [P, i64, P, P, i64]
         L.h2g_build_dev.argtypes = [P, i64, P, P, i64]
         L.h2g_factor.argtypes = [P]
@@ -442,6 +444,11 @@ def gemm(a, b, alpha=1.0, transa=False, transb=False, c=None):
     out = np.array(c, dtype=np.float64, order="F") if acc else np.zeros((m, n), order="F")
     _check(lib().h2g_gemm(m, n, k, alpha, _p(a), int(transa), _p(b), int(transb), int(acc), _p(out)))
     return out
+
+
+def trim_memory():
+    """h2g_trim_memory: return the arena's entirely free segments to the driver."""
+    lib().h2g_trim_memory()
 
 
 GEOMETRIES = {"cube": 0, "line": 1, "sphere": 2, "uniform_sphere": 3, "ellipsoids": 4}

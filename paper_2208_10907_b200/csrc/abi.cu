@@ -130,6 +130,8 @@ int h2g_set_sampling(h2g_problem* p, int64_t sample_cols) {
   });
 }
 
+void h2g_trim_memory(void) { h2g::trim_device_memory(); }
+
 int h2g_build_dev(h2g_problem* p, int64_t n, const double* d_xyz, const double* d_q, int64_t leaf) {
   return guarded([&] { p->P.build(d_xyz, d_q, n, leaf); });
 }

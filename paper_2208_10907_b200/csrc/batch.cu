@@ -31,23 +31,39 @@ void smem_attr(const void* kernel, size_t bytes, const char* what) {
   have = bytes;
 }
 
+size_t Ctx::free_bytes() const {
+  size_t fr = 0, tot = 0;
+  cuda_check(cudaMemGetInfo(&fr, &tot), "meminfo");
+  return fr + arena_free_bytes();
+}
+
+// Device blocks come from the arena (arena.cu); H2G_NO_ARENA=1 goes back to
+// the stream-ordered allocator.
 Slab Ctx::alloc(size_t bytes) {
   void* p = nullptr;
   if (bytes == 0) bytes = 8;
   bytes = (bytes + 255) & ~size_t(255);
   static const bool hp = getenv("H2G_HOST_PROF") != nullptr;
   const auto t0 = hp ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point{};
-  cudaError_t e = cudaMallocAsync(&p, bytes, stream);
+  cudaStream_t s = stream;
+  if (use_arena) {
+    p = arena_alloc(bytes, s);
+    if (!p)
+      throw std::runtime_error("device memory exhausted allocating " + std::to_string(bytes) +
+                               " bytes in phase " + phase + ": out of memory");
+  } else {
+    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw std::runtime_error("device memory exhausted allocating " + std::to_string(bytes) +
+                               " bytes in phase " + phase + ": " + cudaGetErrorString(e));
+    }
+  }
   if (hp) {
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (ms > 2.0) fprintf(stderr, "HOSTALLOC %.1f ms for %.3f GB in phase %s\n", ms, bytes / 1e9, phase.c_str());
   }
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    throw std::runtime_error("device memory exhausted allocating " + std::to_string(bytes) +
-                             " bytes in phase " + phase + ": " + cudaGetErrorString(e));
-  }
-  cudaStream_t s = stream;
+  if (use_arena) return Slab(p, [s](void* q) { arena_free(q, s); });
   return Slab(p, [s](void* q) { cudaFreeAsync(q, s); });
 }
 

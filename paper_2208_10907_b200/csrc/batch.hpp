@@ -23,6 +23,14 @@ void smem_attr(const void* kernel, size_t bytes, const char* what);
 
 using Slab = std::shared_ptr<void>;
 
+// Device memory arena (arena.cu): best-fit blocks carved from a few large
+// cudaMalloc'd segments; stream-ordered reuse on the releasing stream.
+void* arena_alloc(size_t bytes, cudaStream_t st);  // nullptr when the device is exhausted
+void arena_free(void* p, cudaStream_t st);
+void arena_stream_gone(cudaStream_t st);  // the stream was synchronised and is being retired
+size_t arena_free_bytes();
+void trim_device_memory();  // give entirely free segments back to the driver
+
 struct Ctx {
   cudaStream_t stream = nullptr;
   ErrWord* err = nullptr;  // device
@@ -39,6 +47,11 @@ struct Ctx {
     phase_flops[phase] += f;
   }
   Slab alloc(size_t bytes);
+  // Free device memory as the chunking budgets should see it: the driver's, plus the arena's free blocks.
+  size_t free_bytes() const;
+  // Blocks from the arena (default) or from cudaMallocAsync (H2G_NO_ARENA=1, and
+  // factorizations that need most of the device: Problem::factor decides).
+  bool use_arena = getenv("H2G_NO_ARENA") == nullptr;
   // Pinned staging arena for descriptor uploads: a copy from pageable memory
   // larger than a few KB makes cudaMemcpyAsync wait for the stream, which
   // serialises host preparation with the GPU. Regions are handed out

@@ -89,6 +89,7 @@ Problem::Problem() {
 
 void Problem::use_stream(cudaStream_t s) {
   cuda_check(cudaStreamSynchronize(c.stream), "stream");
+  arena_stream_gone(c.stream);
   if (own_stream_) cudaStreamDestroy(c.stream);
   c.stream = s;
   own_stream_ = false;
@@ -104,8 +105,31 @@ Problem::~Problem() {
   near_slab.reset();
   orig_slab.reset();
   if (c.stream) cudaStreamSynchronize(c.stream);
+  arena_stream_gone(c.stream);  // its released blocks are now usable from any stream
   cudaFree(c.err);
   if (c.stream && own_stream_) cudaStreamDestroy(c.stream);
+}
+
+// Memory regime, decided before a build allocates anything. The arena cannot
+// re-map: a factorization whose piece sets (rank x N per box, three alive at
+// the upper levels) take most of the device needs the driver
+// pool's ability to serve a 50 GB request from scattered free memory. Such
+// problems go back to the stream-ordered allocator (after handing the arena's
+// free segments back to the driver).
+void Problem::choose_allocator(int64_t n, int64_t leaf) {
+  size_t fr = 0, tot = 0;
+  cuda_check(cudaMemGetInfo(&fr, &tot), "meminfo");
+  const double boxes = double(int64_t(1) << tree_levels(n, leaf));
+  const double rank = opt.cap > 0 ? double(opt.cap) : double(leaf);
+  const double piece_set = 8.0 * rank * double(n) * boxes;
+  const bool roomy = 3.5 * piece_set < 0.5 * double(tot);
+  if (c.use_arena && !roomy) {
+    c.use_arena = false;
+    c.sync();
+    trim_device_memory();
+  } else if (!c.use_arena && roomy && getenv("H2G_NO_ARENA") == nullptr) {
+    c.use_arena = true;
+  }
 }
 
 // Pipeline::build (report.cpp:79-91): tree, classification, near field.
@@ -117,6 +141,10 @@ void Problem::build(const double* d_xyz, const double* d_q, int64_t n, int64_t l
   V.clear();
   levels.clear();
   top = LuF{};
+  near.clear();
+  near_slab.reset();
+  orig_slab.reset();
+  if (leaf >= 2 && n >= 2 * leaf) choose_allocator(n, leaf);
   double t0 = now_s();
   DevTimer dt(c.stream);
   build_tree_device(T, d_xyz, d_q, n, leaf, c.stream);
@@ -1026,8 +1054,7 @@ struct Driver {
           if (!all_zero) add_rows(pl, p, 1);
         }
     }
-    size_t fr = 0, tot = 0;
-    cuda_check(cudaMemGetInfo(&fr, &tot), "meminfo");
+    const size_t fr = c.free_bytes();
     const size_t budget = std::max<size_t>(size_t(1) << 28, fr / 3);
     size_t p0 = 0;
     while (p0 < plans.size()) {
@@ -1329,8 +1356,7 @@ struct Driver {
       for (size_t t = 0; t < keys.size(); ++t) merged[keys[t].first][keys[t].second] = cm[t];
       // Boxes are processed in chunks so that the g's alive at once stay within
       // a third of the free memory (they are as large as a whole piece set).
-      size_t fr = 0, tot = 0;
-      cuda_check(cudaMemGetInfo(&fr, &tot), "meminfo");
+      const size_t fr = c.free_bytes();
       const size_t budget = std::max<size_t>(size_t(1) << 28, fr / 3);
       auto needed_by = [&](int64_t K, std::vector<std::pair<int64_t, TargetKey>>& out) {
         for (int64_t x = 0; x < S.nnear(lvl, K); ++x) {
@@ -1499,9 +1525,9 @@ struct Driver {
       }
     }
     if (c.fast_solve && lvl >= 3) {
-      size_t need = 0, fr = 0, tot = 0;
+      size_t need = 0;
       for (int64_t k = 0; k < m; ++k) need += sizeof(double) * size_t(sys.dims[k]) * size_t(anc_w[k]);
-      cuda_check(cudaMemGetInfo(&fr, &tot), "meminfo");
+      const size_t fr = c.free_bytes();
       if (need < fr / 4) {
         std::vector<std::pair<int, int>> ks;
         for (int64_t k = 0; k < m; ++k) ks.push_back({sys.dims[k], anc_w[k]});
@@ -2139,8 +2165,7 @@ void Problem::factor() {
   const double t0 = now_s();
   DevTimer dt(c.stream);
   if (auto_budget_) {
-    size_t fr = 0, tot = 0;
-    cuda_check(cudaMemGetInfo(&fr, &tot), "meminfo");
+    const size_t fr = c.free_bytes();
     opt.qr_mem_budget = std::max<size_t>(size_t(1) << 28, fr / 3);
   }
   c.phase_flops.clear();

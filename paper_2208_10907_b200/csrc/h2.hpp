@@ -114,6 +114,7 @@ class Problem {
   void use_stream(cudaStream_t s);
   bool own_stream_ = true;
   void build(const double* d_xyz, const double* d_q, int64_t n, int64_t leaf);  // device inputs
+  void choose_allocator(int64_t n, int64_t leaf);  // arena or stream-ordered pool, by predicted footprint
   void factor();
   // b and x: device, n x nrhs column-major, ORIGINAL point order.
   void solve(const double* d_b, double* d_x, int nrhs);

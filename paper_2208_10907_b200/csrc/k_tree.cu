@@ -538,8 +538,13 @@ void classify_device(DeviceTree& T, double eta, int weak, Structure& S, cudaStre
 namespace h2g {
 
 void DeviceTree::alloc(int64_t n_, int64_t nodes) {
+  // A rebuild of the same size (every step of a factorization sequence) keeps
+  // its buffers: 21 cudaFree + cudaMalloc pairs would each synchronise the device.
+  if (!owned.empty() && alloc_n == n_ && alloc_nodes == nodes) return;
   for (void* p : owned) cudaFree(p);
   owned.clear();
+  alloc_n = n_;
+  alloc_nodes = nodes;
   auto get = [&](size_t bytes) {
     void* p = nullptr;
     check(cudaMalloc(&p, bytes < 8 ? 8 : bytes), "tree alloc");

@@ -24,6 +24,7 @@ struct DeviceTree {
   double *margin = nullptr, *key0 = nullptr, *key1 = nullptr;
   int *idx0 = nullptr, *idx1 = nullptr, *node_of = nullptr, *flag = nullptr;
   std::vector<void*> owned;
+  int64_t alloc_n = -1, alloc_nodes = -1;  // sizes the buffers were allocated for
 
   void alloc(int64_t n_, int64_t nodes);
   void release_scratch();
