@@ -609,6 +609,10 @@ int qrb_cluster_size(int njobs, int typ_n, int max_m, int max_nmem) {
   int best = 1;
   double best_cost = 1e30;
   const int nblk = std::max(1, (typ_n + CB - 1) / CB);
+  if (const char* e = getenv("H2G_QRB_CLUSTER")) {  // experiment override
+    const int g = atoi(e);
+    if (g >= 1 && g <= 8) return std::min(g, std::max(1, nblk));
+  }
   for (int g = 1; g <= 8; ++g) {
     if (g > 1 && g > nblk) break;
     int fit = 0;
