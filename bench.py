@@ -1,18 +1,25 @@
 #!/usr/bin/env python
 """Benchmark of the B200 H2-ULV hot path (build -> factorize -> solve).
 
-Workload (BASELINE.json configs[1], the largest config that fits one GPU):
-N = 65,536 points on the unit sphere (the reference's Fibonacci-lattice
-generator, geometry.cpp:64-95), Yukawa kernel exp(-r)/(r + 1e-3) (scale 1,
-so the diagonal is 1e3), leaf 256, strong admissibility eta = 1, rank cap
-100, tol 1e-6 (tol 1e-8 with cap 100 makes the reference abort with "basis
-does not absorb fill-in" at leaf 256; measured).
+Workload (BASELINE.json configs[1]): N = 65,536 points on the unit sphere (the
+reference's Fibonacci-lattice generator, geometry.cpp:64-95, bit for bit),
+Yukawa kernel exp(-r)/(r + 1e-3) (scale 1, so the diagonal is 1e3), leaf 256,
+strong admissibility eta = 1, rank cap 100, tol 1e-6 (tol 1e-8 with cap 100
+makes the reference abort with "basis does not absorb fill-in" at leaf 256;
+measured). BASELINE assigns configs[2] and [3] to one GPU as
+well; the reference's algorithm carries O(N^2) pieces, so this implementation
+of it holds at most N = 131,072 on one B200 and configs[1] is
+the largest BASELINE config it can run.
 
-QR mode: compressed by default (each member of a box's basis panel replaced
-by a pivoted-Cholesky factor of its Gram matrix -- same range, same member
-masses -- then the blocked QR; the reference's pivoting/stopping rules on the
-compressed panel; parity within tolerance, tests/test_qr_blocked.py); the
-line's "exact_qr" field times the same step with the bit-exact per-step QR.
+Mode: compressed QR (each member of a box's basis panel replaced by a
+pivoted-Cholesky factor of its Gram matrix -- same range, same member masses --
+then the blocked QR; the reference's pivoting/stopping rules on the compressed
+panel; parity within tolerance, tests/test_qr_blocked.py) and the corrected
+assembly (reference_compat = 0, pinned bit for bit against the corrected
+reference, tests/test_corrected.py). The line's "exact_qr" field times the same
+step with the reference's assembly and the bit-exact per-step QR (bitwise equal
+to the unmodified reference at this size, tests/test_bench_parity.py);
+"sampled_members" times it with sampled far-field basis members.
 
 A step = one pass of the hot path from device-resident points: cluster tree
 + admissibility lists + near-field arena (Pipeline::build), fill-in
