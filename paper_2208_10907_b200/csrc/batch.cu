@@ -425,36 +425,46 @@ std::vector<double> NormBatch::run(Ctx& c) {
   return out;
 }
 
-static void run_blocked_lu(Ctx& c, const LuJob& j, const std::string& name) {
-  const int n = j.A.rows;
-  double fl = 0;
-  for (double k = 0; k < n; ++k) fl += (n - k - 1) + 2.0 * (n - k - 1) * (n - k - 1);
+static void run_blocked_lu(Ctx& c, const std::vector<LuJob>& js, const std::vector<std::string>& names) {
+  double fl = 0, by = 0;
+  int max_n = 1;
+  for (auto& j : js) {
+    const double n = j.A.rows;
+    for (double k = 0; k < n; ++k) fl += (n - k - 1) + 2.0 * (n - k - 1) * (n - k - 1);
+    by += 16.0 * n * n;
+    max_n = std::max(max_n, j.A.rows);
+  }
   c.add_flops(fl);
-  c.lu_names[++c.lu_tag] = {name};
+  c.lu_names[++c.lu_tag] = names;
   const int tag = c.lu_tag;
-  Slab am = c.alloc(sizeof(double));
+  const int nj = int(js.size());
+  Slab am = c.alloc(sizeof(double) * js.size()), k1;
   double* amax = static_cast<double*>(am.get());
+  const LuJob* dj = upload(c, js, k1);
   auto ev = c.prof_begin();
-  launch_lu_amax(j, amax, c.stream);
+  launch_lu_amax(dj, nj, amax, c.stream);
   constexpr int NB = 32;
-  for (int kb = 0; kb < n; kb += NB) {
-    const int nb = std::min(NB, n - kb);
-    launch_lu_panel(j, kb, nb, amax, c.err, tag, c.stream);
-    launch_lu_rows(j, kb, nb, c.stream);
-    const int r = n - kb - nb;
-    if (r > 0) {
-      GemmBatch gb;
-      gb.job(j.A.sub(kb + nb, kb + nb, r, r), true);
-      gb.seg(j.A.sub(kb + nb, kb, r, nb), j.A.sub(kb, kb + nb, nb, r), -1.0);
-      const bool pr = c.prof;
-      c.prof = false;  // the trailing GEMMs are part of this "lu" record
-      gb.run(c, tag);
-      c.prof = pr;
-      c.add_flops(-2.0 * r * double(nb) * r);  // counted once above (reference LU rule)
+  for (int kb = 0; kb < max_n; kb += NB) {
+    const int nb = std::min(NB, max_n - kb);
+    launch_lu_panel(dj, nj, max_n, kb, nb, amax, c.err, tag, c.stream);
+    launch_lu_rows(dj, nj, max_n, kb, nb, c.stream);
+    GemmBatch gb;
+    for (auto& j : js) {
+      const int n = j.A.rows;
+      if (kb >= n) continue;
+      const int nbj = std::min(NB, n - kb), r = n - kb - nbj;
+      if (r <= 0) continue;
+      gb.job(j.A.sub(kb + nbj, kb + nbj, r, r), true);
+      gb.seg(j.A.sub(kb + nbj, kb, r, nbj), j.A.sub(kb, kb + nbj, nbj, r), -1.0);
+      c.add_flops(-2.0 * r * double(nbj) * r);  // counted once above (reference LU rule)
     }
+    const bool pr = c.prof;
+    c.prof = false;  // the trailing GEMMs are part of this "lu" record
+    gb.run(c, tag);
+    c.prof = pr;
     c.launches += 2;
   }
-  c.prof_end("lu", ev, fl, 16.0 * n * double(n));
+  c.prof_end("lu", ev, fl, by);
   cuda_check(cudaGetLastError(), "blocked lu");
 }
 
@@ -464,16 +474,25 @@ void LuBatch::run(Ctx& c) {
   // walk a ~1000-column factorization alone (100 ms at the bench size).
   static const bool unblocked = getenv("H2G_LU_UNBLOCKED") != nullptr;
   if (!unblocked) {
-    std::vector<LuJob> small;
-    std::vector<std::string> snames;
+    // Blocks of kLuBlocked rows or more (H2G_LU_BLOCKED_MIN) take the blocked
+    // path together: panel kernels touch 32 columns per step instead of the
+    // whole trailing block, which goes through the DMMA GEMM once per panel.
+    // Default 384 = the top system only. Measured at the bench size with 128
+    // (every leaf block blocked): LU kernels 27 -> 15 ms, but the ~300 extra
+    // small launches cost more stream idle time than that (factor 1.21 -> 1.28 s).
+    static const int kLuBlocked = getenv("H2G_LU_BLOCKED_MIN") ? atoi(getenv("H2G_LU_BLOCKED_MIN")) : 384;
+    std::vector<LuJob> small, big;
+    std::vector<std::string> snames, bnames;
     for (size_t t = 0; t < jobs.size(); ++t) {
-      if (jobs[t].A.rows >= 384) {
-        run_blocked_lu(c, jobs[t], names[t]);
+      if (jobs[t].A.rows >= kLuBlocked) {
+        big.push_back(jobs[t]);
+        bnames.push_back(names[t]);
       } else {
         small.push_back(jobs[t]);
         snames.push_back(names[t]);
       }
     }
+    if (!big.empty()) run_blocked_lu(c, big, bnames);
     if (small.size() != jobs.size()) {
       jobs.swap(small);
       names.swap(snames);

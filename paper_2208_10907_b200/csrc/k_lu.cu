@@ -114,21 +114,24 @@ __global__ void __launch_bounds__(NT, 2) lu_kernel(const LuJob* __restrict__ job
 // 352-388): a row swap only moves a row's values and its multipliers
 // together, so delaying the right-hand columns' updates to the GEMM does not
 // change any element's sequence. Results equal lu_kernel's bit for bit.
-__global__ void __launch_bounds__(1024) lu_panel_kernel(LuJob job, int kb, int nb,
+__global__ void __launch_bounds__(1024) lu_panel_kernel(const LuJob* __restrict__ jobs, int kb, int nb_max,
                                                         const double* __restrict__ amax_p, ErrWord* err,
                                                         int tag) {
-  const double amax = *amax_p;
+  const LuJob job = jobs[blockIdx.x];
+  const double amax = amax_p[blockIdx.x];
   __shared__ ValIdx red[32];
   extern __shared__ double lcol[];
   const Mat M = job.A;
   const int n = M.rows;
+  if (kb >= n) return;  // a smaller block of the batch: already finished
+  const int nb = min(nb_max, n - kb);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
   for (int k = kb; k < kb + nb; ++k) {
     ValIdx best{-1.0, 0x7fffffff};
     for (int i = k + threadIdx.x; i < n; i += blockDim.x) best = better(best, ValIdx{fabs(M.at(i, k)), i});
     best = block_argmax(best, red);
     if (best.v <= job.tol * amax) {
-      if (threadIdx.x == 0) raise_err(err, 2, 0, k, tag);
+      if (threadIdx.x == 0) raise_err(err, 2, int(blockIdx.x), k, tag);
       return;
     }
     const int p = best.i;
@@ -162,10 +165,14 @@ __global__ void __launch_bounds__(1024) lu_panel_kernel(LuJob job, int kb, int n
 
 // Panel rows [kb, kb+nb) of the columns j >= kb + nb: a_ij -= l_ik u_kj for
 // k ascending, i in (k, kb+nb). One thread per column, values in registers.
-__global__ void __launch_bounds__(128) lu_rows_kernel(LuJob job, int kb, int nb) {
+__global__ void __launch_bounds__(128) lu_rows_kernel(const LuJob* __restrict__ jobs, int kb, int nb_max) {
   __shared__ double lblk[32 * 33];
+  const LuJob job = jobs[blockIdx.y];
   const Mat M = job.A;
   const int n = M.rows;
+  if (kb >= n) return;
+  const int nb = min(nb_max, n - kb);
+  if (kb + nb + int(blockIdx.x * blockDim.x) >= n) return;  // (uniform per CTA)
   for (int e = threadIdx.x; e < 32 * 32; e += blockDim.x) {
     const int i = e % 32, kk = e / 32;
     lblk[kk * 33 + i] = (i < nb && kk < nb) ? M.at(kb + i, kb + kk) : 0.0;
@@ -188,8 +195,10 @@ __global__ void __launch_bounds__(128) lu_rows_kernel(LuJob job, int kb, int nb)
     if (i < nb) M.at(kb + i, j) = x[i];
 }
 
-__global__ void lu_amax_kernel(LuJob job, double* out) {
+__global__ void lu_amax_kernel(const LuJob* __restrict__ jobs, double* out_all) {
   __shared__ ValIdx red[32];
+  const LuJob job = jobs[blockIdx.x];
+  double* out = out_all + blockIdx.x;
   const Mat M = job.A;
   const int n = M.rows;
   ValIdx am{0.0, 0};
@@ -565,20 +574,20 @@ void launch_gather_rows(const GatherJob* jobs, const int2* tiles, int ntiles, cu
   if (ntiles > 0) gather_rows_kernel<<<ntiles, 256, 0, st>>>(jobs, tiles);
 }
 
-void launch_lu_amax(const LuJob& job, double* out, cudaStream_t st) {
-  lu_amax_kernel<<<1, 1024, 0, st>>>(job, out);
+void launch_lu_amax(const LuJob* jobs, int njobs, double* out, cudaStream_t st) {
+  lu_amax_kernel<<<njobs, 1024, 0, st>>>(jobs, out);
 }
 
-void launch_lu_panel(const LuJob& job, int kb, int nb, const double* amax, ErrWord* err, int tag,
-                     cudaStream_t st) {
-  const size_t smem = sizeof(double) * size_t(job.A.rows);
+void launch_lu_panel(const LuJob* jobs, int njobs, int max_n, int kb, int nb, const double* amax, ErrWord* err,
+                     int tag, cudaStream_t st) {
+  const size_t smem = sizeof(double) * size_t(max_n);
   smem_attr((const void*)lu_panel_kernel, smem, "lu_panel smem attribute");
-  lu_panel_kernel<<<1, 1024, smem, st>>>(job, kb, nb, amax, err, tag);
+  lu_panel_kernel<<<njobs, 1024, smem, st>>>(jobs, kb, nb, amax, err, tag);
 }
 
-void launch_lu_rows(const LuJob& job, int kb, int nb, cudaStream_t st) {
-  const int ncols = job.A.rows - kb - nb;
-  if (ncols > 0) lu_rows_kernel<<<(ncols + 127) / 128, 128, 0, st>>>(job, kb, nb);
+void launch_lu_rows(const LuJob* jobs, int njobs, int max_n, int kb, int nb, cudaStream_t st) {
+  const int ncols = max_n - kb - nb;
+  if (ncols > 0) lu_rows_kernel<<<dim3((ncols + 127) / 128, njobs), 128, 0, st>>>(jobs, kb, nb);
 }
 
 void launch_lu(const LuJob* jobs, int njobs, int max_n, ErrWord* err, int tag, cudaStream_t st) {

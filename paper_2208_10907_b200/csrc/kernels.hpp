@@ -120,13 +120,14 @@ struct LuJob {
   double tol;
 };
 void launch_lu(const LuJob* jobs, int njobs, int max_n, ErrWord* err, int tag, cudaStream_t st);
-// Blocked LU of one large block (panels of 32 columns; bitwise equal to
-// lu_kernel): amax + identity perm, per panel: panel factorization, panel-row
-// updates, then a DMMA GEMM trailing update by the caller.
-void launch_lu_amax(const LuJob& job, double* out, cudaStream_t st);
-void launch_lu_panel(const LuJob& job, int kb, int nb, const double* amax, ErrWord* err, int tag,
-                     cudaStream_t st);
-void launch_lu_rows(const LuJob& job, int kb, int nb, cudaStream_t st);
+// Blocked LU of a batch of blocks (panels of 32 columns; bitwise equal to
+// lu_kernel): amax + identity perm, per panel step: panel factorization (one
+// CTA per block), panel-row updates, then a DMMA GEMM trailing update by the
+// caller. Blocks smaller than the current panel offset sit the step out.
+void launch_lu_amax(const LuJob* jobs, int njobs, double* out, cudaStream_t st);  // out[job]; identity perms
+void launch_lu_panel(const LuJob* jobs, int njobs, int max_n, int kb, int nb, const double* amax, ErrWord* err,
+                     int tag, cudaStream_t st);
+void launch_lu_rows(const LuJob* jobs, int njobs, int max_n, int kb, int nb, cudaStream_t st);
 
 // LuFactors solve family (linalg.cpp:404-559), in place on X.
 enum SolveKind : int {
