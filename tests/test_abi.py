@@ -59,3 +59,10 @@ def test_python_generator_matches_oracle():
     a, _ = generate_uniform_cube(777, 42)
     b, _ = cpu.generate("cube", 777, 42)
     assert np.array_equal(a.view(np.int64), b.view(np.int64))
+
+
+def test_trim_memory_is_safe_without_allocations():
+    """h2g_trim_memory (the arena's release entry point) is a no-op when nothing
+    was ever allocated - in particular on a host without a GPU."""
+    _lib.trim_memory()
+    _lib.trim_memory()

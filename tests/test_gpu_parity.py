@@ -311,3 +311,32 @@ def test_gemm_kernels_bitwise_vs_live_reference():
         got = g.gemm(a, b, alpha, ta, tb, c0)
         want = ref.gemm(a, b, alpha, ta, tb, c0)
         assert np.array_equal(got.view(np.int64), want.view(np.int64)), (m, n, k, ta, tb, alpha)
+
+
+def test_arena_reuse_and_trim():
+    """Device memory arena: a second factorization of the same problem reuses
+    the first one's blocks (bitwise the same x), h2g_trim_memory hands the free
+    segments back to the driver, and a factorization afterwards still works."""
+    import torch
+    xyz, q = cpu.generate("cube", 2048, 42)
+    b = ref.splitmix_signed(2048, 7)
+
+    def run():
+        p = h2.Problem()
+        p.set_kernel("laplace", 0.0, 1.0, 1e-3)
+        p.set_options(tol=1e-8)
+        p.build(xyz, q, 128)
+        p.factor()
+        x = p.solve(b)
+        p.close()
+        return x
+
+    x0 = run()
+    x1 = run()
+    assert np.array_equal(x0.view(np.int64), x1.view(np.int64))
+    free0 = torch.cuda.mem_get_info()[0]
+    g.trim_memory()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free1 >= free0
+    x2 = run()
+    assert np.array_equal(x0.view(np.int64), x2.view(np.int64))
