@@ -207,24 +207,58 @@ std::vector<LuF> alloc_lus(Ctx& c, const std::vector<int>& ns) {
 
 namespace {
 
+// Prefix sums of the jobs' 64 x 64 tile counts (njobs + 1 entries).
 template <class J>
-void tiles_of(const std::vector<J>& jobs, std::vector<int>& tj, std::vector<int>& ti,
-              Mat J::*field) {
+std::vector<int> tiles_of(const std::vector<J>& jobs, Mat J::*field) {
+  std::vector<int> ptr(jobs.size() + 1, 0);
   for (size_t j = 0; j < jobs.size(); ++j) {
     const Mat& m = jobs[j].*field;
-    if (m.rows <= 0 || m.cols <= 0) continue;
-    const int t = ((m.rows + 63) / 64) * ((m.cols + 63) / 64);
-    for (int k = 0; k < t; ++k) {
-      tj.push_back(int(j));
-      ti.push_back(k);
-    }
+    const int64_t t = (m.rows <= 0 || m.cols <= 0) ? 0 : int64_t((m.rows + 63) / 64) * ((m.cols + 63) / 64);
+    if (ptr[j] + t > int64_t(0x7fffffff)) throw std::runtime_error("batch: too many tiles in one launch");
+    ptr[j + 1] = ptr[j] + int(t);
   }
+  return ptr;
 }
 
 }  // namespace
 
+// H2G_HOST_PROF: host seconds spent inside the batch launchers (descriptor
+// building, uploads, launches), by kind; printed by host_prof_report().
+namespace {
+struct HostTimer {
+  static std::map<std::string, std::pair<double, int64_t>>& acc() {
+    static std::map<std::string, std::pair<double, int64_t>> a;
+    return a;
+  }
+  static bool on() {
+    static const bool v = getenv("H2G_HOST_PROF") != nullptr;
+    return v;
+  }
+  const char* name;
+  std::chrono::steady_clock::time_point t0;
+  explicit HostTimer(const char* n) : name(n) {
+    if (on()) t0 = std::chrono::steady_clock::now();
+  }
+  ~HostTimer() {
+    if (!on()) return;
+    auto& e = acc()[name];
+    e.first += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    e.second++;
+  }
+};
+}  // namespace
+
+void host_prof_report() {
+  if (!HostTimer::on()) return;
+  for (auto& [k, v] : HostTimer::acc())
+    fprintf(stderr, "HOSTBATCH %-10s %8.2f ms in %6ld calls (%.1f us each)\n", k.c_str(), v.first * 1e3, long(v.second),
+            v.second ? v.first * 1e6 / v.second : 0.0);
+  HostTimer::acc().clear();
+}
+
 void GemmBatch::run(Ctx& c, int tag) {
   if (jobs.empty()) return;
+  HostTimer ht("gemm");
   std::vector<GemmTile> tiles;
   double fl = 0;
   int max_rows = 0;
@@ -352,20 +386,19 @@ void GemmBatch::run(Ctx& c, int tag) {
 
 void EvalBatch::run(Ctx& c, int tag) {
   if (jobs.empty()) return;
-  std::vector<int> tj, ti;
-  tiles_of(jobs, tj, ti, &EvalJob::out);
+  HostTimer ht("eval");
+  const std::vector<int> tp = tiles_of(jobs, &EvalJob::out);
   double evn_ = 0;
   for (auto& j : jobs) evn_ += double(j.out.rows) * j.out.cols;
   const double ev_flops_ = evn_ * kernel_entry_flops(c.kp.kind);
   c.kernel_evals += evn_;
   c.add_flops(ev_flops_);
-  if (tj.empty()) return;
-  Slab k1, k2, k3;
+  if (tp.back() == 0) return;
+  Slab k1, k2;
   auto* dj = upload(c, jobs, k1);
-  auto* dtj = upload(c, tj, k2);
-  auto* dti = upload(c, ti, k3);
+  auto* dtp = upload(c, tp, k2);
   auto ev = c.prof_begin();
-  launch_eval(dj, dtj, dti, int(tj.size()), c.kp, c.cloud, c.err, tag, c.stream);
+  launch_eval(dj, dtp, int(jobs.size()), tp.back(), c.kp, c.cloud, c.err, tag, c.stream);
   c.prof_end(c.prof_detail ? ("eval@" + c.phase).c_str() : "eval", ev, ev_flops_, 8.0 * evn_);
   c.launches++;
   cuda_check(cudaGetLastError(), "eval launch");
@@ -373,17 +406,16 @@ void EvalBatch::run(Ctx& c, int tag) {
 
 void CopyBatch::run(Ctx& c) {
   if (jobs.empty()) return;
-  std::vector<int> tj, ti;
-  tiles_of(jobs, tj, ti, &CopyJob::dst);
-  if (tj.empty()) return;
-  Slab k1, k2, k3;
+  HostTimer ht("copy");
+  const std::vector<int> tp = tiles_of(jobs, &CopyJob::dst);
+  if (tp.back() == 0) return;
+  Slab k1, k2;
   auto* dj = upload(c, jobs, k1);
-  auto* dtj = upload(c, tj, k2);
-  auto* dti = upload(c, ti, k3);
+  auto* dtp = upload(c, tp, k2);
   double by = 0;
   for (auto& j : jobs) by += 8.0 * j.dst.rows * double(j.dst.cols) * (1 + (j.src.p ? 1 : 0) + j.add);
   auto ev = c.prof_begin();
-  launch_copy(dj, dtj, dti, int(tj.size()), c.stream);
+  launch_copy(dj, dtp, int(jobs.size()), tp.back(), c.stream);
   c.prof_end(c.prof_detail ? ("copy@" + c.phase).c_str() : "copy", ev, 0.0, by);
   c.launches++;
   cuda_check(cudaGetLastError(), "copy launch");
@@ -391,18 +423,17 @@ void CopyBatch::run(Ctx& c) {
 
 void AccBatch::run(Ctx& c) {
   if (jobs.empty()) return;
-  std::vector<int> tj, ti;
-  tiles_of(jobs, tj, ti, &AccJob::dst);
-  if (tj.empty()) return;
-  Slab k1, k2, k3, k4;
+  HostTimer ht("accum");
+  const std::vector<int> tp = tiles_of(jobs, &AccJob::dst);
+  if (tp.back() == 0) return;
+  Slab k1, k2, k4;
   auto* dj = upload(c, jobs, k1);
   auto* ds = upload(c, srcs, k4);
-  auto* dtj = upload(c, tj, k2);
-  auto* dti = upload(c, ti, k3);
+  auto* dtp = upload(c, tp, k2);
   double by = 0;
   for (auto& j : jobs) by += 8.0 * j.dst.rows * double(j.dst.cols) * (1 + j.nsrc + (j.zero_init ? 0 : 1));
   auto ev = c.prof_begin();
-  launch_accum(dj, ds, dtj, dti, int(tj.size()), c.stream);
+  launch_accum(dj, ds, dtp, int(jobs.size()), tp.back(), c.stream);
   c.prof_end("accum", ev, 0.0, by);
   c.launches++;
   cuda_check(cudaGetLastError(), "accum launch");
@@ -470,6 +501,7 @@ static void run_blocked_lu(Ctx& c, const std::vector<LuJob>& js, const std::vect
 
 void LuBatch::run(Ctx& c) {
   if (jobs.empty()) return;
+  HostTimer ht("lu");
   // Large blocks (the top system) go through the blocked LU: one CTA would
   // walk a ~1000-column factorization alone (100 ms at the bench size).
   static const bool unblocked = getenv("H2G_LU_UNBLOCKED") != nullptr;
@@ -712,6 +744,7 @@ static void run_inverse(Ctx& c, const std::vector<SolveJob>& ij, size_t budget) 
 }
 
 void SolveBatch::run(Ctx& c) {
+  HostTimer ht("solve");
   if (jobs.empty()) return;
   if (c.fast_solve) {
     std::vector<SolveJob> ij, rest;

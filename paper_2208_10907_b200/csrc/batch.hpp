@@ -104,6 +104,8 @@ struct Ctx {
   void prof_resolve();  // after a sync: fold finished records into pagg
 };
 
+void host_prof_report();  // H2G_HOST_PROF: host time inside the batch launchers
+
 struct DMat {
   Mat m;
   Slab owner;

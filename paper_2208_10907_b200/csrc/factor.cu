@@ -2182,6 +2182,7 @@ void Problem::factor() {
   stats.t_factor_dev = dt.stop();
   stats.t_factor = now_s() - t0;
   c.prof_resolve();
+  host_prof_report();
   for (auto& [k, v] : c.phase_flops) stats.phase_flops[k] += v;
   stats.launches = c.launches;
   stats.max_fill_residual = 0;

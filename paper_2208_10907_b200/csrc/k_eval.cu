@@ -8,22 +8,33 @@ namespace {
 
 constexpr int T = 64, NT = 256;
 
+// Tile -> (job, tile index within the job) from the per-job prefix sums of tile
+// counts (the host uploads njobs + 1 integers instead of two per tile).
+__device__ __forceinline__ int find_job(const int* __restrict__ ptr, int njobs, int tile, int& idx) {
+  int lo = 0, hi = njobs;  // ptr[lo] <= tile < ptr[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (ptr[mid] <= tile) lo = mid; else hi = mid;
+  }
+  idx = tile - ptr[lo];
+  return lo;
+}
+
 // assemble_block (kernels.cpp:242-268) over 64x64 tiles; rows fastest so a
 // column-major destination is written coalesced. The near-field arena write
 // is the HBM-bound phase (8 B per entry).
 __global__ void __launch_bounds__(NT) eval_kernel(const EvalJob* __restrict__ jobs,
-                                                  const int* __restrict__ tile_job,
-                                                  const int* __restrict__ tile_idx,
+                                                  const int* __restrict__ tile_ptr, int njobs,
                                                   KernelParams kp, Cloud cloud, ErrWord* err,
                                                   int tag) {
   // A thread's row is fixed (NT is a multiple of T): its point stays in
   // registers; the tile's 64 column points are staged in shared memory and
   // read as warp-wide broadcasts (a warp's 32 entries share one column).
   __shared__ double cpt[T][4];
-  const int jb = tile_job[blockIdx.x];
+  int ti;
+  const int jb = find_job(tile_ptr, njobs, blockIdx.x, ti);
   const EvalJob job = jobs[jb];
   const int tpr = (job.out.rows + T - 1) / T;
-  const int ti = tile_idx[blockIdx.x];
   const int r0 = (ti % tpr) * T, c0 = (ti / tpr) * T;
   {
     const int jj = threadIdx.x >> 2, comp = threadIdx.x & 3;  // NT = 4 T
@@ -59,11 +70,10 @@ __global__ void __launch_bounds__(NT) eval_kernel(const EvalJob* __restrict__ jo
 // dst = (add ? dst : 0) + alpha * src  — the reference's add_block computes
 // dst[i] += alpha * src[i], contracted to fma(alpha, src, dst).
 __global__ void __launch_bounds__(NT) copy_kernel(const CopyJob* __restrict__ jobs,
-                                                  const int* __restrict__ tile_job,
-                                                  const int* __restrict__ tile_idx) {
-  const CopyJob job = jobs[tile_job[blockIdx.x]];
+                                                  const int* __restrict__ tile_ptr, int njobs) {
+  int ti;
+  const CopyJob job = jobs[find_job(tile_ptr, njobs, blockIdx.x, ti)];
   const int tpr = (job.dst.rows + T - 1) / T;
-  const int ti = tile_idx[blockIdx.x];
   const int r0 = (ti % tpr) * T, c0 = (ti / tpr) * T;
   for (int e = threadIdx.x; e < T * T; e += NT) {
     const int i = r0 + (e % T), j = c0 + (e / T);
@@ -83,11 +93,10 @@ __global__ void __launch_bounds__(NT) copy_kernel(const CopyJob* __restrict__ jo
 
 __global__ void __launch_bounds__(NT) accum_kernel(const AccJob* __restrict__ jobs,
                                                    const AccSrc* __restrict__ srcs,
-                                                   const int* __restrict__ tile_job,
-                                                   const int* __restrict__ tile_idx) {
-  const AccJob job = jobs[tile_job[blockIdx.x]];
+                                                   const int* __restrict__ tile_ptr, int njobs) {
+  int ti;
+  const AccJob job = jobs[find_job(tile_ptr, njobs, blockIdx.x, ti)];
   const int tpr = (job.dst.rows + T - 1) / T;
-  const int ti = tile_idx[blockIdx.x];
   const int r0 = (ti % tpr) * T, c0 = (ti / tpr) * T;
   for (int e = threadIdx.x; e < T * T; e += NT) {
     const int i = r0 + (e % T), j = c0 + (e / T);
@@ -210,19 +219,18 @@ void launch_matvec(KernelParams kp, Cloud c, const double* x, double* y, int nrh
   if (c.n > 0) matvec_kernel<<<unsigned((c.n + 255) / 256), 256, 0, st>>>(kp, c, x, y, nrhs, singular);
 }
 
-void launch_eval(const EvalJob* jobs, const int* tile_job, const int* tile_idx, int ntiles,
-                 KernelParams kp, Cloud cloud, ErrWord* err, int tag, cudaStream_t st) {
-  if (ntiles > 0) eval_kernel<<<ntiles, NT, 0, st>>>(jobs, tile_job, tile_idx, kp, cloud, err, tag);
+void launch_eval(const EvalJob* jobs, const int* tile_ptr, int njobs, int ntiles, KernelParams kp, Cloud cloud,
+                 ErrWord* err, int tag, cudaStream_t st) {
+  if (ntiles > 0) eval_kernel<<<ntiles, NT, 0, st>>>(jobs, tile_ptr, njobs, kp, cloud, err, tag);
 }
 
-void launch_copy(const CopyJob* jobs, const int* tile_job, const int* tile_idx, int ntiles,
-                 cudaStream_t st) {
-  if (ntiles > 0) copy_kernel<<<ntiles, NT, 0, st>>>(jobs, tile_job, tile_idx);
+void launch_copy(const CopyJob* jobs, const int* tile_ptr, int njobs, int ntiles, cudaStream_t st) {
+  if (ntiles > 0) copy_kernel<<<ntiles, NT, 0, st>>>(jobs, tile_ptr, njobs);
 }
 
-void launch_accum(const AccJob* jobs, const AccSrc* srcs, const int* tile_job, const int* tile_idx,
-                  int ntiles, cudaStream_t st) {
-  if (ntiles > 0) accum_kernel<<<ntiles, NT, 0, st>>>(jobs, srcs, tile_job, tile_idx);
+void launch_accum(const AccJob* jobs, const AccSrc* srcs, const int* tile_ptr, int njobs, int ntiles,
+                  cudaStream_t st) {
+  if (ntiles > 0) accum_kernel<<<ntiles, NT, 0, st>>>(jobs, srcs, tile_ptr, njobs);
 }
 
 void launch_permute_rows(Mat dst, Mat src, const int64_t* idx, int scatter, cudaStream_t st) {

@@ -68,8 +68,9 @@ struct EvalJob {
   int64_t rb, cb;
   int rstep = 1, cstep = 1;
 };
-void launch_eval(const EvalJob* jobs, const int* tile_job, const int* tile_idx, int ntiles,
-                 KernelParams kp, Cloud cloud, ErrWord* err, int tag, cudaStream_t st);
+// tile_ptr: njobs + 1 prefix sums of the jobs' 64 x 64 tile counts (the kernels find their job by bisection).
+void launch_eval(const EvalJob* jobs, const int* tile_ptr, int njobs, int ntiles, KernelParams kp, Cloud cloud,
+                 ErrWord* err, int tag, cudaStream_t st);
 
 // ---- batched copies / adds / zero-fills (k_eval.cu) -----------------------
 // dst = (add ? dst : 0) + alpha * src (add_block alpha form, matrix.cpp:55-64);
@@ -80,8 +81,7 @@ struct CopyJob {
   int add = 0;
   int ident = 0;
 };
-void launch_copy(const CopyJob* jobs, const int* tile_job, const int* tile_idx, int ntiles,
-                 cudaStream_t st);
+void launch_copy(const CopyJob* jobs, const int* tile_ptr, int njobs, int ntiles, cudaStream_t st);
 
 // ---- ordered accumulation: dst = (zero ? 0 : dst) then, for s in order,
 // dst = fma(alpha_s, src_s, dst) — a chain of the reference's add_block calls.
@@ -94,8 +94,8 @@ struct AccSrc {
   Mat src;
   double alpha;
 };
-void launch_accum(const AccJob* jobs, const AccSrc* srcs, const int* tile_job, const int* tile_idx,
-                  int ntiles, cudaStream_t st);
+void launch_accum(const AccJob* jobs, const AccSrc* srcs, const int* tile_ptr, int njobs, int ntiles,
+                  cudaStream_t st);
 
 // Row gather/scatter of a multi-column vector block: dst(i, :) = src(idx[i], :)
 // (scatter = 0) or dst(idx[i], :) = src(i, :) (scatter = 1).
