@@ -300,15 +300,26 @@ def run_b200_arm(args):
     # Breakdown pass (separate from the timed region): per-kernel-family CUDA
     # events and per-phase device time of one more step.
     with torch.cuda.stream(stream):
+        os.environ["H2G_PROF_DETAIL"] = "1"  # kernel records named family@phase (read at handle creation)
         p = new_problem()
+        os.environ.pop("H2G_PROF_DETAIL", None)
         p.set_profile(True)
         p.reset_profile()
         step(p)
         barrier()
         sd = p.stats_dev()
         t_phase = {k: sd[k] for k in ("build", "factor", "solve")}
-        kstats = p.kernel_stats()
+        kdetail = p.kernel_stats()
         p.close()
+    # per family (all phases) and per phase (all families)
+    kstats, by_phase = {}, {}
+    for k, v in kdetail.items():
+        fam, _, ph = k.partition("@")
+        ph = ph.split("@")[0].split(":")[0] or "other"
+        a = kstats.setdefault(fam, {"ms": 0.0, "flops": 0.0, "bytes": 0.0, "launches": 0})
+        for f in ("ms", "flops", "bytes", "launches"):
+            a[f] += v[f]
+        by_phase.setdefault(ph, {})[fam] = v
 
     # e2e through the public C-ABI with host buffers (H2D/D2H inside the region).
     # Like the device-timed steps, one handle serves every e2e step (creating it
@@ -451,6 +462,26 @@ def run_b200_arm(args):
             families[k] = {"bound": "hbm", "achieved": a, "unit": "GB/s", "peak": hbm_peak,
                            "frac": a / hbm_peak, "ms": v["ms"], "launches": v["launches"]}
     roofline["families"] = families
+    # every batched phase of the factorization against its roofs: the FP64 work of the
+    # phase (GEMM, Gram, LU, pivoted Cholesky) against the FP64 peak over the time those
+    # kernels take, its data movement (evaluation writes, copies, QR sweeps, solves)
+    # against the HBM bandwidth over theirs
+    phases = {}
+    for ph, fams in by_phase.items():
+        f_ms = sum(v["ms"] for k, v in fams.items() if k in fp64_families)
+        f_fl = sum(v["flops"] for k, v in fams.items() if k in fp64_families)
+        h_ms = sum(v["ms"] for k, v in fams.items() if k not in fp64_families)
+        h_by = sum(v["bytes"] for k, v in fams.items() if k not in fp64_families)
+        e = {"ms": f_ms + h_ms, "launches": int(sum(v["launches"] for v in fams.values()))}
+        if f_ms:
+            tf = f_fl / (f_ms * 1e-3) / 1e12
+            e["fp64"] = {"ms": f_ms, "achieved": tf, "unit": "TFLOP/s", "frac": tf / FP64_DMMA_TFLOPS}
+        if h_ms:
+            gb = h_by / (h_ms * 1e-3) / 1e9
+            e["hbm"] = {"ms": h_ms, "achieved": gb, "unit": "GB/s", "frac": gb / hbm_peak}
+        e["bound"] = "fp64" if f_ms >= h_ms else "hbm"
+        phases[ph] = e
+    roofline["phases"] = phases
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.skip_cpu:

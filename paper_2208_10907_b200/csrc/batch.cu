@@ -98,7 +98,9 @@ void Ctx::prof_end(const char* name, cudaEvent_t a, double flops, double bytes) 
   cudaEvent_t e;
   cuda_check(cudaEventCreate(&e), "event");
   cuda_check(cudaEventRecord(e, stream), "event record");
-  prec.push_back({name, a, e, flops, bytes, phase});
+  std::string nm = name;
+  if (prof_detail && nm.find('@') == std::string::npos) nm += "@" + phase;  // every record carries its phase
+  prec.push_back({nm, a, e, flops, bytes, phase});
 }
 
 void Ctx::prof_resolve() {
