@@ -823,7 +823,15 @@ static void compress_members(Ctx& c, std::vector<QrBatch::Item>& items, size_t m
       if (w >= kPcholMinWidth) wide.push_back({t, int(s), w, std::min(it.m, w)});
     }
   }
-  if (wide.empty()) return;
+  auto view_of = [](const QrBatch::Item& it, size_t s) {
+    return s < it.views.size() && it.views[s].p ? it.views[s] : Mat{};
+  };
+  std::vector<char> has_view(items.size(), 0);
+  bool any_view = false;
+  for (size_t t = 0; t < items.size(); ++t)
+    for (auto& v : items[t].views)
+      if (v.p) has_view[t] = 1, any_view = true;
+  if (wide.empty() && !any_view) return;
   std::vector<std::vector<DMat>> comp(items.size());  // per item, per member (wide only)
   for (size_t t = 0; t < items.size(); ++t) comp[t].resize(items[t].offs.size() > 0 ? items[t].offs.size() - 1 : 0);
   size_t g0 = 0;
@@ -851,7 +859,8 @@ static void compress_members(Ctx& c, std::vector<QrBatch::Item>& items, size_t m
     int max_m = 1, max_k = 1;
     for (size_t g = g0; g < g1; ++g) {
       const auto& it = items[wide[g].item];
-      const Mat A = it.concat.m.sub(0, int(it.offs[wide[g].mem]), it.m, wide[g].w);
+      const Mat vw = view_of(it, size_t(wide[g].mem));
+      const Mat A = vw.p ? vw : it.concat.m.sub(0, int(it.offs[wide[g].mem]), it.m, wide[g].w);
       const DMat& G = gr[2 * (g - g0)];
       const DMat& R = gr[2 * (g - g0) + 1];
       gemm1(gb, G.m, A, A.t());
@@ -904,8 +913,12 @@ static void compress_members(Ctx& c, std::vector<QrBatch::Item>& items, size_t m
   CopyBatch cb;
   std::vector<DMat> old;  // source concats stay alive until the copies are enqueued
   std::vector<size_t> touched;
-  for (const auto& w : wide)
-    if (touched.empty() || touched.back() != w.item) touched.push_back(w.item);
+  {
+    std::vector<char> mark(items.size(), 0);
+    for (const auto& w : wide) mark[w.item] = 1;
+    for (size_t t = 0; t < items.size(); ++t)
+      if (mark[t] || has_view[t]) touched.push_back(t);  // a view member must be packed into the panel
+  }
   for (size_t t : touched) {
     auto& it = items[t];
     std::vector<int64_t> offs{0};
@@ -924,6 +937,8 @@ static void compress_members(Ctx& c, std::vector<QrBatch::Item>& items, size_t m
       const Mat dst = nc.m.sub(0, int(offs[s]), it.m, w2);
       if (comp[t][s].owner)
         cb.copy(dst, comp[t][s].m);
+      else if (view_of(it, s).p)
+        cb.copy(dst, view_of(it, s));
       else
         cb.copy(dst, it.concat.m.sub(0, int(it.offs[s]), it.m, w2));
     }
@@ -931,6 +946,7 @@ static void compress_members(Ctx& c, std::vector<QrBatch::Item>& items, size_t m
     it.concat = nc;
     it.n = n2;
     it.offs = std::move(offs);
+    it.views.clear();
     it.inplace = true;
   }
   cb.run(c);

@@ -270,6 +270,10 @@ struct QrBatch {
     int cap;
     bool inplace;  // factor the concat itself (it is consumed)
     int fixed = 0;  // compressed mode: members [0, fixed) are already compressed
+    // Compressed mode: views[s].p != nullptr -> member s is that m x w_s matrix (not
+    // stored in the concat): its Gram GEMM reads it in place, only its compressed
+    // columns enter the panel.
+    std::vector<Mat> views;
   };
   std::vector<Item> items;
   int add(DMat concat, int m, int n, std::vector<int64_t> offs, double tol, int cap,

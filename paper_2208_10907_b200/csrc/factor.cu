@@ -447,6 +447,12 @@ struct Driver {
       const int ld = std::max(2, (dim + 1) & ~1);
       return Mat{concat.m.p + int64_t(off) * ld, dim, w, 1, ld};
     }
+    // Compressed mode: member s read in place from views[s] (see QrBatch::Item).
+    std::vector<Mat> views;
+    void set_view(size_t s, const Mat& v) {
+      if (views.size() < offs.size() - 1) views.resize(offs.size() - 1);
+      views[s] = v;
+    }
     int add(int w) {
       const int off = width;
       width += w;
@@ -674,6 +680,7 @@ struct Driver {
       for (int64_t k = k0; k < k1; ++k) {
         qb.add(rows[k].concat, rows[k].dim, rows[k].width, rows[k].offs, opt.tol, opt.cap, true);
         qb.items.back().fixed = rows[k].fixed;
+        qb.items.back().views = rows[k].views;
         rows[k].concat = DMat{};
       }
       if (cols)
@@ -1547,10 +1554,16 @@ struct Driver {
                     cb.copy(rows[k].slice(off, F->cols()), F->m);
                     off += F->cols();
                   }
+                  size_t mem = FI.by_row[k].size();
                   for (auto& [tk, piece] : merged[k]) {
                     const Samp sp = samp(piece.cols());
-                    cb.copy(rows[k].slice(off, sp.count), sample_cols_view(piece.m, sp));
+                    // compressed mode: the Gram GEMM reads the piece in place (no copy into the panel)
+                    if (c.qr_compress)
+                      rows[k].set_view(mem, sample_cols_view(piece.m, sp));
+                    else
+                      cb.copy(rows[k].slice(off, sp.count), sample_cols_view(piece.m, sp));
                     off += sp.count;
+                    ++mem;
                   }
                   off = 0;
                   for (const DMat* F : FI.by_col[k]) {
