@@ -3,10 +3,9 @@ import sys
 import numpy as np
 sys.path.insert(0, '.')
 import paper_2208_10907_b200 as h2
-from paper_2208_10907_b200.pipeline import _fib_spheres
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
-xyz, q = _fib_spheres(n, 1, 3.0, 42)
+xyz, q = h2.generate_points("sphere", n, 42)
 p = h2.Problem()
 p.set_kernel("yukawa", 1.0, 1.0, 1e-3)
 import os
