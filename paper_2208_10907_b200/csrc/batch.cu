@@ -894,7 +894,7 @@ static void compress_members(Ctx& c, std::vector<QrBatch::Item>& items, size_t m
       cs.push_back({m, std::max(k, 0)});
     }
     c.add_flops(fl);
-    if (prof_at > 0 && prof_at == c.prec.size() && c.prec.back().name == "pchol") {
+    if (prof_at > 0 && prof_at == c.prec.size() && c.prec.back().name.rfind("pchol", 0) == 0) {
       c.prec.back().flops = fl;
       c.prec.back().bytes = by;
     }
