@@ -159,6 +159,16 @@ Ctx::~Ctx() {
 }
 
 
+int* Ctx::ticket() {
+  constexpr int kTickets = 8192;
+  if (!tickets || tickets_used >= kTickets) {
+    if (!tickets) tickets = alloc(sizeof(int) * kTickets);
+    cuda_check(cudaMemsetAsync(tickets.get(), 0, sizeof(int) * kTickets, stream), "ticket reset");
+    tickets_used = 0;
+  }
+  return static_cast<int*>(tickets.get()) + tickets_used++;
+}
+
 void Ctx::sync() {
   pin_head = 0;
   cuda_check(cudaStreamSynchronize(stream), "stream sync");
@@ -367,7 +377,7 @@ void GemmBatch::run(Ctx& c, int tag) {
   }
   auto ev = c.prof_begin();
   if (p8)
-    launch_gemm_p8(dj, ds, dt, int(tiles.size()), c.stream);
+    launch_gemm_p8(dj, ds, dt, int(tiles.size()), c.ticket(), c.stream);
   else
     launch_gemm(dj, ds, dt, int(tiles.size()), bm, c.kp, c.cloud, c.err, tag, c.stream,
                 name && std::string(name) == "gram" ? 1 : 0);

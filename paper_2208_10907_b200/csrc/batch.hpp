@@ -59,6 +59,11 @@ struct Ctx {
   char* pin = nullptr;
   size_t pin_cap = 0, pin_head = 0;
   const void* stage(const void* src, size_t bytes);
+  // Zeroed device integers, one per launch that hands work out dynamically
+  // (k_gemm8.cu): a slab of them, re-zeroed (stream-ordered) when used up.
+  Slab tickets;
+  int tickets_used = 0;
+  int* ticket();
   Ctx() = default;
   Ctx(const Ctx&) = delete;
   Ctx& operator=(const Ctx&) = delete;

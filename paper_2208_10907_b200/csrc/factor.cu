@@ -88,6 +88,7 @@ Problem::Problem() {
 }
 
 void Problem::use_stream(cudaStream_t s) {
+  c.tickets.reset();  // (re-created, and zeroed, on the new stream)
   cuda_check(cudaStreamSynchronize(c.stream), "stream");
   arena_stream_gone(c.stream);
   if (own_stream_) cudaStreamDestroy(c.stream);
@@ -104,6 +105,7 @@ Problem::~Problem() {
   near.clear();
   near_slab.reset();
   orig_slab.reset();
+  c.tickets.reset();
   if (c.stream) cudaStreamSynchronize(c.stream);
   arena_stream_gone(c.stream);  // its released blocks are now usable from any stream
   cudaFree(c.err);

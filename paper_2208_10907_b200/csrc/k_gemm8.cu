@@ -42,12 +42,15 @@ constexpr int B_ST = TN * SK > BK * SBN ? TN * SK : BK * SBN;
 struct Meta {
   double alpha;
   int a_kmajor, b_kmajor;
+  int tile;  // tile this stage belongs to; -1: no more tiles (the consumers leave)
+  int nch;   // chunks of that tile; 0: a data-less stage announcing a tile without chunks
 };
 struct Smem {
   double A[NS][A_ST];
   double B[NS][B_ST];
   Meta meta[NS];
   unsigned long long full[NS], empty[NS];
+  int next_tile;
 };
 
 __device__ __forceinline__ unsigned su32(const void* p) {
@@ -196,7 +199,8 @@ __device__ __forceinline__ int warp_window(CInfo& ci, int nb) {
 
 __global__ void __launch_bounds__(NT, 1) gemm_p8_kernel(const GemmJob* __restrict__ jobs,
                                                        const GemmSeg* __restrict__ segs,
-                                                       const GemmTile* __restrict__ tiles, int ntiles) {
+                                                       const GemmTile* __restrict__ tiles, int ntiles,
+                                                       int* __restrict__ counter) {
   extern __shared__ __align__(16) unsigned char smraw[];
   Smem& sm = *reinterpret_cast<Smem*>(smraw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -211,11 +215,36 @@ __global__ void __launch_bounds__(NT, 1) gemm_p8_kernel(const GemmJob* __restric
   if (warp >= NC / 32) {
     // ---------------- producers ----------------
     const int pt = threadIdx.x - NC;
-    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    // Tiles are handed out dynamically (one atomic per tile): their K extents
+    // differ by up to 4x inside a launch, and a static round-robin left 5 % of
+    // the SM-cycles idle at the end of the largest launch.
+    auto announce = [&](int tile_id, int nch) {  // a data-less stage
+      const int st = gc % NS;
+      if (gc >= NS) mb_wait(&sm.empty[st], ((gc / NS) - 1) & 1);
+      if (pt == 0) sm.meta[st] = Meta{1.0, 1, 1, tile_id, nch};
+      mb_arrive_cp_async(&sm.full[st]);
+      mb_arrive(&sm.full[st]);
+      ++gc;
+    };
+    while (true) {
+      if (pt == 0) sm.next_tile = atomicAdd(counter, 1);
+      asm volatile("bar.sync 1, %0;\n" ::"n"(NP) : "memory");
+      const int ti = sm.next_tile;
+      asm volatile("bar.sync 1, %0;\n" ::"n"(NP) : "memory");  // everyone has read it before the next overwrite
+      if (ti >= ntiles) {
+        announce(-1, 0);
+        break;
+      }
       const GemmTile tile = tiles[ti];
       const GemmJob job = jobs[tile.job];
       const TileGeom tg = geom(tile, job.C.rows);
       const int mrows = tg.mf * 8, ccols = job.C.cols;
+      int nch = 0;
+      for (int s = 0; s < job.nseg; ++s) nch += (segs[job.seg0 + s].A.cols + BK - 1) / BK;
+      if (nch == 0) {
+        announce(ti, 0);
+        continue;
+      }
       for (int s = 0; s < job.nseg; ++s) {
         const GemmSeg& sg = segs[job.seg0 + s];
         const Mat A = sg.A, B = sg.B;
@@ -226,7 +255,7 @@ __global__ void __launch_bounds__(NT, 1) gemm_p8_kernel(const GemmJob* __restric
         for (int pk = 0; pk < K; pk += BK, ++gc) {
           const int st = gc % NS;
           if (gc >= NS) mb_wait(&sm.empty[st], ((gc / NS) - 1) & 1);
-          if (pt == 0) sm.meta[st] = Meta{alpha, a_km ? 1 : 0, b_km ? 1 : 0};
+          if (pt == 0) sm.meta[st] = Meta{alpha, a_km ? 1 : 0, b_km ? 1 : 0, ti, nch};
           double* As = sm.A[st];
           double* Bs = sm.B[st];
           if (a_km) {
@@ -300,16 +329,20 @@ __global__ void __launch_bounds__(NT, 1) gemm_p8_kernel(const GemmJob* __restric
   // symmetric tile the work falls with the column index, so the second four
   // take the groups in reverse (group s and 7 - s per scheduler).
   const int nb = 16 * (warp < 4 ? warp : 11 - warp);
-  for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+  while (true) {
+    // The first stage of a tile names it (and says how many chunks follow).
+    int st = gc % NS;
+    mb_wait(&sm.full[st], (gc / NS) & 1);
+    const int ti = sm.meta[st].tile;
+    const int nch = sm.meta[st].nch;
+    if (ti < 0) break;  // no more tiles
     double acc[MF][2][2];
-    int nch = 0, mfc = 0, fskip = 0;
+    int mfc = 0, fskip = 0;
     {
       CInfo ci = load_info(jobs, tiles, ti);
       fskip = warp_window(ci, nb);
       const int c0 = ci.n0 + nb;
       mfc = (c0 < ci.cols && ci.mf > 0) ? (ci.mf >= 10 ? ci.mf : ((ci.mf + 1) & ~1)) : 0;  // 0: idle warp
-      const volatile GemmSeg* vs = segs + ci.seg0;
-      for (int s = 0; s < ci.nseg; ++s) nch += (vs[s].A.cols + BK - 1) / BK;
       const int64_t rstep = 8 * ci.irs;
 #pragma unroll
       for (int fn = 0; fn < 2; ++fn)
@@ -324,9 +357,14 @@ __global__ void __launch_bounds__(NT, 1) gemm_p8_kernel(const GemmJob* __restric
           }
         }
     }
+    if (nch == 0) {  // the announcing stage carried no data
+      __syncwarp();
+      if (lane == 0) mb_arrive(&sm.empty[st]);
+      ++gc;
+    }
     for (int ch = 0; ch < nch; ++ch, ++gc) {
-      const int st = gc % NS;
-      mb_wait(&sm.full[st], (gc / NS) & 1);
+      st = gc % NS;
+      if (ch > 0) mb_wait(&sm.full[st], (gc / NS) & 1);
       if (mfc > 0) {
         const Meta me = sm.meta[st];
         const unsigned sAm = me.a_kmajor ? SK : 1, sAk = me.a_kmajor ? 1 : SAM;
@@ -381,7 +419,7 @@ int gemm_p8_row_end(int rows, int tm) {
 }
 
 void launch_gemm_p8(const GemmJob* jobs, const GemmSeg* segs, const GemmTile* tiles, int ntiles,
-                    cudaStream_t st) {
+                    int* counter, cudaStream_t st) {
   if (ntiles <= 0) return;
   static int sms = 0;
   if (!sms) {
@@ -392,7 +430,7 @@ void launch_gemm_p8(const GemmJob* jobs, const GemmSeg* segs, const GemmTile* ti
   }
   const int smem = int(sizeof(p8::Smem));
   smem_attr((const void*)p8::gemm_p8_kernel, smem, "gemm_p8 smem attribute");
-  p8::gemm_p8_kernel<<<ntiles < sms ? ntiles : sms, p8::NT, smem, st>>>(jobs, segs, tiles, ntiles);
+  p8::gemm_p8_kernel<<<ntiles < sms ? ntiles : sms, p8::NT, smem, st>>>(jobs, segs, tiles, ntiles, counter);
 }
 
 }  // namespace h2g

@@ -56,8 +56,9 @@ int gemm_p8_row_tiles(int rows);
 int gemm_p8_col_tiles(int cols);
 int gemm_p8_tile_cols();
 int gemm_p8_row_end(int rows, int tm);  // one past the last row of row tile tm
+// counter: a zeroed device integer of this launch's own (dynamic tile hand-out).
 void launch_gemm_p8(const GemmJob* jobs, const GemmSeg* segs, const GemmTile* tiles, int ntiles,
-                    cudaStream_t st);
+                    int* counter, cudaStream_t st);
 
 // ---- batched kernel-block evaluation (k_eval.cu) ---------------------------
 // out(i, j) = K(x[rb + i], x[cb + j]) (assemble_block, kernels.cpp:242-268).
