@@ -16,7 +16,7 @@
 // (a = +0, b = -0) as in k_gemm.cu, so every C element sees the reference's
 // c = fma(a, alpha*b, c) sequence (linalg.cpp:17-62).
 //
-// Structure: one CTA per SM, looping over tiles (static round-robin). 4
+// Structure: one CTA per SM, taking tiles from a per-launch ticket. 4
 // producer warps copy operand chunks of BK = 32 with 16-byte cp.async along
 // whichever direction is contiguous in HBM, into a 3-stage ring whose layout
 // (k-major or m/n-major, both conflict-free for the fragment loads) is
