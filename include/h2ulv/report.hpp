@@ -45,6 +45,7 @@ struct RunConfig {
   // B200 extensions: member-panel QR mode and the assembly (FactorOptions).
   int b200_qr_mode = 0;
   bool b200_reference_compat = true;
+  int64_t b200_sample_cols = 0;
 
   AdmissibilityKind effective_admissibility() const {
     if (admissibility) return *admissibility;
@@ -290,6 +291,7 @@ class Pipeline {
     o.absorb_coupling = cfg_.absorb_coupling;
     o.b200_qr_mode = cfg_.b200_qr_mode;
     o.b200_reference_compat = cfg_.b200_reference_compat;
+    o.b200_sample_cols = cfg_.b200_sample_cols;
     if (o.variant == FactorVariant::h2dep)
       throw std::invalid_argument("config: the dep variant is not on the B200 path (sequential driver)");
     return o;

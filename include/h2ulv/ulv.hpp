@@ -52,6 +52,7 @@ struct FactorOptions {
   // 2 compressed) and the reference's assembly bit for bit (1) or corrected (0).
   int b200_qr_mode = 0;
   bool b200_reference_compat = true;
+  int64_t b200_sample_cols = 0;  // h2g_set_sampling: 0 = the reference's full far-field members
 };
 
 struct ClusterFactors {
@@ -132,6 +133,7 @@ inline void apply_options(Device& d, const FactorOptions& o) {
   op.qr_mode = o.b200_qr_mode;
   op.reference_compat = o.b200_reference_compat ? 1 : 0;
   check(h2g_set_options(d.handle->p, &op));
+  check(h2g_set_sampling(d.handle->p, o.b200_sample_cols));
 }
 
 inline LuFactors read_lu(h2g_problem* p, int li, int which, int64_t k) {
