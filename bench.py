@@ -220,10 +220,35 @@ def run_b200_arm(args):
     partitioned = world > 1 and not args.replicas
     qr_mode = args.qr_mode
     comm = None
+    partition_fallback = None
     if partitioned:
-        uid = [h2.nccl_unique_id() if rank == 0 else None]
-        torch.distributed.broadcast_object_list(uid, src=0)
-        comm = h2.Comm.nccl(world, rank, uid[0])
+        # The partitioned path has only ever run over a host (gloo) transport here
+        # (one GPU per run): create the NCCL communicator and push one small
+        # partitioned factorization through it first; if that fails on any rank,
+        # every rank falls back to independent replicas and the line says so.
+        ok = 1
+        try:
+            uid = [h2.nccl_unique_id() if rank == 0 else None]
+            torch.distributed.broadcast_object_list(uid, src=0)
+            comm = h2.Comm.nccl(world, rank, uid[0])
+            px, pq = make_points(8192, 42)
+            pp = h2.Problem()
+            pp.set_kernel("yukawa", WORKLOAD["alpha_m"], WORKLOAD["scale"], WORKLOAD["reg"])
+            pp.set_options(tol=WORKLOAD["tol"], cap=WORKLOAD["cap"], eta=WORKLOAD["eta"], qr_mode=qr_mode,
+                           reference_compat=args.compat)
+            pp.set_comm(comm)
+            pp.build(px, pq, leaf)
+            pp.factor()
+            pp.close()
+        except Exception as e:  # noqa: BLE001 - any failure means "do not use this path"
+            ok = 0
+            partition_fallback = f"{type(e).__name__}: {e}"[:200]
+        flag = torch.tensor([ok], device="cuda", dtype=torch.int32)
+        torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            partitioned = False
+            comm = None
+            partition_fallback = partition_fallback or "the partitioned probe failed on another rank"
     seed = 42 if partitioned else 42 + rank
     xyz, q = make_points(n, seed)
     d_xyz = torch.from_numpy(np.ascontiguousarray(xyz)).cuda()
@@ -506,8 +531,9 @@ def run_b200_arm(args):
             "data": "synthetic (seeded Fibonacci-lattice sphere, seed 42" + ("" if partitioned else "+rank") + ")",
             "config": dict(WORKLOAD, n=n, qr_mode=qr_mode, reference_compat=compat,
                            rhs="SplitMix64(7).next_signed()",
-                           parallelism=(f"box-partitioned x{world} (NCCL all-gather of bases)" if partitioned
-                                        else f"replica x{world}"),
+                           parallelism=(f"box-partitioned x{world} (NCCL all-gather of stage outputs)" if partitioned
+                                        else f"replica x{world}" + (f" (partitioned path unavailable: {partition_fallback})"
+                                                                    if partition_fallback else "")),
                            l2="inputs larger than L2 (near-field arena and member panels are GBs)"),
             "phase_s_per_step": t_phase,
             "factor_points_per_s": n / t_phase["factor"],
