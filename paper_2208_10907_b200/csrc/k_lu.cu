@@ -3,6 +3,7 @@
 // sees the reference's exact rounding sequence (linalg.cpp:352-559), so the
 // packed factors and solutions are bitwise equal to the reference.
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.hpp"
 
@@ -99,6 +100,111 @@ __global__ void __launch_bounds__(NT, 2) lu_kernel(const LuJob* __restrict__ job
       const double u = M.at(k, j);
       for (int i = k + 1 + lane; i < n; i += 32) M.at(i, j) = fma(-lcol[i], u, M.at(i, j));
     }
+    __syncthreads();
+  }
+}
+
+// ---- blocked LU inside one CTA (medium blocks) ------------------------------
+// The same right-looking order as lu_kernel, with the trailing update delayed
+// by panels of FNB columns (exactly the scheme of the multi-kernel blocked LU
+// below, fused into one CTA per block so a batch of leaf blocks costs no extra
+// launches): per panel, (A) the panel's columns are factored step by step
+// (pivot search, full-row swap, scaling, rank-1 updates inside the panel),
+// (B) the panel rows of the columns to the right receive the panel's
+// unit-lower steps, (C) the trailing block gets its FNB updates per element
+// from shared-memory copies of L21 and U12. Every element still receives
+// fma(-l_ik, u_kj, a_ij) in ascending k: bitwise equal to lu_kernel. The
+// trailing block is read and written once per panel instead of once per step.
+constexpr int FNB = 16;
+__global__ void __launch_bounds__(NT, 1) lu_fused_kernel(const LuJob* __restrict__ jobs, ErrWord* err, int tag) {
+  __shared__ ValIdx red[32];
+  extern __shared__ double fsm[];
+  const LuJob job = jobs[blockIdx.x];
+  const Mat M = job.A;
+  const int n = M.rows;
+  double* lcol = fsm;                 // n
+  double* Lp = lcol + n;              // FNB x n   (k-major: Lp[kk * n + i])
+  double* Up = Lp + size_t(FNB) * n;  // FNB x n   (Up[kk * n + j])
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = NT / 32;
+  for (int i = threadIdx.x; i < n; i += NT) job.perm[i] = i;
+  ValIdx am{0.0, 0};
+  for (int j = warp; j < n; j += nwarp)
+    for (int i = lane; i < n; i += 32) {
+      const double v = fabs(M.at(i, j));
+      if (v > am.v) am.v = v;
+    }
+  const double amax = block_argmax(am, red).v;
+  for (int kb = 0; kb < n; kb += FNB) {
+    const int nb = min(FNB, n - kb);
+    // (A) panel columns [kb, kb + nb)
+    for (int k = kb; k < kb + nb; ++k) {
+      ValIdx best{-1.0, 0x7fffffff};
+      for (int i = k + threadIdx.x; i < n; i += NT) best = better(best, ValIdx{fabs(M.at(i, k)), i});
+      best = block_argmax(best, red);
+      if (best.v <= job.tol * amax) {
+        if (threadIdx.x == 0) raise_err(err, 2, blockIdx.x, k, tag);
+        return;
+      }
+      const int p = best.i;
+      if (p != k) {
+        for (int j = threadIdx.x; j < n; j += NT) {
+          const double t = M.at(k, j);
+          M.at(k, j) = M.at(p, j);
+          M.at(p, j) = t;
+        }
+        if (threadIdx.x == 0) {
+          const int64_t t = job.perm[k];
+          job.perm[k] = job.perm[p];
+          job.perm[p] = t;
+        }
+        __syncthreads();
+      }
+      const double inv = 1.0 / M.at(k, k);
+      for (int i = k + 1 + threadIdx.x; i < n; i += NT) {
+        const double l = M.at(i, k) * inv;
+        M.at(i, k) = l;
+        lcol[i] = l;
+      }
+      __syncthreads();
+      for (int j = k + 1 + warp; j < kb + nb; j += nwarp) {
+        const double u = M.at(k, j);
+        for (int i = k + 1 + lane; i < n; i += 32) M.at(i, j) = fma(-lcol[i], u, M.at(i, j));
+      }
+      __syncthreads();
+    }
+    const int c0 = kb + nb, r = n - c0;
+    if (r <= 0) break;
+    // (B) panel rows of the columns to the right: one thread per column, k ascending
+    for (int j = c0 + threadIdx.x; j < n; j += NT) {
+      double x[FNB];
+#pragma unroll
+      for (int i = 0; i < FNB; ++i) x[i] = i < nb ? M.at(kb + i, j) : 0.0;
+#pragma unroll
+      for (int kk = 0; kk < FNB; ++kk) {
+        const double u = x[kk];
+#pragma unroll
+        for (int i = kk + 1; i < FNB; ++i)
+          if (i < nb) x[i] = fma(-M.at(kb + i, kb + kk), u, x[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < FNB; ++i)
+        if (i < nb) {
+          M.at(kb + i, j) = x[i];
+          Up[i * n + (j - c0)] = x[i];
+        }
+    }
+    for (int e = threadIdx.x; e < nb * r; e += NT) {
+      const int kk = e / r, i = e % r;
+      Lp[kk * n + i] = M.at(c0 + i, kb + kk);
+    }
+    __syncthreads();
+    // (C) trailing block: nb ordered updates per element
+    for (int j = warp; j < r; j += nwarp)
+      for (int i = lane; i < r; i += 32) {
+        double v = M.at(c0 + i, c0 + j);
+        for (int kk = 0; kk < nb; ++kk) v = fma(-Lp[kk * n + i], Up[kk * n + j], v);
+        M.at(c0 + i, c0 + j) = v;
+      }
     __syncthreads();
   }
 }
@@ -591,9 +697,17 @@ void launch_lu_rows(const LuJob* jobs, int njobs, int max_n, int kb, int nb, cud
 }
 
 void launch_lu(const LuJob* jobs, int njobs, int max_n, ErrWord* err, int tag, cudaStream_t st) {
+  if (njobs <= 0) return;
+  static const bool unfused = getenv("H2G_LU_UNFUSED") != nullptr;
+  const size_t fsmem = sizeof(double) * size_t(max_n > 0 ? max_n : 1) * (1 + 2 * FNB);
+  if (!unfused && max_n >= 48 && fsmem <= size_t(200) << 10) {
+    smem_attr((const void*)lu_fused_kernel, fsmem, "lu_fused smem attribute");
+    lu_fused_kernel<<<njobs, NT, fsmem, st>>>(jobs, err, tag);
+    return;
+  }
   const size_t smem = sizeof(double) * size_t(max_n > 0 ? max_n : 1);
   smem_attr((const void*)lu_kernel, smem, "lu smem attribute");
-  if (njobs > 0) lu_kernel<<<njobs, NT, smem, st>>>(jobs, err, tag);
+  lu_kernel<<<njobs, NT, smem, st>>>(jobs, err, tag);
 }
 
 int solve_chunk_width(int m) {
