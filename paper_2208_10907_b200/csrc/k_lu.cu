@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(NT, 2) lu_kernel(const LuJob* __restrict__ job
 // trailing block is read and written once per panel instead of once per step.
 constexpr int FNB = 16;
 __global__ void __launch_bounds__(NT, 1) lu_fused_kernel(const LuJob* __restrict__ jobs, ErrWord* err, int tag) {
-  __shared__ ValIdx red[32];
+  __shared__ ValIdx red[32 + FNB];  // reduction scratch + the panel's pivots
   extern __shared__ double fsm[];
   const LuJob job = jobs[blockIdx.x];
   const Mat M = job.A;
@@ -136,42 +136,72 @@ __global__ void __launch_bounds__(NT, 1) lu_fused_kernel(const LuJob* __restrict
   const double amax = block_argmax(am, red).v;
   for (int kb = 0; kb < n; kb += FNB) {
     const int nb = min(FNB, n - kb);
-    // (A) panel columns [kb, kb + nb)
+    // (A) panel columns [kb, kb + nb), factored in shared memory: Lp holds the
+    // panel's rows kb.. (column c at Lp[c * n + (i - kb)]); the row
+    // interchanges are applied to the panel at once and to every other column
+    // of the block after the panel (a permutation commutes with the delayed
+    // updates: a row's values and multipliers still move together).
+    const int pr = n - kb;
+    for (int e = threadIdx.x; e < nb * pr; e += NT) {
+      const int cc = e / pr, i = e % pr;
+      Lp[cc * n + i] = M.at(kb + i, kb + cc);
+    }
+    __syncthreads();
+    int* piv = reinterpret_cast<int*>(red + 32);  // FNB pivots (shared, after the reduction scratch)
     for (int k = kb; k < kb + nb; ++k) {
+      const int kc = k - kb;
+      double* colk = Lp + kc * n;
       ValIdx best{-1.0, 0x7fffffff};
-      for (int i = k + threadIdx.x; i < n; i += NT) best = better(best, ValIdx{fabs(M.at(i, k)), i});
+      for (int i = kc + threadIdx.x; i < pr; i += NT) best = better(best, ValIdx{fabs(colk[i]), kb + i});
       best = block_argmax(best, red);
       if (best.v <= job.tol * amax) {
         if (threadIdx.x == 0) raise_err(err, 2, blockIdx.x, k, tag);
         return;
       }
       const int p = best.i;
+      if (threadIdx.x == 0) piv[kc] = p;
       if (p != k) {
-        for (int j = threadIdx.x; j < n; j += NT) {
-          const double t = M.at(k, j);
-          M.at(k, j) = M.at(p, j);
-          M.at(p, j) = t;
+        if (threadIdx.x < nb) {
+          double* cc = Lp + threadIdx.x * n;
+          const double t = cc[kc];
+          cc[kc] = cc[p - kb];
+          cc[p - kb] = t;
         }
         if (threadIdx.x == 0) {
           const int64_t t = job.perm[k];
           job.perm[k] = job.perm[p];
           job.perm[p] = t;
         }
-        __syncthreads();
-      }
-      const double inv = 1.0 / M.at(k, k);
-      for (int i = k + 1 + threadIdx.x; i < n; i += NT) {
-        const double l = M.at(i, k) * inv;
-        M.at(i, k) = l;
-        lcol[i] = l;
       }
       __syncthreads();
-      for (int j = k + 1 + warp; j < kb + nb; j += nwarp) {
-        const double u = M.at(k, j);
-        for (int i = k + 1 + lane; i < n; i += 32) M.at(i, j) = fma(-lcol[i], u, M.at(i, j));
+      const double inv = 1.0 / colk[kc];
+      __syncthreads();
+      for (int i = kc + 1 + threadIdx.x; i < pr; i += NT) colk[i] = colk[i] * inv;
+      __syncthreads();
+      for (int j = kc + 1 + warp; j < nb; j += nwarp) {
+        double* colj = Lp + j * n;
+        const double u = colj[kc];
+        for (int i = kc + 1 + lane; i < pr; i += 32) colj[i] = fma(-colk[i], u, colj[i]);
       }
       __syncthreads();
     }
+    // panel back to the block; its interchanges on every other column, in order
+    for (int e = threadIdx.x; e < nb * pr; e += NT) {
+      const int cc = e / pr, i = e % pr;
+      M.at(kb + i, kb + cc) = Lp[cc * n + i];
+    }
+    for (int j = threadIdx.x; j < n; j += NT) {
+      if (j >= kb && j < kb + nb) continue;
+      for (int kc = 0; kc < nb; ++kc) {
+        const int p = piv[kc];
+        if (p != kb + kc) {
+          const double t = M.at(kb + kc, j);
+          M.at(kb + kc, j) = M.at(p, j);
+          M.at(p, j) = t;
+        }
+      }
+    }
+    __syncthreads();
     const int c0 = kb + nb, r = n - c0;
     if (r <= 0) break;
     // (B) panel rows of the columns to the right: one thread per column, k ascending
