@@ -1418,10 +1418,17 @@ struct Driver {
           } else {
             // P's content over J's columns from every target of P overlapping J
             // (oracle/fix_reference.py fix 3); the rest are P's near columns.
-            zb.zero(mats[t].m);
-            for (auto& o : overlapping(stack[Pp], tk))
+            // (only the columns no target covers are zero-filled, not the whole block)
+            auto ov = overlapping(stack[Pp], tk);
+            std::sort(ov.begin(), ov.end(), [](const Overlap& a, const Overlap& b) { return a.dst < b.dst; });
+            int at = 0;
+            for (auto& o : ov) {
+              if (o.dst > at) zb.zero(mats[t].m.sub(0, at, mats[t].rows(), o.dst - at));
               cb.copy(mats[t].m.sub(0, o.dst, mats[t].rows(), o.len),
                       stack[Pp].at(o.tk).m.sub(0, o.src, mats[t].rows(), o.len));
+              at = std::max(at, o.dst + o.len);
+            }
+            if (at < mats[t].cols()) zb.zero(mats[t].m.sub(0, at, mats[t].rows(), mats[t].cols() - at));
           }
           if (opt.reference_compat)
             for (auto& r : gmasks[t]) zb.zero(mats[t].m.sub(0, r.x, mats[t].rows(), r.y - r.x));
