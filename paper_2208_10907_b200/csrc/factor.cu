@@ -1031,6 +1031,10 @@ struct Driver {
       std::map<std::pair<int64_t, int>, int> off;  // (box, masked) -> row offset
       std::vector<std::pair<int64_t, int>> order;  // row blocks in layout order
       std::vector<size_t> jobs;                     // indices into pkeys
+      // neighbour p -> which block its term reads: 1 = the masked copy, 0 = the
+      // unmasked block (p has no near column inside the target, so the two are
+      // the same values and one evaluation serves both), -1 = all zero (skipped)
+      std::map<int64_t, int> nb;
     };
     std::map<TargetKey, size_t> at;
     std::vector<Plan> plans;
@@ -1058,9 +1062,13 @@ struct Driver {
         for (int64_t x = 0; x < S.nnear(L, cc); ++x) {
           const int64_t p = S.near(L, cc)[x];
           if (p == cc) continue;
-          bool all_zero;
-          mask_for(L, p, pl.jb, pl.jb + pl.w, all_zero);
-          if (!all_zero) add_rows(pl, p, 1);
+          auto known = pl.nb.find(p);
+          if (known == pl.nb.end()) {
+            bool all_zero;
+            const auto mk = mask_for(L, p, pl.jb, pl.jb + pl.w, all_zero);
+            known = pl.nb.emplace(p, all_zero ? -1 : (mk.empty() ? 0 : 1)).first;
+          }
+          if (known->second >= 0) add_rows(pl, p, known->second);
         }
     }
     const size_t fr = c.free_bytes();
@@ -1108,8 +1116,10 @@ struct Driver {
           if (Ub[cc].rank > 0 && sys.offdiag)
             for (int64_t x = 0; x < S.nnear(L, cc); ++x) {
               const int64_t p = S.near(L, cc)[x];
-              if (p == cc || !pl.off.count({p, 1})) continue;
-              gb.seg(qcm.at({cc, p}).m, rows_of(p, 1), -1.0);
+              if (p == cc) continue;
+              const auto nbp = pl.nb.find(p);
+              if (nbp == pl.nb.end() || nbp->second < 0) continue;
+              gb.seg(qcm.at({cc, p}).m, rows_of(p, nbp->second), -1.0);
             }
         }
       }
