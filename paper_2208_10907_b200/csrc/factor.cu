@@ -1073,6 +1073,37 @@ struct Driver {
     }
     const size_t fr = c.free_bytes();
     const size_t budget = std::max<size_t>(size_t(1) << 28, fr / 3);
+    // Equal charges: A(I, c)^T == A(c, I) bit for bit, so the first transfer
+    // level's ancestor-partner column members (A(I, c) Vs_c)^T = Vs_c^T A(c, I)
+    // are plain GEMMs on the kernel blocks materialised here for the pieces
+    // (same operands, same k order as the kernel-generated GEMM of
+    // build_transfers, which they replace: 71 ms at 11 TF/s at the bench size).
+    // leaf_cols_[c]: r_c x (widths of ancestor_far_partners(L - 1, c >> 1)).
+    leaf_cols_.clear();
+    std::map<std::pair<int64_t, TargetKey>, Mat> leaf_col_dst;
+    if (P.uniform_q && opt.sample_cols <= 0 && L >= 3 && getenv("H2G_NO_LEAF_COLS") == nullptr) {
+      const auto& Vb = P.V[L];
+      std::vector<std::pair<int, int>> shp;
+      size_t need = 0;
+      const int64_t mleaf = int64_t(1) << L;
+      for (int64_t cc = 0; cc < mleaf; ++cc) {
+        int w = 0;
+        for (auto [l2, I] : ancestor_far_partners(L - 1, cc >> 1)) w += int(rs(l2, I));
+        shp.push_back({Vb[cc].rank, w});
+        need += sizeof(double) * size_t(Vb[cc].rank) * size_t(w);
+      }
+      if (need < fr / 4) {
+        leaf_cols_ = alloc_mats(c, shp);
+        for (int64_t cc = lo; cc < hi; ++cc) {
+          int off = 0;
+          for (auto [l2, I] : ancestor_far_partners(L - 1, cc >> 1)) {
+            const int w = int(rs(l2, I));
+            leaf_col_dst[{cc, TargetKey{l2, I}}] = leaf_cols_[size_t(cc)].m.sub(0, off, Vb[cc].rank, w);
+            off += w;
+          }
+        }
+      }
+    }
     size_t p0 = 0;
     while (p0 < plans.size()) {
       size_t p1 = p0, bytes = 0;
@@ -1121,12 +1152,22 @@ struct Driver {
               if (nbp == pl.nb.end() || nbp->second < 0) continue;
               gb.seg(qcm.at({cc, p}).m, rows_of(p, nbp->second), -1.0);
             }
+          const auto lc = leaf_col_dst.find({cc, pl.tk});
+          if (lc != leaf_col_dst.end() && lc->second.rows > 0)
+            gemm1(gb, lc->second, P.V[L][cc].Qs().t(), rows_of(cc, 0));
         }
       }
       gb.run(c);
       p0 = p1;  // B is freed (stream-ordered) when it goes out of scope
     }
+    if (!leaf_cols_.empty()) {  // multi-GPU: every rank needs every leaf's members
+      std::vector<int64_t> box;
+      for (int64_t cc = 0; cc < (int64_t(1) << L); ++cc) box.push_back(cc);
+      exchange_mats(leaf_cols_, box, int64_t(1) << L);
+    }
   }
+  // First transfer level's ancestor-partner column members per leaf (see above).
+  std::vector<DMat> leaf_cols_;
 
   // ---- build_leaf_pieces (ulv.cpp:336-401) -----------------------------------
   void build_leaf_pieces(SysL& sys, const FillSet& fills, std::vector<PieceMap>& pieces,
@@ -1600,6 +1641,14 @@ struct Driver {
                   const Mat v0 = Vbig[2 * k], v1 = Vbig[2 * k + 1];
                   if (!keepm.empty() && anc_w[k] > 0 && sys.dims[k] > 0)
                     kb.copy(keepm[k].m, cols[k].slice(anc_off[k], anc_w[k]));
+                  if (lvl + 1 == L && int64_t(leaf_cols_.size()) == 2 * m && opt.sample_cols <= 0) {
+                    // children are leaves: their members were formed beside the leaf pieces
+                    const Mat dst = cols[k].slice(off, anc_w[k]);
+                    if (v0.cols > 0 && anc_w[k] > 0) cb.copy(dst.sub(0, 0, v0.cols, anc_w[k]), leaf_cols_[2 * k].m);
+                    if (v1.cols > 0 && anc_w[k] > 0)
+                      cb.copy(dst.sub(v0.cols, 0, v1.cols, anc_w[k]), leaf_cols_[2 * k + 1].m);
+                    continue;
+                  }
                   if (nest && prev_cols_[2 * k].m.p && prev_cols_[2 * k + 1].m.p) {
                     // prev_cols_[c]: c's ancestor members of the finer level, in
                     // ancestor_far_partners(lvl + 1, c) order = far(lvl, k), then anc.
@@ -1647,6 +1696,7 @@ struct Driver {
       exchange_mats(keepm, box, m);
     }
     prev_cols_ = std::move(keepm);
+    if (lvl + 1 == L) leaf_cols_.clear();
   }
   // Transfer stage, tolerance modes: per box of the previous (finer) transfer
   // level, its ancestor-partner column members (dims x sum of sampled widths).
