@@ -1081,14 +1081,14 @@ struct Driver {
     // leaf_cols_[c]: r_c x (widths of ancestor_far_partners(L - 1, c >> 1)).
     leaf_cols_.clear();
     std::map<std::pair<int64_t, TargetKey>, Mat> leaf_col_dst;
-    if (P.uniform_q && opt.sample_cols <= 0 && L >= 3 && getenv("H2G_NO_LEAF_COLS") == nullptr) {
+    if (P.uniform_q && L >= 3 && getenv("H2G_NO_LEAF_COLS") == nullptr) {
       const auto& Vb = P.V[L];
       std::vector<std::pair<int, int>> shp;
       size_t need = 0;
       const int64_t mleaf = int64_t(1) << L;
       for (int64_t cc = 0; cc < mleaf; ++cc) {
         int w = 0;
-        for (auto [l2, I] : ancestor_far_partners(L - 1, cc >> 1)) w += int(rs(l2, I));
+        for (auto [l2, I] : ancestor_far_partners(L - 1, cc >> 1)) w += samp(rs(l2, I)).count;
         shp.push_back({Vb[cc].rank, w});
         need += sizeof(double) * size_t(Vb[cc].rank) * size_t(w);
       }
@@ -1097,7 +1097,7 @@ struct Driver {
         for (int64_t cc = lo; cc < hi; ++cc) {
           int off = 0;
           for (auto [l2, I] : ancestor_far_partners(L - 1, cc >> 1)) {
-            const int w = int(rs(l2, I));
+            const int w = samp(rs(l2, I)).count;  // (sampled members: the same strided columns)
             leaf_col_dst[{cc, TargetKey{l2, I}}] = leaf_cols_[size_t(cc)].m.sub(0, off, Vb[cc].rank, w);
             off += w;
           }
@@ -1154,7 +1154,7 @@ struct Driver {
             }
           const auto lc = leaf_col_dst.find({cc, pl.tk});
           if (lc != leaf_col_dst.end() && lc->second.rows > 0)
-            gemm1(gb, lc->second, P.V[L][cc].Qs().t(), rows_of(cc, 0));
+            gemm1(gb, lc->second, P.V[L][cc].Qs().t(), sample_cols_view(rows_of(cc, 0), samp(pl.w)));
         }
       }
       gb.run(c);
@@ -1641,7 +1641,7 @@ struct Driver {
                   const Mat v0 = Vbig[2 * k], v1 = Vbig[2 * k + 1];
                   if (!keepm.empty() && anc_w[k] > 0 && sys.dims[k] > 0)
                     kb.copy(keepm[k].m, cols[k].slice(anc_off[k], anc_w[k]));
-                  if (lvl + 1 == L && int64_t(leaf_cols_.size()) == 2 * m && opt.sample_cols <= 0) {
+                  if (lvl + 1 == L && int64_t(leaf_cols_.size()) == 2 * m) {
                     // children are leaves: their members were formed beside the leaf pieces
                     const Mat dst = cols[k].slice(off, anc_w[k]);
                     if (v0.cols > 0 && anc_w[k] > 0) cb.copy(dst.sub(0, 0, v0.cols, anc_w[k]), leaf_cols_[2 * k].m);
