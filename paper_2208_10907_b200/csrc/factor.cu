@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <functional>
+#include <future>
 #include <set>
 #include <stdexcept>
 
@@ -1019,23 +1020,28 @@ struct Driver {
   // once per (c, p, J), ~26 times at the bench size). Targets are processed
   // in chunks under a memory budget. Same values (one kernel_pair per entry,
   // masked entries +0), same segments in the same order: bit-identical pieces.
-  void leaf_pieces_materialized(SysL& sys, const std::vector<std::pair<int64_t, TargetKey>>& pkeys,
-                                const std::vector<DMat>& mats, const std::map<int64_t, DMat>& usT,
-                                const std::map<std::pair<int64_t, int64_t>, DMat>& qcm, int64_t lo,
-                                int64_t hi) {
-    const auto& Ub = P.U[L];
-    struct Plan {
-      TargetKey tk;
-      int64_t jb = 0;
-      int w = 0, rows = 0;
-      std::map<std::pair<int64_t, int>, int> off;  // (box, masked) -> row offset
-      std::vector<std::pair<int64_t, int>> order;  // row blocks in layout order
-      std::vector<size_t> jobs;                     // indices into pkeys
-      // neighbour p -> which block its term reads: 1 = the masked copy, 0 = the
-      // unmasked block (p has no near column inside the target, so the two are
-      // the same values and one evaluation serves both), -1 = all zero (skipped)
-      std::map<int64_t, int> nb;
-    };
+  struct Plan {
+    TargetKey tk;
+    int64_t jb = 0;
+    int w = 0, rows = 0;
+    std::map<std::pair<int64_t, int>, int> off;  // (box, masked) -> row offset
+    std::vector<std::pair<int64_t, int>> order;  // row blocks in layout order
+    std::vector<size_t> jobs;                     // indices into pkeys
+    // neighbour p -> which block its term reads: 1 = the masked copy, 0 = the
+    // unmasked block (p has no near column inside the target, so the two are
+    // the same values and one evaluation serves both), -1 = all zero (skipped)
+    std::map<int64_t, int> nb;
+  };
+  // pkeys of build_leaf_pieces: (box, target) in box order, targets_of order.
+  std::vector<std::pair<int64_t, TargetKey>> leaf_piece_keys() const {
+    std::vector<std::pair<int64_t, TargetKey>> pkeys;
+    for (int64_t cc = 0; cc < (int64_t(1) << L); ++cc)
+      for (auto& tk : targets_of(L, cc)) pkeys.push_back({cc, tk});
+    return pkeys;
+  }
+  // positive: per box, rank > 0 (nullptr: assume so). Reads the integer structure only.
+  std::vector<Plan> make_leaf_plans(const std::vector<std::pair<int64_t, TargetKey>>& pkeys, bool offdiag,
+                                    int64_t lo, int64_t hi, const std::vector<char>* positive) const {
     std::map<TargetKey, size_t> at;
     std::vector<Plan> plans;
     auto add_rows = [&](Plan& pl, int64_t box, int masked) {
@@ -1058,7 +1064,7 @@ struct Driver {
       Plan& pl = plans[it->second];
       pl.jobs.push_back(t);
       add_rows(pl, cc, 0);
-      if (Ub[cc].rank > 0 && sys.offdiag)
+      if ((!positive || (*positive)[size_t(cc)]) && offdiag)
         for (int64_t x = 0; x < S.nnear(L, cc); ++x) {
           const int64_t p = S.near(L, cc)[x];
           if (p == cc) continue;
@@ -1070,6 +1076,30 @@ struct Driver {
           }
           if (known->second >= 0) add_rows(pl, p, known->second);
         }
+    }
+    return plans;
+  }
+  std::future<std::vector<Plan>> leaf_plan_future_;
+
+  void leaf_pieces_materialized(SysL& sys, const std::vector<std::pair<int64_t, TargetKey>>& pkeys,
+                                const std::vector<DMat>& mats, const std::map<int64_t, DMat>& usT,
+                                const std::map<std::pair<int64_t, int64_t>, DMat>& qcm, int64_t lo,
+                                int64_t hi) {
+    const auto& Ub = P.U[L];
+    // The plans depend on the integer structure only (given that every own box
+    // has a nonzero rank): Driver::run starts computing them on a host thread
+    // while the fills and the bases keep the device busy.
+    bool ranks_ok = true;
+    for (int64_t cc = lo; cc < hi; ++cc) ranks_ok = ranks_ok && Ub[cc].rank > 0;
+    std::vector<Plan> plans;
+    if (leaf_plan_future_.valid()) {
+      plans = leaf_plan_future_.get();
+      if (!ranks_ok) plans.clear();
+    }
+    if (plans.empty()) {
+      std::vector<char> pos(size_t(sys.m));
+      for (int64_t cc = 0; cc < sys.m; ++cc) pos[size_t(cc)] = Ub[cc].rank > 0;
+      plans = make_leaf_plans(pkeys, sys.offdiag, lo, hi, &pos);
     }
     const size_t fr = c.free_bytes();
     const size_t budget = std::max<size_t>(size_t(1) << 28, fr / 3);
@@ -2123,6 +2153,13 @@ struct Driver {
     for (int l = 0; l <= L; ++l) {
       P.U[l].resize(size_t(1) << l);
       P.V[l].resize(size_t(1) << l);
+    }
+    if (getenv("H2G_LEAF_GEN") == nullptr) {
+      const auto [plo, phi] = own_range(sys.m);
+      const bool offdiag = sys.offdiag;
+      leaf_plan_future_ = std::async(std::launch::async, [this, plo = plo, phi = phi, offdiag] {
+        return make_leaf_plans(leaf_piece_keys(), offdiag, plo, phi, nullptr);
+      });
     }
     // prepare_factor_inputs (ulv.cpp:1108-1126)
     FillSet fills;
