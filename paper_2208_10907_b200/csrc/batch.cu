@@ -131,6 +131,26 @@ void Ctx::prof_resolve() {
   prec.clear();
 }
 
+char* Ctx::stage_reserve(size_t bytes) {
+  if (!pin) {
+    pin_cap = size_t(64) << 20;
+    if (cudaMallocHost(&pin, pin_cap) != cudaSuccess) {
+      cudaGetLastError();
+      pin = nullptr;
+      pin_cap = 0;
+    }
+  }
+  const size_t need = (bytes + 255) & ~size_t(255);
+  if (!pin || need > pin_cap) return nullptr;
+  if (pin_head + need > pin_cap) {
+    cuda_check(cudaStreamSynchronize(stream), "stage sync");
+    pin_head = 0;
+  }
+  char* d = pin + pin_head;
+  pin_head += need;
+  return d;
+}
+
 const void* Ctx::stage(const void* src, size_t bytes) {
   if (!pin) {
     pin_cap = size_t(64) << 20;
@@ -321,14 +341,18 @@ void GemmBatch::run(Ctx& c, int tag) {
   }
   c.add_flops(fl);
   if (tiles.empty()) return;
-  Slab k1, k2, k3, k4;
-  const int2* dmask = upload(c, masks, k4);
+  Slab k1, k4;
+  const int2* dmask = masks.empty() ? nullptr : upload(c, masks, k4);  // (its address goes into the segments)
   for (size_t s = 0; s < segs.size(); ++s)
     if (segs[s].gen && seg_mask_off[s] >= 0) segs[s].g.mask = dmask + seg_mask_off[s];
   for (size_t j = 0; j < jobs.size(); ++j) jobs[j].lower = lower[j] ? 1 : 0;
-  const GemmJob* dj = upload(c, jobs, k1);
-  const GemmSeg* ds = upload(c, segs, k2);
-  const GemmTile* dt = upload(c, tiles, k3);
+  void *pj = nullptr, *ps = nullptr, *ptl = nullptr;
+  upload_parts(c, k1, {{jobs.data(), sizeof(GemmJob) * jobs.size(), &pj},
+                       {segs.data(), sizeof(GemmSeg) * segs.size(), &ps},
+                       {tiles.data(), sizeof(GemmTile) * tiles.size(), &ptl}});
+  const GemmJob* dj = static_cast<const GemmJob*>(pj);
+  const GemmSeg* ds = static_cast<const GemmSeg*>(ps);
+  const GemmTile* dt = static_cast<const GemmTile*>(ptl);
   double by = 0;
   for (auto& j : jobs) {
     by += 8.0 * j.C.rows * double(j.C.cols) * (j.acc ? 2 : 1);
@@ -406,9 +430,11 @@ void EvalBatch::run(Ctx& c, int tag) {
   c.kernel_evals += evn_;
   c.add_flops(ev_flops_);
   if (tp.back() == 0) return;
-  Slab k1, k2;
-  auto* dj = upload(c, jobs, k1);
-  auto* dtp = upload(c, tp, k2);
+  Slab k1;
+  void *pj = nullptr, *pt = nullptr;
+  upload_parts(c, k1, {{jobs.data(), sizeof(EvalJob) * jobs.size(), &pj}, {tp.data(), sizeof(int) * tp.size(), &pt}});
+  auto* dj = static_cast<const EvalJob*>(pj);
+  auto* dtp = static_cast<const int*>(pt);
   auto ev = c.prof_begin();
   launch_eval(dj, dtp, int(jobs.size()), tp.back(), c.kp, c.cloud, c.err, tag, c.stream);
   c.prof_end(c.prof_detail ? ("eval@" + c.phase).c_str() : "eval", ev, ev_flops_, 8.0 * evn_);
@@ -421,9 +447,11 @@ void CopyBatch::run(Ctx& c) {
   HostTimer ht("copy");
   const std::vector<int> tp = tiles_of(jobs, &CopyJob::dst);
   if (tp.back() == 0) return;
-  Slab k1, k2;
-  auto* dj = upload(c, jobs, k1);
-  auto* dtp = upload(c, tp, k2);
+  Slab k1;
+  void *pj = nullptr, *pt = nullptr;
+  upload_parts(c, k1, {{jobs.data(), sizeof(CopyJob) * jobs.size(), &pj}, {tp.data(), sizeof(int) * tp.size(), &pt}});
+  auto* dj = static_cast<const CopyJob*>(pj);
+  auto* dtp = static_cast<const int*>(pt);
   double by = 0;
   for (auto& j : jobs) by += 8.0 * j.dst.rows * double(j.dst.cols) * (1 + (j.src.p ? 1 : 0) + j.add);
   auto ev = c.prof_begin();

@@ -5,6 +5,8 @@
 #pragma once
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
+#include <initializer_list>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -59,6 +61,7 @@ struct Ctx {
   char* pin = nullptr;
   size_t pin_cap = 0, pin_head = 0;
   const void* stage(const void* src, size_t bytes);
+  char* stage_reserve(size_t bytes);  // a region of the staging arena to fill (nullptr: does not fit)
   // Zeroed device integers, one per launch that hands work out dynamically
   // (k_gemm8.cu): a slab of them, re-zeroed (stream-ordered) when used up.
   Slab tickets;
@@ -137,6 +140,35 @@ T* upload(Ctx& c, const std::vector<T>& v, Slab& keep) {
                              sizeof(T) * v.size(), cudaMemcpyHostToDevice, c.stream),
              "upload");
   return static_cast<T*>(keep.get());
+}
+
+// Several descriptor arrays of one launch in ONE device block and ONE copy
+// (an allocation and a cudaMemcpyAsync per array cost ~7 us of host time each,
+// four arrays per GEMM launch, ~1,100 launches per factorization).
+struct UploadPart {
+  const void* src;
+  size_t bytes;
+  void** dst;  // receives the device address (nullptr when bytes == 0)
+};
+inline void upload_parts(Ctx& c, Slab& keep, std::initializer_list<UploadPart> parts) {
+  size_t total = 0;
+  for (auto& p : parts) total += (p.bytes + 255) & ~size_t(255);
+  for (auto& p : parts) *p.dst = nullptr;
+  if (total == 0) return;
+  keep = c.alloc(total);
+  char* dev = static_cast<char*>(keep.get());
+  char* pin = c.stage_reserve(total);
+  size_t off = 0;
+  for (auto& p : parts) {
+    if (p.bytes == 0) continue;
+    *p.dst = dev + off;
+    if (pin)
+      memcpy(pin + off, p.src, p.bytes);
+    else  // larger than the staging arena: one (pageable) copy per array
+      cuda_check(cudaMemcpyAsync(dev + off, p.src, p.bytes, cudaMemcpyHostToDevice, c.stream), "upload");
+    off += (p.bytes + 255) & ~size_t(255);
+  }
+  if (pin) cuda_check(cudaMemcpyAsync(dev, pin, total, cudaMemcpyHostToDevice, c.stream), "upload");
 }
 
 // ---- GEMM -----------------------------------------------------------------
